@@ -1,0 +1,230 @@
+/*
+ * sinkr_cuda.h — C-ABI of the B200-native (sm_100a) SinkRouter decode engine.
+ *
+ * This is the drop-in boundary for the reference's C++ operator API
+ * (/root/reference/proj/include/sinkr/*.hpp).  Every entry point below names
+ * the reference interface it replaces.  Plain pointers and sizes only; no
+ * torch or C++ types cross the boundary.  A C++ shim with the reference's own
+ * signatures and exception types sits on top: include/sinkr/cuda/router.hpp.
+ *
+ * Hot path per call (one CUDA stream, captured once in a CUDA graph):
+ *   probe kernel   — cosine proxy vs. the cached token-0 key, group mean,
+ *                    tau(L) compare  -> route bitmap + compacted active list
+ *   decode kernel  — persistent Split-K flash-decode; only Active groups'
+ *                    K/V pages are streamed (TMA -> smem ring -> mma.sync
+ *                    hi/lo-split bf16, fp32 online softmax)
+ *   combine kernel — log-sum-exp merge of the Split-K partials; Sink groups get
+ *                    bitwise-zero rows.
+ *
+ * Threading: an engine is bound to one device and one stream; like the
+ * reference's ThreadPool (parallel.hpp:15-18) it must not be driven by two host
+ * threads at once.  Errors are reported as sinkr_status codes that mirror the
+ * reference's exception classes; the message of the last failing call on the
+ * calling thread is available from sinkr_last_error().
+ */
+#ifndef SINKR_CUDA_H_
+#define SINKR_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Exception classes of the reference (router.cpp:37-38,51-53,60,86-90;
+ * kv_cache.cpp:56-57,67-74,93,101,110-113; attention.cpp:15-22,187-190). */
+typedef enum sinkr_status {
+    SINKR_OK = 0,
+    SINKR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    SINKR_OUT_OF_RANGE = 2,     /* std::out_of_range     */
+    SINKR_RUNTIME_ERROR = 3,    /* std::runtime_error    */
+    SINKR_LOGIC_ERROR = 4,      /* std::logic_error      */
+    SINKR_CUDA_ERROR = 5,       /* CUDA runtime / driver failure */
+    SINKR_NO_DEVICE = 6         /* no sm_100 device: the engine never falls back to the CPU */
+} sinkr_status;
+
+typedef struct sinkr_engine sinkr_engine;
+
+/* CacheConfig (kv_cache.hpp:13-24).  num_seqs > 1 batches B independent caches
+ * (the reference realises batch as independent KvCache instances)
+ * so one launch serves all of them; 0 means 1. */
+typedef struct sinkr_cache_config {
+    size_t num_layers;
+    size_t num_q_heads;  /* H_q */
+    size_t num_kv_heads; /* H_kv */
+    size_t head_dim;     /* D: 32, 64 or 128 */
+    size_t capacity;     /* L_max tokens per (layer, seq, kv_head) slot */
+    size_t num_seqs;     /* B */
+} sinkr_cache_config;
+
+/* The part of ThresholdProfile (calibration.hpp:21-34) that routing reads. */
+typedef struct sinkr_threshold_profile {
+    double coeffs[4]; /* a, b, c, d */
+    double length_normalizer;
+    double clamp_lo;
+    double clamp_hi;
+} sinkr_threshold_profile;
+
+/* RoutingConfig (router.hpp:16-26). */
+typedef struct sinkr_routing_config {
+    double gamma; /* carried for parity; routing does not read it */
+    sinkr_threshold_profile profile;
+    const size_t* excluded_layers; /* reference default {0, 1} */
+    size_t num_excluded_layers;
+    int sink_on_tie; /* fault-injection hook: S >= tau instead of S > tau */
+} sinkr_routing_config;
+
+/* EngineOptions (router.hpp:69-76).  num_splits and block_size are validated
+ * and accepted for API parity; the GPU partitions work over its SMs itself
+ * (outputs agree within tolerance, loaded-token counts exactly).
+ * global_context_len: tau(L) uses this length when the sequence is sharded
+ * across GPUs (0 = this engine's token_count, router.cpp:89,113). */
+typedef struct sinkr_engine_options {
+    size_t num_splits;
+    size_t block_size;
+    int observe_only;
+    size_t global_context_len;
+} sinkr_engine_options;
+
+/* LoadCounters (counters.hpp:9-28).  kv_floats_loaded counts K/V ELEMENTS as
+ * the reference does (2 * rows * D per Active group), measured by the decode
+ * kernel itself; the *_seconds fields come from CUDA events. */
+typedef struct sinkr_load_counters {
+    uint64_t kv_floats_loaded;
+    uint64_t anchor_floats_loaded;
+    uint64_t groups_active;
+    uint64_t groups_skipped;
+    double routing_seconds;
+    double attention_seconds;
+    double merge_seconds;
+} sinkr_load_counters;
+
+/* GroupStepInfo + RouteDecision (router.hpp:28-39,56-61).  Head scores are
+ * returned in a separate H_q array (query-head order, router.cpp:118). */
+typedef struct sinkr_group_info {
+    size_t layer;
+    size_t kv_head;
+    double group_score;
+    double threshold;
+    int32_t sink;
+    int32_t degenerate;
+    uint64_t kv_floats_loaded;
+    uint64_t tokens_loaded; /* rows streamed by the decode kernel (the skipped-block record) */
+} sinkr_group_info;
+
+const char* sinkr_last_error(void);
+const char* sinkr_version(void);
+
+/* ---- engine / KvCache (kv_cache.hpp:42-80) --------------------------------- */
+/* KvCache::KvCache — allocates bf16 K/V [layer][seq][kv_head][capacity][D] in
+ * HBM plus the f32 anchor table; throws like CacheConfig::validate
+ * (kv_cache.cpp:32-39). */
+sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
+                                 sinkr_engine** out);
+sinkr_status sinkr_engine_destroy(sinkr_engine* engine);
+/* The engine's CUDA stream (cudaStream_t) — all work is ordered on it. */
+void* sinkr_engine_stream(sinkr_engine* engine);
+
+/* KvCache::append (kv_cache.cpp:61-84), for `rows` consecutive f32 host rows.
+ * Rows are stored as bf16 (RNE).  On a slot's first row the anchor is captured
+ * from the stored (bf16-rounded) key with the reference's rule: k0_norm =
+ * (float)sqrt(sum (double)k^2), degenerate (< 1e-12) -> RUNTIME_ERROR. */
+sinkr_status sinkr_kv_append(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                             const float* k, const float* v, size_t rows);
+/* Same, for bf16 rows already on the device (device prefill path). */
+sinkr_status sinkr_kv_append_device_bf16(sinkr_engine* e, size_t seq, size_t layer,
+                                         size_t kv_head, const void* k, const void* v,
+                                         size_t rows);
+/* Appends `rows` synthetic rows generated on the device (see
+ * oracle/sinkr_oracle.c:orc_fill_rows for the bit-identical CPU restatement):
+ * value(row, j) = bf16(scale * gauss12(key, row * D + j)). */
+sinkr_status sinkr_kv_append_synthetic(sinkr_engine* e, size_t seq, size_t layer,
+                                       size_t kv_head, uint64_t key_k, uint64_t key_v,
+                                       float k_scale, float v_scale, size_t rows);
+/* KvCache::length / token_count (kv_cache.cpp:86-96); token_count throws
+ * LOGIC_ERROR when the sequence's slots are ragged. */
+sinkr_status sinkr_kv_length(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                             size_t* out);
+sinkr_status sinkr_kv_token_count(sinkr_engine* e, size_t seq, size_t* out);
+/* KvCache::anchor (kv_cache.cpp:98-104): k0[D] and k0_norm. */
+sinkr_status sinkr_kv_anchor(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                             float* k0, float* k0_norm);
+/* Installs a replicated anchor on a sequence-shard engine whose slice does not
+ * hold global token 0 (multi-GPU sequence sharding). */
+sinkr_status sinkr_kv_set_anchor(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                                 const float* k0, float k0_norm);
+/* KvCache::historical (kv_cache.cpp:106-121) as a copy: rows [from, to) as f32
+ * (exact upcast of the stored bf16), for checkers and snapshots. */
+sinkr_status sinkr_kv_read(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                           size_t from, size_t to, float* k, float* v);
+
+/* ---- routing helpers (router.hpp:47-54,78; attention.hpp:82-85) ------------
+ * Host scalar control logic of the reference, reproduced with the reference's
+ * exact expression order (tau is computed on the host and handed to the probe
+ * kernel so no device FMA contraction can perturb it). */
+sinkr_status sinkr_threshold_for_length(size_t context_len,
+                                        const sinkr_threshold_profile* profile, double* out);
+sinkr_status sinkr_route(size_t layer, double score, size_t context_len,
+                         const sinkr_routing_config* config, int* sink, double* threshold);
+size_t sinkr_auto_num_splits(size_t context_len);
+sinkr_status sinkr_split_ranges(size_t len, size_t num_splits, size_t* from_to);
+
+/* ---- the hot path ---------------------------------------------------------- */
+/* routed_decode_step (router.hpp:84-86, router.cpp:82-188) for sequence 0, or
+ * for all B sequences with the _batch variant.  Host buffers:
+ *   queries  [B][H_q][D] f32 (read)      outputs [B][H_q][D] f32 (written)
+ *   groups   [B][H_kv]                   head_scores [B][H_q] f64
+ *   counters summed over the batch (may be NULL).
+ * The call copies the queries to the device, runs probe -> decode -> combine
+ * and copies the result back (blocking). */
+sinkr_status sinkr_routed_decode_step(sinkr_engine* e, const float* queries, size_t layer,
+                                      const sinkr_routing_config* config,
+                                      const sinkr_engine_options* options, float* outputs,
+                                      sinkr_group_info* groups, double* head_scores,
+                                      sinkr_load_counters* counters);
+sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, size_t layer,
+                                       const sinkr_routing_config* config,
+                                       const sinkr_engine_options* options, float* outputs,
+                                       sinkr_group_info* groups, double* head_scores,
+                                       sinkr_load_counters* counters);
+
+/* Device-resident variant: d_queries / d_outputs are device pointers; the
+ * call only enqueues work on the engine stream (no host sync).  Routing
+ * results stay on the device until sinkr_fetch_step_info (which syncs). */
+sinkr_status sinkr_routed_decode_async(sinkr_engine* e, const float* d_queries, size_t layer,
+                                       const sinkr_routing_config* config,
+                                       const sinkr_engine_options* options, float* d_outputs);
+sinkr_status sinkr_fetch_step_info(sinkr_engine* e, sinkr_group_info* groups,
+                                   double* head_scores, sinkr_load_counters* counters);
+
+/* Sequence-sharded multi-GPU split.  A rank's engine holds the
+ * token slice it owns; sinkr_decode_rank_partial_async writes one
+ * un-normalised LSE partial per (seq, kv_head, head): d_partial is
+ * [B*H_kv][r][D+2] f32 laid out per unit as m[r] (log2 domain), l[r], acc[r][D].
+ * After the caller all-gathers N such buffers (NCCL over NVLink),
+ * sinkr_merge_rank_partials_async LSE-merges them into d_outputs; Sink units
+ * (same bitmap on every rank) come out as bitwise zeros. */
+size_t sinkr_rank_partial_floats(sinkr_engine* e);
+sinkr_status sinkr_decode_rank_partial_async(sinkr_engine* e, const float* d_queries,
+                                             size_t layer, const sinkr_routing_config* config,
+                                             const sinkr_engine_options* options,
+                                             float* d_partial);
+sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gathered,
+                                             size_t num_ranks, float* d_outputs);
+
+/* ---- instrumentation ------------------------------------------------------- */
+/* Launch count of the last step (kernels of this library) and the device
+ * time (ms) of its decode kernel, measured with events on the engine stream. */
+sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches,
+                                   float* decode_ms, float* step_ms);
+/* Enables per-kernel event timing on the async path (costs two event records). */
+sinkr_status sinkr_set_timing(sinkr_engine* e, int enabled);
+/* Number of SMs / persistent CTAs used by the decode kernel. */
+int sinkr_decode_grid(sinkr_engine* e);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* SINKR_CUDA_H_ */

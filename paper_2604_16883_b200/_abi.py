@@ -1,0 +1,118 @@
+"""ctypes binding of include/sinkr_cuda.h (the C-ABI of libsinkr_cuda.so).
+
+The library is the product: there is no Python or CPU fallback.  If the
+shared object is missing, importing the package still works (so the CPU test
+suite can inspect the host logic), but every call that needs the engine
+raises loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .build import LIB
+
+c_size_t = C.c_size_t
+
+
+class CacheConfigC(C.Structure):
+    _fields_ = [("num_layers", c_size_t), ("num_q_heads", c_size_t),
+                ("num_kv_heads", c_size_t), ("head_dim", c_size_t),
+                ("capacity", c_size_t), ("num_seqs", c_size_t)]
+
+
+class ThresholdProfileC(C.Structure):
+    _fields_ = [("coeffs", C.c_double * 4), ("length_normalizer", C.c_double),
+                ("clamp_lo", C.c_double), ("clamp_hi", C.c_double)]
+
+
+class RoutingConfigC(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("profile", ThresholdProfileC),
+                ("excluded_layers", C.POINTER(c_size_t)), ("num_excluded_layers", c_size_t),
+                ("sink_on_tie", C.c_int)]
+
+
+class EngineOptionsC(C.Structure):
+    _fields_ = [("num_splits", c_size_t), ("block_size", c_size_t),
+                ("observe_only", C.c_int), ("global_context_len", c_size_t)]
+
+
+class LoadCountersC(C.Structure):
+    _fields_ = [("kv_floats_loaded", C.c_uint64), ("anchor_floats_loaded", C.c_uint64),
+                ("groups_active", C.c_uint64), ("groups_skipped", C.c_uint64),
+                ("routing_seconds", C.c_double), ("attention_seconds", C.c_double),
+                ("merge_seconds", C.c_double)]
+
+
+class GroupInfoC(C.Structure):
+    _fields_ = [("layer", c_size_t), ("kv_head", c_size_t), ("group_score", C.c_double),
+                ("threshold", C.c_double), ("sink", C.c_int32), ("degenerate", C.c_int32),
+                ("kv_floats_loaded", C.c_uint64), ("tokens_loaded", C.c_uint64)]
+
+
+# sinkr_status -> the Python analogue of the reference's exception classes
+SINKR_OK = 0
+_EXC = {
+    1: ValueError,        # std::invalid_argument
+    2: IndexError,        # std::out_of_range
+    3: RuntimeError,      # std::runtime_error
+    4: AssertionError,    # std::logic_error (ragged cache)
+}
+
+
+class SinkrCudaError(RuntimeError):
+    """CUDA failure (status 5) or no sm_100 device (status 6)."""
+
+
+class LogicError(AssertionError):
+    """std::logic_error (status 4)."""
+
+
+_EXC[4] = LogicError
+_EXC[5] = SinkrCudaError
+_EXC[6] = SinkrCudaError
+
+# Every symbol include/sinkr_cuda.h declares (checked by the CPU test suite).
+EXPORTS = (
+    "sinkr_last_error", "sinkr_version", "sinkr_engine_create", "sinkr_engine_destroy",
+    "sinkr_engine_stream", "sinkr_kv_append", "sinkr_kv_append_device_bf16",
+    "sinkr_kv_append_synthetic", "sinkr_kv_length", "sinkr_kv_token_count", "sinkr_kv_anchor",
+    "sinkr_kv_set_anchor", "sinkr_kv_read", "sinkr_threshold_for_length", "sinkr_route",
+    "sinkr_auto_num_splits", "sinkr_split_ranges", "sinkr_routed_decode_step",
+    "sinkr_routed_decode_batch", "sinkr_routed_decode_async", "sinkr_fetch_step_info",
+    "sinkr_rank_partial_floats", "sinkr_decode_rank_partial_async",
+    "sinkr_merge_rank_partials_async", "sinkr_last_step_stats", "sinkr_set_timing",
+    "sinkr_decode_grid",
+)
+
+_lib = None
+
+
+def lib():
+    """Load libsinkr_cuda.so; raise (never fall back) if it is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(
+                f"{LIB} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the engine has no CPU fallback)")
+        L = C.CDLL(LIB)
+        L.sinkr_last_error.restype = C.c_char_p
+        L.sinkr_version.restype = C.c_char_p
+        L.sinkr_engine_stream.restype = C.c_void_p
+        L.sinkr_engine_stream.argtypes = [C.c_void_p]
+        L.sinkr_auto_num_splits.restype = c_size_t
+        L.sinkr_auto_num_splits.argtypes = [c_size_t]
+        L.sinkr_rank_partial_floats.restype = c_size_t
+        L.sinkr_rank_partial_floats.argtypes = [C.c_void_p]
+        L.sinkr_decode_grid.restype = C.c_int
+        L.sinkr_decode_grid.argtypes = [C.c_void_p]
+        L.sinkr_engine_destroy.argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != SINKR_OK:
+        msg = lib().sinkr_last_error().decode(errors="replace")
+        raise _EXC.get(rc, SinkrCudaError)(msg)

@@ -1,0 +1,62 @@
+"""Build recipe for the in-tree CUDA library (sm_100a only).
+
+``python -m paper_2604_16883_b200.build`` or ``__graft_entry__.build()``
+compiles ``csrc/*.cu`` with nvcc into ``_lib/libsinkr_cuda.so``.  The library
+travels with the repo snapshot to the GPU box; nothing is JIT-compiled there.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB_DIR = os.path.join(HERE, "_lib")
+LIB = os.path.join(LIB_DIR, "libsinkr_cuda.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: cannot build the sm_100a library")
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cuh", ".h")))
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    deps = sources() + [os.path.join(ROOT, "include", "sinkr_cuda.h")]
+    return all(os.path.getmtime(p) <= t for p in deps)
+
+
+def build_library(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return LIB
+    os.makedirs(LIB_DIR, exist_ok=True)
+    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo",
+           # host side: no FMA contraction, so tau(L) matches the reference
+           "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-shared", "-I", os.path.join(ROOT, "include"),
+           os.path.join(CSRC, "engine.cu"), "-o", LIB + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build_library(force="--force" in sys.argv, verbose="-v" in sys.argv))

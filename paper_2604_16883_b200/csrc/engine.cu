@@ -1,0 +1,904 @@
+// engine.cu — host side of the B200 SinkRouter engine and its C-ABI
+// (include/sinkr_cuda.h).  Owns the HBM-resident KV cache, the anchor table,
+// the per-step work buffers, the TMA tensor maps and one CUDA graph per
+// (queries, outputs, mode) binding that replays probe -> decode -> combine.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sinkr_cuda.h"
+#include "kernels.cuh"
+
+namespace {
+
+using namespace sinkr;
+
+thread_local std::string g_err;
+
+struct Error {
+    sinkr_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(sinkr_status code, const std::string& msg) { throw Error{code, msg}; }
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            fail(SINKR_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+template <class F>
+sinkr_status guard(F&& f) {
+    try {
+        f();
+        return SINKR_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SINKR_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SINKR_RUNTIME_ERROR;
+    }
+}
+
+// f32 -> bf16 round-to-nearest-even (bit-identical to __float2bfloat16_rn for
+// finite inputs and to oracle/sinkr_oracle.c:orc_round_bf16).
+uint16_t f32_to_bf16(float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    if ((b & 0x7F800000u) == 0x7F800000u) return (uint16_t)((b >> 16) | ((x != x) ? 0x40u : 0u));
+    return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+float bf16_to_f32(uint16_t h) {
+    const uint32_t b = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &b, 4);
+    return f;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// router.cpp:59-65 with the reference's expression order.  Compiled for the
+// host without FMA contraction (see build flags), like the reference.
+double threshold_for_length(size_t len, const sinkr_threshold_profile& p) {
+    if (len == 0) fail(SINKR_INVALID_ARGUMENT, "context length must be positive");
+    const double x = static_cast<double>(len) / p.length_normalizer;
+    const double tau = ((p.coeffs[0] * x + p.coeffs[1]) * x + p.coeffs[2]) * x + p.coeffs[3];
+    return tau < p.clamp_lo ? p.clamp_lo : (p.clamp_hi < tau ? p.clamp_hi : tau);
+}
+
+bool layer_excluded(size_t layer, const sinkr_routing_config& c) {
+    for (size_t i = 0; i < c.num_excluded_layers; ++i)
+        if (c.excluded_layers[i] == layer) return true;
+    return false;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            fail(SINKR_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int D>
+int smem_bytes() {
+    return dev::Cfg<D>::kSmemBytes;
+}
+
+}  // namespace
+
+struct sinkr_engine {
+    sinkr_cache_config cfg{};
+    size_t B = 1, U = 0, r = 0, D = 0, layers = 0, cap = 0;
+    int device = 0, num_sms = 0, grid = 0, probe_grid = 1;
+    uint32_t* d_head_degen = nullptr;
+    cudaStream_t stream = nullptr;
+
+    __nv_bfloat16* d_k = nullptr;
+    __nv_bfloat16* d_v = nullptr;
+    float* d_anchor = nullptr;
+    float* d_anchor_norm = nullptr;
+    double* d_norm64 = nullptr;
+    std::vector<size_t> len;  // [layers][B][Hkv]
+    std::vector<float> h_anchor, h_anchor_norm;
+    std::vector<uint8_t> anchored;
+
+    // step input block: hdr | tau[B] | len[B] | q[B][Hq][D]
+    size_t off_tau = 0, off_len = 0, off_q = 0, in_bytes = 0;
+    uint8_t* d_in = nullptr;
+    uint8_t* h_in = nullptr;
+    // step result block: out | head_scores | group_scores | tokens | flags
+    size_t off_hs = 0, off_gs = 0, off_tok = 0, off_fl = 0, res_bytes = 0;
+    uint8_t* d_res = nullptr;
+    uint8_t* h_res = nullptr;
+
+    dev::WorkState* d_ws = nullptr;
+    uint32_t* d_active = nullptr;
+    uint32_t* d_prefix = nullptr;
+    uint32_t* d_slot_count = nullptr;
+    float* d_partials = nullptr;
+    size_t S = 0, PS = 0;
+
+    CUtensorMap tmk{}, tmv{};
+    cudaEvent_t ev[4] = {};
+    cudaEvent_t ev_in = nullptr;
+    bool timing = true;
+    bool params_valid = false;
+    std::vector<uint8_t> last_params;
+    std::map<std::tuple<const void*, void*, int>, cudaGraphExec_t> graphs;
+    uint32_t last_launches = 0;
+    int last_mode = 0;
+
+    size_t slot_index(size_t layer, size_t seq, size_t g) const {
+        return (layer * B + seq) * cfg.num_kv_heads + g;
+    }
+    size_t row_base(size_t layer, size_t seq, size_t g) const {
+        return slot_index(layer, seq, g) * cap;
+    }
+    dev::DevTables tables(const float* q) const {
+        dev::DevTables t{};
+        t.hdr = reinterpret_cast<const dev::StepHdr*>(d_in);
+        t.tau = reinterpret_cast<const double*>(d_in + off_tau);
+        t.len = reinterpret_cast<const uint32_t*>(d_in + off_len);
+        t.q = q;
+        t.anchors = d_anchor;
+        t.anchor_norm = d_anchor_norm;
+        t.head_scores = reinterpret_cast<double*>(d_res + off_hs);
+        t.head_degen = d_head_degen;
+        t.group_scores = reinterpret_cast<double*>(d_res + off_gs);
+        t.unit_flags = reinterpret_cast<uint32_t*>(d_res + off_fl);
+        t.tokens = reinterpret_cast<unsigned long long*>(d_res + off_tok);
+        t.ws = d_ws;
+        t.act_info = reinterpret_cast<uint4*>(d_active);
+        t.unit_next = d_prefix;
+        t.slot_count = d_slot_count;
+        t.partials = d_partials;
+        t.B = (uint32_t)B;
+        t.Hq = (uint32_t)cfg.num_q_heads;
+        t.Hkv = (uint32_t)cfg.num_kv_heads;
+        t.r = (uint32_t)r;
+        t.D = (uint32_t)D;
+        t.cap = (uint32_t)cap;
+        t.S = (uint32_t)S;
+        t.grid = (uint32_t)grid;
+        t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
+        return t;
+    }
+};
+
+namespace {
+
+void check_slot(const sinkr_engine* e, size_t seq, size_t layer, size_t kv_head) {
+    if (layer >= e->layers) fail(SINKR_OUT_OF_RANGE, "layer index out of range");
+    if (kv_head >= e->cfg.num_kv_heads) fail(SINKR_OUT_OF_RANGE, "kv_head index out of range");
+    if (seq >= e->B) fail(SINKR_OUT_OF_RANGE, "sequence index out of range");
+}
+
+void make_tmap(CUtensorMap* map, void* base, size_t rows, size_t D) {
+    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(D * 2)};
+    const cuuint32_t box[2] = {(cuuint32_t)(D >= 64 ? 64 : D), (cuuint32_t)dev::kStageTok};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw =
+        D >= 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const CUresult rc = get_encode()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides,
+                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) fail(SINKR_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+}
+
+int probe_smem(const sinkr_engine* e) { return 2 * dev::kProbeHeads * (int)(e->D + 1) * 8; }
+
+// decode and combine are launched with programmatic dependent launch: their
+// CTAs become resident while the previous kernel drains and block in
+// griddepcontrol.wait until its results are visible.
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+template <int D>
+void launch_decode(sinkr_engine* e, const dev::DevTables& t) {
+    launch_pdl(dev::decode_kernel<D>, dim3(e->grid), dim3(dev::kThreads), smem_bytes<D>(),
+               e->stream, e->tmk, e->tmv, t);
+}
+
+void launch_combine(sinkr_engine* e, const dev::DevTables& t, const float* src, size_t ustride,
+                    size_t sstride, uint32_t fixed_n, float* dst, int mode, size_t max_n) {
+    launch_pdl(dev::combine_kernel, dim3((unsigned)e->U, (unsigned)e->r, (unsigned)(e->D / 32)),
+               dim3(32 * dev::kCombineGroups), max_n * 4, e->stream, t, src, (uint32_t)ustride,
+               (uint32_t)sstride, fixed_n, dst, mode);
+}
+
+// Enqueues probe -> decode -> combine on the engine stream (graph-captured).
+void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
+    const dev::DevTables t = e->tables(d_q);
+    if (e->timing) CK(cudaEventRecord(e->ev[0], e->stream));
+    switch (e->D) {
+        case 32: dev::probe_kernel<32><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t); break;
+        case 64: dev::probe_kernel<64><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t); break;
+        default: dev::probe_kernel<128><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t); break;
+    }
+    if (e->timing) CK(cudaEventRecord(e->ev[1], e->stream));
+    switch (e->D) {
+        case 32: launch_decode<32>(e, t); break;
+        case 64: launch_decode<64>(e, t); break;
+        default: launch_decode<128>(e, t); break;
+    }
+    if (e->timing) CK(cudaEventRecord(e->ev[2], e->stream));
+    launch_combine(e, t, e->d_partials, e->S * e->PS, e->PS, 0u, d_out, mode, e->S);
+    if (e->timing) CK(cudaEventRecord(e->ev[3], e->stream));
+    CK(cudaGetLastError());
+}
+
+// Timing mode launches the three kernels eagerly with events between them
+// (per-phase seconds, like the reference's phase timers).  Otherwise the step
+// is one CUDA-graph replay, bracketed by events outside the graph.
+void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
+    e->last_launches = 3;
+    e->last_mode = mode;
+    if (e->timing) {
+        enqueue_step(e, d_q, d_out, mode);
+        return;
+    }
+    const auto key = std::make_tuple((const void*)d_q, (void*)d_out, mode);
+    auto it = e->graphs.find(key);
+    if (it == e->graphs.end()) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_step(e, d_q, d_out, mode);
+        } catch (...) {
+            cudaStreamEndCapture(e->stream, &g);
+            throw;
+        }
+        CK(cudaStreamEndCapture(e->stream, &g));
+        cudaGraphExec_t ex;
+        CK(cudaGraphInstantiate(&ex, g, 0));
+        CK(cudaGraphDestroy(g));
+        it = e->graphs.emplace(key, ex).first;
+    }
+    CK(cudaEventRecord(e->ev[0], e->stream));
+    CK(cudaGraphLaunch(it->second, e->stream));
+    CK(cudaEventRecord(e->ev[3], e->stream));
+}
+
+size_t token_count(const sinkr_engine* e, size_t seq) {
+    const size_t H = e->cfg.num_kv_heads;
+    const size_t n = e->len[e->slot_index(0, seq, 0)];
+    for (size_t l = 0; l < e->layers; ++l)
+        for (size_t g = 0; g < H; ++g)
+            if (e->len[e->slot_index(l, seq, g)] != n)
+                fail(SINKR_LOGIC_ERROR, "kv cache lengths are ragged across slots");
+    return n;
+}
+
+// Validates a step (router.cpp:85-90) and stages hdr / tau / len into the
+// pinned input block; uploads them only when they changed.
+void stage_params(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg,
+                  const sinkr_engine_options* opt, bool defer_upload) {
+    if (!cfg) fail(SINKR_INVALID_ARGUMENT, "routing config is null");
+    if (layer >= e->layers) fail(SINKR_OUT_OF_RANGE, "layer index out of range");
+    sinkr_engine_options o{};
+    o.block_size = dev::kStageTok;
+    if (opt) o = *opt;
+    // wait until the previous upload consumed the pinned staging block
+    CK(cudaEventSynchronize(e->ev_in));
+    auto* hdr = reinterpret_cast<dev::StepHdr*>(e->h_in);
+    auto* tau = reinterpret_cast<double*>(e->h_in + e->off_tau);
+    auto* len = reinterpret_cast<uint32_t*>(e->h_in + e->off_len);
+    hdr->layer = (uint32_t)layer;
+    hdr->flags = (o.observe_only ? dev::kObserveOnly : 0u) |
+                 (cfg->sink_on_tie ? dev::kSinkOnTie : 0u) |
+                 (layer_excluded(layer, *cfg) ? dev::kLayerExcluded : 0u);
+    hdr->pad[0] = hdr->pad[1] = 0;
+    for (size_t s = 0; s < e->B; ++s) {
+        const size_t L = token_count(e, s);
+        if (L == 0) fail(SINKR_RUNTIME_ERROR, "routed decode over an empty cache");
+        for (size_t g = 0; g < e->cfg.num_kv_heads; ++g)
+            if (!e->anchored[e->slot_index(layer, s, g)])
+                fail(SINKR_RUNTIME_ERROR, "anchor requested from empty cache slot");
+        const size_t Lg = o.global_context_len ? o.global_context_len : L;
+        tau[s] = threshold_for_length(Lg, cfg->profile);
+        len[s] = (uint32_t)L;
+    }
+    const size_t pbytes = e->off_q;
+    const bool same = e->params_valid && e->last_params.size() == pbytes &&
+                      std::memcmp(e->last_params.data(), e->h_in, pbytes) == 0;
+    if (!defer_upload && !same) {
+        CK(cudaMemcpyAsync(e->d_in, e->h_in, pbytes, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaEventRecord(e->ev_in, e->stream));
+    }
+    e->last_params.assign(e->h_in, e->h_in + pbytes);
+    e->params_valid = true;
+}
+
+void fill_info(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg,
+               sinkr_group_info* groups, double* head_scores, sinkr_load_counters* counters,
+               const sinkr_engine_options* opt) {
+    const size_t H = e->cfg.num_kv_heads, Hq = e->cfg.num_q_heads;
+    const auto* hs = reinterpret_cast<const double*>(e->h_res + e->off_hs);
+    const auto* gs = reinterpret_cast<const double*>(e->h_res + e->off_gs);
+    const auto* tok = reinterpret_cast<const unsigned long long*>(e->h_res + e->off_tok);
+    const auto* fl = reinterpret_cast<const uint32_t*>(e->h_res + e->off_fl);
+    const auto* tau = reinterpret_cast<const double*>(e->h_in + e->off_tau);
+    sinkr_load_counters c{};
+    for (size_t u = 0; u < e->U; ++u) {
+        const size_t s = u / H;
+        if (groups) {
+            sinkr_group_info& gi = groups[u];
+            gi.layer = layer;
+            gi.kv_head = u % H;
+            gi.group_score = gs[u];
+            gi.threshold = tau[s];
+            gi.sink = (fl[u] & dev::kSink) ? 1 : 0;
+            gi.degenerate = (fl[u] & dev::kDegenerate) ? 1 : 0;
+            gi.tokens_loaded = tok[u];
+            gi.kv_floats_loaded = 2ull * tok[u] * e->D;
+        }
+        c.kv_floats_loaded += 2ull * tok[u] * e->D;
+        if (fl[u] & dev::kActive)
+            ++c.groups_active;
+        else
+            ++c.groups_skipped;
+    }
+    c.anchor_floats_loaded = (uint64_t)(e->U * e->D);
+    if (head_scores) std::memcpy(head_scores, hs, e->B * Hq * sizeof(double));
+    if (e->timing) {
+        float ms[3] = {0, 0, 0};
+        for (int i = 0; i < 3; ++i) CK(cudaEventElapsedTime(&ms[i], e->ev[i], e->ev[i + 1]));
+        c.routing_seconds = ms[0] * 1e-3;
+        c.attention_seconds = ms[1] * 1e-3;
+        c.merge_seconds = ms[2] * 1e-3;
+    }
+    if (counters) *counters = c;
+    (void)cfg;
+    // attend_chunk rejects block_size == 0 only when a group actually runs
+    // (attention.cpp:297), so the check happens after routing.
+    if (opt && opt->block_size == 0 && c.groups_active > 0)
+        fail(SINKR_INVALID_ARGUMENT, "block_size must be positive");
+}
+
+void check_error_flag(sinkr_engine* e) {
+    dev::WorkState ws;
+    CK(cudaMemcpyAsync(&ws, e->d_ws, sizeof(ws), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    if (ws.error) fail(SINKR_RUNTIME_ERROR, "decode partial-slot overflow");
+}
+
+void upload_anchor(sinkr_engine* e, size_t idx) {
+    CK(cudaMemcpyAsync(e->d_anchor + idx * e->D, e->h_anchor.data() + idx * e->D, e->D * 4,
+                       cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(e->d_anchor_norm + idx, e->h_anchor_norm.data() + idx, 4,
+                       cudaMemcpyHostToDevice, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+}
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+extern "C" {
+
+const char* sinkr_last_error(void) { return g_err.c_str(); }
+const char* sinkr_version(void) { return "sinkr-b200 0.1 (sm_100a)"; }
+
+sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
+                                 sinkr_engine** out) {
+    return guard([&] {
+        if (!config || !out) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        const sinkr_cache_config& c = *config;
+        // CacheConfig::validate (kv_cache.cpp:32-39)
+        if (c.num_layers == 0) fail(SINKR_INVALID_ARGUMENT, "num_layers must be positive");
+        if (c.num_kv_heads == 0) fail(SINKR_INVALID_ARGUMENT, "num_kv_heads must be positive");
+        if (c.num_q_heads == 0 || c.num_q_heads % c.num_kv_heads != 0)
+            fail(SINKR_INVALID_ARGUMENT, "num_q_heads must be a positive multiple of num_kv_heads");
+        if (c.head_dim == 0) fail(SINKR_INVALID_ARGUMENT, "head_dim must be positive");
+        if (c.capacity == 0) fail(SINKR_INVALID_ARGUMENT, "capacity must be positive");
+        if (c.head_dim != 32 && c.head_dim != 64 && c.head_dim != 128)
+            fail(SINKR_INVALID_ARGUMENT, "head_dim must be 32, 64 or 128 on the GPU engine");
+        if (c.num_q_heads / c.num_kv_heads > (size_t)dev::kMaxR)
+            fail(SINKR_INVALID_ARGUMENT, "GQA group width above 8 is not supported");
+
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            fail(SINKR_NO_DEVICE, "no CUDA device visible (the engine has no CPU fallback)");
+        }
+        if (device < 0 || device >= ndev) fail(SINKR_NO_DEVICE, "device ordinal out of range");
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            fail(SINKR_NO_DEVICE, std::string("sm_100 device required, found ") + prop.name);
+        CK(cudaSetDevice(device));
+
+        auto* e = new sinkr_engine();
+        try {
+            e->cfg = c;
+            e->B = c.num_seqs ? c.num_seqs : 1;
+            e->cfg.num_seqs = e->B;
+            e->U = e->B * c.num_kv_heads;
+            e->r = c.num_q_heads / c.num_kv_heads;
+            e->D = c.head_dim;
+            e->layers = c.num_layers;
+            e->cap = c.capacity;
+            e->device = device;
+            e->num_sms = prop.multiProcessorCount;
+            e->grid = e->num_sms;
+            const size_t rows = e->layers * e->B * c.num_kv_heads * e->cap;
+            if (rows >= (size_t(1) << 31))
+                fail(SINKR_INVALID_ARGUMENT, "cache exceeds 2^31 rows (TMA coordinate range)");
+            CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+            const size_t kv_bytes = rows * e->D * 2;
+            CK(cudaMalloc(&e->d_k, kv_bytes));
+            CK(cudaMalloc(&e->d_v, kv_bytes));
+            // rows past a slot's length are read (and masked) by tail stages:
+            // keep them finite.
+            CK(cudaMemsetAsync(e->d_k, 0, kv_bytes, e->stream));
+            CK(cudaMemsetAsync(e->d_v, 0, kv_bytes, e->stream));
+            const size_t slots = e->layers * e->B * c.num_kv_heads;
+            CK(cudaMalloc(&e->d_anchor, slots * e->D * 4));
+            CK(cudaMalloc(&e->d_anchor_norm, slots * 4));
+            CK(cudaMalloc(&e->d_norm64, 8));
+            CK(cudaMemsetAsync(e->d_anchor, 0, slots * e->D * 4, e->stream));
+            CK(cudaMemsetAsync(e->d_anchor_norm, 0, slots * 4, e->stream));
+            e->len.assign(slots, 0);
+            e->h_anchor.assign(slots * e->D, 0.f);
+            e->h_anchor_norm.assign(slots, 0.f);
+            e->anchored.assign(slots, 0);
+
+            const size_t Hq = c.num_q_heads;
+            e->off_tau = 64;
+            e->off_len = align_up(e->off_tau + 8 * e->B, 64);
+            e->off_q = align_up(e->off_len + 4 * e->B, 128);
+            e->in_bytes = e->off_q + e->B * Hq * e->D * 4;
+            CK(cudaMalloc(&e->d_in, e->in_bytes));
+            CK(cudaMallocHost(&e->h_in, e->in_bytes));
+            std::memset(e->h_in, 0, e->in_bytes);
+
+            e->off_hs = align_up(e->B * Hq * e->D * 4, 128);
+            e->off_gs = align_up(e->off_hs + e->B * Hq * 8, 128);
+            e->off_tok = align_up(e->off_gs + e->U * 8, 128);
+            e->off_fl = align_up(e->off_tok + e->U * 8, 128);
+            e->res_bytes = align_up(e->off_fl + e->U * 4, 128);
+            CK(cudaMalloc(&e->d_res, e->res_bytes));
+            CK(cudaMallocHost(&e->h_res, e->res_bytes));
+            CK(cudaMemsetAsync(e->d_res, 0, e->res_bytes, e->stream));
+
+            CK(cudaMalloc(&e->d_head_degen, e->B * Hq * 4));
+            e->probe_grid = (int)((e->B * Hq + dev::kProbeHeads - 1) / dev::kProbeHeads);
+            CK(cudaMalloc(&e->d_ws, sizeof(dev::WorkState)));
+            CK(cudaMemsetAsync(e->d_ws, 0, sizeof(dev::WorkState), e->stream));
+            CK(cudaMalloc(&e->d_active, e->U * 16));
+            CK(cudaMalloc(&e->d_prefix, (e->U + 1) * 4));  // unit_next cursors
+            CK(cudaMalloc(&e->d_slot_count, e->U * 4));
+            // one flush per (CTA, unit) at most: S = min(grid, stages per slot)
+            e->S = std::min<size_t>(e->grid, (e->cap + dev::kStageTok - 1) / dev::kStageTok);
+            e->PS = e->r * (e->D + 2);
+            CK(cudaMalloc(&e->d_partials, e->U * e->S * e->PS * 4));
+
+            make_tmap(&e->tmk, e->d_k, rows, e->D);
+            make_tmap(&e->tmv, e->d_v, rows, e->D);
+            CK(cudaFuncSetAttribute(dev::decode_kernel<32>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<32>()));
+            CK(cudaFuncSetAttribute(dev::decode_kernel<64>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>()));
+            CK(cudaFuncSetAttribute(dev::decode_kernel<128>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_bytes<128>()));
+            CK(cudaFuncSetAttribute(dev::probe_kernel<32>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
+            CK(cudaFuncSetAttribute(dev::probe_kernel<64>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
+            CK(cudaFuncSetAttribute(dev::probe_kernel<128>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
+            for (auto& ev : e->ev) CK(cudaEventCreate(&ev));
+            CK(cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming));
+            CK(cudaEventRecord(e->ev_in, e->stream));
+            CK(cudaStreamSynchronize(e->stream));
+        } catch (...) {
+            sinkr_engine_destroy(e);
+            throw;
+        }
+        *out = e;
+    });
+}
+
+sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
+    if (!e) return SINKR_OK;
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& ev : e->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->ev_in) cudaEventDestroy(e->ev_in);
+    cudaFree(e->d_k);
+    cudaFree(e->d_v);
+    cudaFree(e->d_anchor);
+    cudaFree(e->d_anchor_norm);
+    cudaFree(e->d_norm64);
+    cudaFree(e->d_in);
+    cudaFree(e->d_res);
+    cudaFree(e->d_ws);
+    cudaFree(e->d_head_degen);
+    cudaFree(e->d_active);
+    cudaFree(e->d_prefix);
+    cudaFree(e->d_slot_count);
+    cudaFree(e->d_partials);
+    if (e->h_in) cudaFreeHost(e->h_in);
+    if (e->h_res) cudaFreeHost(e->h_res);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+    return SINKR_OK;
+}
+
+void* sinkr_engine_stream(sinkr_engine* e) { return e ? (void*)e->stream : nullptr; }
+int sinkr_decode_grid(sinkr_engine* e) { return e ? e->grid : 0; }
+
+sinkr_status sinkr_kv_append(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                             const float* k, const float* v, size_t rows) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        check_slot(e, seq, layer, kv_head);
+        if (rows == 0) return;
+        if (!k || !v) fail(SINKR_INVALID_ARGUMENT, "k/v row size does not match head_dim");
+        const size_t idx = e->slot_index(layer, seq, kv_head), D = e->D;
+        if (e->len[idx] + rows > e->cap)
+            fail(SINKR_RUNTIME_ERROR,
+                 "kv cache overflow: slot at capacity " + std::to_string(e->cap));
+        std::vector<uint16_t> kb(rows * D), vb(rows * D);
+        for (size_t i = 0; i < rows * D; ++i) {
+            kb[i] = f32_to_bf16(k[i]);
+            vb[i] = f32_to_bf16(v[i]);
+        }
+        if (e->len[idx] == 0) {
+            // kv_cache.cpp:71-77 on the stored (bf16-rounded) first key
+            double s = 0.0;
+            for (size_t j = 0; j < D; ++j) {
+                const double x = bf16_to_f32(kb[j]);
+                s += x * x;
+            }
+            const double n = std::sqrt(s);
+            if (n < 1e-12)
+                fail(SINKR_RUNTIME_ERROR, "degenerate anchor: first-token key norm below 1e-12");
+            for (size_t j = 0; j < D; ++j) e->h_anchor[idx * D + j] = bf16_to_f32(kb[j]);
+            e->h_anchor_norm[idx] = (float)n;
+            upload_anchor(e, idx);
+            e->anchored[idx] = 1;
+        }
+        const size_t off = (e->row_base(layer, seq, kv_head) + e->len[idx]) * D;
+        CK(cudaMemcpyAsync(e->d_k + off, kb.data(), rows * D * 2, cudaMemcpyHostToDevice,
+                           e->stream));
+        CK(cudaMemcpyAsync(e->d_v + off, vb.data(), rows * D * 2, cudaMemcpyHostToDevice,
+                           e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        e->len[idx] += rows;
+    });
+}
+
+static void capture_anchor_device(sinkr_engine* e, size_t idx) {
+    const size_t D = e->D;
+    const __nv_bfloat16* row0 = e->d_k + idx * e->cap * D;  // row 0 of the slot
+    dev::anchor_capture_kernel<<<1, 32, 0, e->stream>>>(row0, (uint32_t)D, e->d_anchor + idx * D,
+                                                        e->d_anchor_norm + idx, e->d_norm64);
+    CK(cudaGetLastError());
+    double n = 0;
+    CK(cudaMemcpyAsync(&n, e->d_norm64, 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(e->h_anchor.data() + idx * D, e->d_anchor + idx * D, D * 4,
+                       cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(e->h_anchor_norm.data() + idx, e->d_anchor_norm + idx, 4,
+                       cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    if (n < 1e-12) fail(SINKR_RUNTIME_ERROR, "degenerate anchor: first-token key norm below 1e-12");
+    e->anchored[idx] = 1;
+}
+
+sinkr_status sinkr_kv_append_device_bf16(sinkr_engine* e, size_t seq, size_t layer,
+                                         size_t kv_head, const void* k, const void* v,
+                                         size_t rows) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        check_slot(e, seq, layer, kv_head);
+        if (rows == 0) return;
+        const size_t idx = e->slot_index(layer, seq, kv_head), D = e->D;
+        if (e->len[idx] + rows > e->cap)
+            fail(SINKR_RUNTIME_ERROR,
+                 "kv cache overflow: slot at capacity " + std::to_string(e->cap));
+        const size_t off = (e->row_base(layer, seq, kv_head) + e->len[idx]) * D;
+        CK(cudaMemcpyAsync(e->d_k + off, k, rows * D * 2, cudaMemcpyDeviceToDevice, e->stream));
+        CK(cudaMemcpyAsync(e->d_v + off, v, rows * D * 2, cudaMemcpyDeviceToDevice, e->stream));
+        if (e->len[idx] == 0) capture_anchor_device(e, idx);
+        CK(cudaStreamSynchronize(e->stream));
+        e->len[idx] += rows;
+    });
+}
+
+sinkr_status sinkr_kv_append_synthetic(sinkr_engine* e, size_t seq, size_t layer,
+                                       size_t kv_head, uint64_t key_k, uint64_t key_v,
+                                       float k_scale, float v_scale, size_t rows) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        check_slot(e, seq, layer, kv_head);
+        if (rows == 0) return;
+        const size_t idx = e->slot_index(layer, seq, kv_head), D = e->D;
+        if (e->len[idx] + rows > e->cap)
+            fail(SINKR_RUNTIME_ERROR,
+                 "kv cache overflow: slot at capacity " + std::to_string(e->cap));
+        const size_t row0 = e->len[idx];
+        const size_t off = (e->row_base(layer, seq, kv_head) + row0) * D;
+        const uint64_t n = (uint64_t)rows * D;
+        const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 64);
+        dev::synth_rows_kernel<<<blocks, 256, 0, e->stream>>>(e->d_k + off, e->d_v + off, key_k,
+                                                             key_v, k_scale, v_scale, row0, rows,
+                                                             (uint32_t)D);
+        CK(cudaGetLastError());
+        if (row0 == 0) capture_anchor_device(e, idx);
+        CK(cudaStreamSynchronize(e->stream));
+        e->len[idx] += rows;
+    });
+}
+
+sinkr_status sinkr_kv_length(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                             size_t* out) {
+    return guard([&] {
+        if (!e || !out) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        check_slot(e, seq, layer, kv_head);
+        *out = e->len[e->slot_index(layer, seq, kv_head)];
+    });
+}
+
+sinkr_status sinkr_kv_token_count(sinkr_engine* e, size_t seq, size_t* out) {
+    return guard([&] {
+        if (!e || !out) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        if (seq >= e->B) fail(SINKR_OUT_OF_RANGE, "sequence index out of range");
+        *out = token_count(e, seq);
+    });
+}
+
+sinkr_status sinkr_kv_anchor(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                             float* k0, float* k0_norm) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        check_slot(e, seq, layer, kv_head);
+        const size_t idx = e->slot_index(layer, seq, kv_head);
+        if (!e->anchored[idx]) fail(SINKR_RUNTIME_ERROR, "anchor requested from empty cache slot");
+        if (k0) std::memcpy(k0, e->h_anchor.data() + idx * e->D, e->D * 4);
+        if (k0_norm) *k0_norm = e->h_anchor_norm[idx];
+    });
+}
+
+sinkr_status sinkr_kv_set_anchor(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                                 const float* k0, float k0_norm) {
+    return guard([&] {
+        if (!e || !k0) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        check_slot(e, seq, layer, kv_head);
+        if (!(k0_norm >= 1e-12f))
+            fail(SINKR_RUNTIME_ERROR, "degenerate anchor: first-token key norm below 1e-12");
+        const size_t idx = e->slot_index(layer, seq, kv_head);
+        std::memcpy(e->h_anchor.data() + idx * e->D, k0, e->D * 4);
+        e->h_anchor_norm[idx] = k0_norm;
+        upload_anchor(e, idx);
+        e->anchored[idx] = 1;
+    });
+}
+
+sinkr_status sinkr_kv_read(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
+                           size_t from, size_t to, float* k, float* v) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        check_slot(e, seq, layer, kv_head);
+        const size_t idx = e->slot_index(layer, seq, kv_head), D = e->D;
+        if (from > to || to > e->len[idx])
+            fail(SINKR_OUT_OF_RANGE, "historical range [" + std::to_string(from) + ", " +
+                                         std::to_string(to) + ") exceeds length " +
+                                         std::to_string(e->len[idx]));
+        const size_t n = (to - from) * D;
+        if (n == 0) return;
+        float* tmp = nullptr;
+        CK(cudaMallocAsync(&tmp, n * 4, e->stream));
+        const size_t off = (e->row_base(layer, seq, kv_head) + from) * D;
+        const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 32);
+        for (int which = 0; which < 2; ++which) {
+            float* dst = which ? v : k;
+            if (!dst) continue;
+            dev::upcast_kernel<<<blocks, 256, 0, e->stream>>>((which ? e->d_v : e->d_k) + off, tmp,
+                                                              n);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(dst, tmp, n * 4, cudaMemcpyDeviceToHost, e->stream));
+        }
+        CK(cudaFreeAsync(tmp, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+    });
+}
+
+// ---- routing helpers ---------------------------------------------------------
+sinkr_status sinkr_threshold_for_length(size_t context_len,
+                                        const sinkr_threshold_profile* profile, double* out) {
+    return guard([&] {
+        if (!profile || !out) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        *out = threshold_for_length(context_len, *profile);
+    });
+}
+
+sinkr_status sinkr_route(size_t layer, double score, size_t context_len,
+                         const sinkr_routing_config* config, int* sink, double* threshold) {
+    return guard([&] {
+        if (!config || !sink || !threshold) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        *threshold = threshold_for_length(context_len, config->profile);
+        const bool over = config->sink_on_tie ? score >= *threshold : score > *threshold;
+        *sink = (over && !layer_excluded(layer, *config)) ? 1 : 0;
+    });
+}
+
+size_t sinkr_auto_num_splits(size_t context_len) {
+    const size_t s = (context_len + 8191) / 8192;
+    return std::clamp<size_t>(s, 1, 16);
+}
+
+sinkr_status sinkr_split_ranges(size_t len, size_t num_splits, size_t* from_to) {
+    return guard([&] {
+        if (num_splits == 0 || num_splits > len)
+            fail(SINKR_INVALID_ARGUMENT, "num_splits must be in [1, len], got " +
+                                             std::to_string(num_splits) + " for len " +
+                                             std::to_string(len));
+        if (!from_to) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        const size_t base = len / num_splits, rem = len % num_splits;
+        size_t start = 0;
+        for (size_t c = 0; c < num_splits; ++c) {
+            const size_t sz = base + (c < rem ? 1 : 0);
+            from_to[2 * c] = start;
+            from_to[2 * c + 1] = start + sz;
+            start += sz;
+        }
+    });
+}
+
+// ---- hot path ------------------------------------------------------------------
+sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, size_t layer,
+                                       const sinkr_routing_config* config,
+                                       const sinkr_engine_options* options, float* outputs,
+                                       sinkr_group_info* groups, double* head_scores,
+                                       sinkr_load_counters* counters) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        if (!queries) fail(SINKR_INVALID_ARGUMENT, "queries span must be H_q x D for one layer");
+        CK(cudaSetDevice(e->device));
+        stage_params(e, layer, config, options, true);  // validates before touching q
+        const size_t qbytes = e->B * e->cfg.num_q_heads * e->D * 4;
+        // params were written into h_in by stage_params; append the queries
+        // and upload the whole input block in one H2D copy.
+        std::memcpy(e->h_in + e->off_q, queries, qbytes);
+        CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaEventRecord(e->ev_in, e->stream));
+        float* d_out = reinterpret_cast<float*>(e->d_res);
+        run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, 0);
+        CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        dev::WorkState ws;
+        CK(cudaMemcpy(&ws, e->d_ws, sizeof(ws), cudaMemcpyDeviceToHost));
+        if (ws.error) fail(SINKR_RUNTIME_ERROR, "decode partial-slot overflow");
+        if (outputs) std::memcpy(outputs, e->h_res, qbytes);
+        fill_info(e, layer, config, groups, head_scores, counters, options);
+    });
+}
+
+sinkr_status sinkr_routed_decode_step(sinkr_engine* e, const float* queries, size_t layer,
+                                      const sinkr_routing_config* config,
+                                      const sinkr_engine_options* options, float* outputs,
+                                      sinkr_group_info* groups, double* head_scores,
+                                      sinkr_load_counters* counters) {
+    if (e && e->B != 1) {
+        g_err = "sinkr_routed_decode_step serves single-sequence engines; use _batch";
+        return SINKR_INVALID_ARGUMENT;
+    }
+    return sinkr_routed_decode_batch(e, queries, layer, config, options, outputs, groups,
+                                     head_scores, counters);
+}
+
+sinkr_status sinkr_routed_decode_async(sinkr_engine* e, const float* d_queries, size_t layer,
+                                       const sinkr_routing_config* config,
+                                       const sinkr_engine_options* options, float* d_outputs) {
+    return guard([&] {
+        if (!e || !d_queries || !d_outputs) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        stage_params(e, layer, config, options, false);
+        run_graph(e, d_queries, d_outputs, 0);
+    });
+}
+
+sinkr_status sinkr_fetch_step_info(sinkr_engine* e, sinkr_group_info* groups,
+                                   double* head_scores, sinkr_load_counters* counters) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        CK(cudaMemcpyAsync(e->h_res + e->off_hs, e->d_res + e->off_hs, e->res_bytes - e->off_hs,
+                           cudaMemcpyDeviceToHost, e->stream));
+        check_error_flag(e);
+        const auto* hdr = reinterpret_cast<const dev::StepHdr*>(e->h_in);
+        fill_info(e, hdr->layer, nullptr, groups, head_scores, counters, nullptr);
+    });
+}
+
+size_t sinkr_rank_partial_floats(sinkr_engine* e) { return e ? e->U * e->PS : 0; }
+
+sinkr_status sinkr_decode_rank_partial_async(sinkr_engine* e, const float* d_queries,
+                                             size_t layer, const sinkr_routing_config* config,
+                                             const sinkr_engine_options* options,
+                                             float* d_partial) {
+    return guard([&] {
+        if (!e || !d_queries || !d_partial) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        stage_params(e, layer, config, options, false);
+        run_graph(e, d_queries, d_partial, 1);
+    });
+}
+
+sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gathered,
+                                             size_t num_ranks, float* d_outputs) {
+    return guard([&] {
+        if (!e || !d_gathered || !d_outputs || num_ranks == 0)
+            fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        const dev::DevTables t = e->tables(nullptr);
+        launch_combine(e, t, d_gathered, e->PS, e->U * e->PS, (uint32_t)num_ranks, d_outputs, 0,
+                       num_ranks);
+        CK(cudaGetLastError());
+    });
+}
+
+sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches, float* decode_ms,
+                                   float* step_ms) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        CK(cudaStreamSynchronize(e->stream));
+        if (kernel_launches) *kernel_launches = e->last_launches;
+        if (decode_ms) {
+            *decode_ms = 0.f;
+            if (e->timing) CK(cudaEventElapsedTime(decode_ms, e->ev[1], e->ev[2]));
+        }
+        if (step_ms) CK(cudaEventElapsedTime(step_ms, e->ev[0], e->ev[3]));
+    });
+}
+
+sinkr_status sinkr_set_timing(sinkr_engine* e, int enabled) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        e->timing = enabled != 0;
+    });
+}
+
+}  // extern "C"

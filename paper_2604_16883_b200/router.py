@@ -1,0 +1,382 @@
+"""Host-side mirror of the reference's operator API (router.hpp, kv_cache.hpp,
+calibration.hpp's ThresholdProfile, counters.hpp), backed by the sm_100a engine
+through the C-ABI in include/sinkr_cuda.h.
+
+Names, argument meaning and error behaviour follow the reference:
+
+=============================  ===============================================
+reference                      here
+=============================  ===============================================
+CacheConfig (kv_cache.hpp:13)  CacheConfig (+ num_seqs for batched caches)
+KvCache (kv_cache.hpp:42-80)   KvCache — bf16 K/V resident in HBM
+ThresholdProfile (calib.:21)   ThresholdProfile, ThresholdProfile.constant
+RoutingConfig (router.hpp:16)  RoutingConfig, RoutingConfig.from_profile
+EngineOptions (router.hpp:69)  EngineOptions (+ global_context_len)
+threshold_for_length / route   threshold_for_length / route (host scalar logic)
+auto_num_splits / split_ranges auto_num_splits / split_ranges
+routed_decode_step (:84-86)    routed_decode_step  -> LayerStepResult
+=============================  ===============================================
+
+Exceptions: std::invalid_argument -> ValueError, std::out_of_range ->
+IndexError, std::runtime_error -> RuntimeError, std::logic_error ->
+LogicError (an AssertionError subclass).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import check, lib
+
+kDefaultBlockSize = 128  # attention.hpp:35
+
+
+# ----------------------------------------------------------------------------
+# configuration types
+@dataclass
+class CacheConfig:
+    num_layers: int = 0
+    num_q_heads: int = 0
+    num_kv_heads: int = 0
+    head_dim: int = 0
+    capacity: int = 0
+    num_seqs: int = 1
+
+    def group_width(self) -> int:
+        return self.num_q_heads // self.num_kv_heads
+
+
+@dataclass
+class ThresholdProfile:
+    coeffs: Sequence[float] = (0.0, 0.0, 0.0, 0.0)
+    length_normalizer: float = 1.0
+    clamp_lo: float = 0.0
+    clamp_hi: float = 1.0
+    target_skip: float = 0.60
+    gamma: float = 0.65
+    excluded_layers: Sequence[int] = (0, 1)
+    points: list = field(default_factory=list)
+
+    @staticmethod
+    def constant(tau: float) -> "ThresholdProfile":
+        """calibration.cpp:29-35 — clamp widened so tau outside [0,1] holds."""
+        return ThresholdProfile(coeffs=(0.0, 0.0, 0.0, float(tau)),
+                                clamp_lo=min(tau, 0.0), clamp_hi=max(tau, 1.0))
+
+    def _c(self) -> _abi.ThresholdProfileC:
+        p = _abi.ThresholdProfileC()
+        for i in range(4):
+            p.coeffs[i] = float(self.coeffs[i])
+        p.length_normalizer = float(self.length_normalizer)
+        p.clamp_lo = float(self.clamp_lo)
+        p.clamp_hi = float(self.clamp_hi)
+        return p
+
+
+@dataclass
+class RoutingConfig:
+    gamma: float = 0.65
+    profile: ThresholdProfile = field(default_factory=ThresholdProfile)
+    excluded_layers: Sequence[int] = (0, 1)
+    sink_on_tie: bool = False
+
+    @staticmethod
+    def from_profile(profile: ThresholdProfile) -> "RoutingConfig":
+        """router.cpp:23-29."""
+        return RoutingConfig(gamma=profile.gamma, profile=profile,
+                             excluded_layers=tuple(profile.excluded_layers))
+
+    def layer_excluded(self, layer: int) -> bool:
+        return layer in tuple(self.excluded_layers)
+
+    def _c(self):
+        arr = (C.c_size_t * max(1, len(self.excluded_layers)))(*self.excluded_layers)
+        c = _abi.RoutingConfigC()
+        c.gamma = float(self.gamma)
+        c.profile = self.profile._c()
+        c.excluded_layers = C.cast(arr, C.POINTER(C.c_size_t))
+        c.num_excluded_layers = len(self.excluded_layers)
+        c.sink_on_tie = int(bool(self.sink_on_tie))
+        return c, arr  # keep `arr` alive for the duration of the call
+
+
+@dataclass
+class EngineOptions:
+    num_splits: int = 0
+    block_size: int = kDefaultBlockSize
+    observe_only: bool = False
+    global_context_len: int = 0
+
+    def _c(self) -> _abi.EngineOptionsC:
+        o = _abi.EngineOptionsC()
+        o.num_splits = int(self.num_splits)
+        o.block_size = int(self.block_size)
+        o.observe_only = int(bool(self.observe_only))
+        o.global_context_len = int(self.global_context_len)
+        return o
+
+
+# ----------------------------------------------------------------------------
+# result types (router.hpp:28-39,56-67; counters.hpp:9-28)
+@dataclass
+class LoadCounters:
+    kv_floats_loaded: int = 0
+    anchor_floats_loaded: int = 0
+    groups_active: int = 0
+    groups_skipped: int = 0
+    routing_seconds: float = 0.0
+    attention_seconds: float = 0.0
+    merge_seconds: float = 0.0
+
+
+@dataclass
+class RouteDecision:
+    group_score: float = 0.0
+    threshold: float = 0.0
+    sink: bool = False
+    degenerate: bool = False
+    head_scores: List[float] = field(default_factory=list)
+
+
+@dataclass
+class GroupStepInfo:
+    layer: int = 0
+    kv_head: int = 0
+    decision: RouteDecision = field(default_factory=RouteDecision)
+    kv_floats_loaded: int = 0
+    tokens_loaded: int = 0
+    seq: int = 0
+
+
+@dataclass
+class LayerStepResult:
+    outputs: np.ndarray  # [H_q, D] (or [B, H_q, D] for batched caches)
+    groups: List[GroupStepInfo]
+    counters: LoadCounters
+
+    @property
+    def route_bitmap(self) -> np.ndarray:
+        """Sink bit per group (the routing decision the probe kernel emits)."""
+        return np.array([g.decision.sink for g in self.groups], dtype=bool)
+
+
+# ----------------------------------------------------------------------------
+# host scalar helpers (router.hpp:47-54,78; attention.hpp:82-85)
+def threshold_for_length(context_len: int, profile: ThresholdProfile) -> float:
+    out = C.c_double()
+    p = profile._c()
+    check(lib().sinkr_threshold_for_length(C.c_size_t(context_len), C.byref(p), C.byref(out)))
+    return out.value
+
+
+def route(layer: int, score: float, context_len: int, config: RoutingConfig) -> RouteDecision:
+    c, keep = config._c()
+    sink, tau = C.c_int(), C.c_double()
+    check(lib().sinkr_route(C.c_size_t(layer), C.c_double(score), C.c_size_t(context_len),
+                            C.byref(c), C.byref(sink), C.byref(tau)))
+    del keep
+    return RouteDecision(group_score=score, threshold=tau.value, sink=bool(sink.value))
+
+
+def auto_num_splits(context_len: int) -> int:
+    return int(lib().sinkr_auto_num_splits(C.c_size_t(context_len)))
+
+
+def split_ranges(length: int, num_splits: int):
+    buf = (C.c_size_t * (2 * max(1, num_splits)))()
+    check(lib().sinkr_split_ranges(C.c_size_t(length), C.c_size_t(num_splits), buf))
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(num_splits)]
+
+
+# ----------------------------------------------------------------------------
+class KvCache:
+    """kv_cache.hpp:42-80 on the GPU: bf16 K/V [layer][seq][kv_head][cap][D] in
+    HBM, f32 anchors captured at first append (kv_cache.cpp:71-77)."""
+
+    def __init__(self, config: CacheConfig, device: int = 0):
+        self._h = None
+        self._config = config
+        cc = _abi.CacheConfigC(config.num_layers, config.num_q_heads, config.num_kv_heads,
+                               config.head_dim, config.capacity, config.num_seqs or 1)
+        h = C.c_void_p()
+        check(lib().sinkr_engine_create(C.byref(cc), C.c_int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+        self.B = config.num_seqs or 1
+        self._keep = []
+
+    # -- lifetime
+    def close(self):
+        if self._h:
+            lib().sinkr_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def config(self) -> CacheConfig:
+        return self._config
+
+    @property
+    def stream(self) -> int:
+        return int(lib().sinkr_engine_stream(self._h) or 0)
+
+    def decode_grid(self) -> int:
+        return int(lib().sinkr_decode_grid(self._h))
+
+    # -- KvCache API
+    def append(self, layer: int, kv_head: int, k, v, seq: int = 0) -> None:
+        """Append one row (D,) or rows (n, D) of f32 keys/values."""
+        d = self._config.head_dim
+        k = np.ascontiguousarray(k, dtype=np.float32).reshape(-1)
+        v = np.ascontiguousarray(v, dtype=np.float32).reshape(-1)
+        if k.size != v.size or k.size % d != 0 or k.size == 0:
+            raise ValueError("k/v row size does not match head_dim")
+        check(lib().sinkr_kv_append(self._h, C.c_size_t(seq), C.c_size_t(layer),
+                                    C.c_size_t(kv_head), k.ctypes.data_as(C.c_void_p),
+                                    v.ctypes.data_as(C.c_void_p), C.c_size_t(k.size // d)))
+
+    def append_device_bf16(self, layer: int, kv_head: int, k_ptr: int, v_ptr: int, rows: int,
+                           seq: int = 0) -> None:
+        check(lib().sinkr_kv_append_device_bf16(self._h, C.c_size_t(seq), C.c_size_t(layer),
+                                                C.c_size_t(kv_head), C.c_void_p(k_ptr),
+                                                C.c_void_p(v_ptr), C.c_size_t(rows)))
+
+    def append_synthetic(self, layer: int, kv_head: int, key_k: int, key_v: int, rows: int,
+                         k_scale: float = 1.0, v_scale: float = 1.0, seq: int = 0) -> None:
+        check(lib().sinkr_kv_append_synthetic(
+            self._h, C.c_size_t(seq), C.c_size_t(layer), C.c_size_t(kv_head),
+            C.c_uint64(key_k), C.c_uint64(key_v), C.c_float(k_scale), C.c_float(v_scale),
+            C.c_size_t(rows)))
+
+    def length(self, layer: int, kv_head: int, seq: int = 0) -> int:
+        out = C.c_size_t()
+        check(lib().sinkr_kv_length(self._h, C.c_size_t(seq), C.c_size_t(layer),
+                                    C.c_size_t(kv_head), C.byref(out)))
+        return out.value
+
+    def token_count(self, seq: int = 0) -> int:
+        out = C.c_size_t()
+        check(lib().sinkr_kv_token_count(self._h, C.c_size_t(seq), C.byref(out)))
+        return out.value
+
+    def anchor(self, layer: int, kv_head: int, seq: int = 0):
+        k0 = np.zeros(self._config.head_dim, dtype=np.float32)
+        n = C.c_float()
+        check(lib().sinkr_kv_anchor(self._h, C.c_size_t(seq), C.c_size_t(layer),
+                                    C.c_size_t(kv_head), k0.ctypes.data_as(C.c_void_p),
+                                    C.byref(n)))
+        return k0, n.value
+
+    def set_anchor(self, layer: int, kv_head: int, k0, k0_norm: float, seq: int = 0) -> None:
+        k0 = np.ascontiguousarray(k0, dtype=np.float32)
+        check(lib().sinkr_kv_set_anchor(self._h, C.c_size_t(seq), C.c_size_t(layer),
+                                        C.c_size_t(kv_head), k0.ctypes.data_as(C.c_void_p),
+                                        C.c_float(k0_norm)))
+
+    def historical(self, layer: int, kv_head: int, frm: int, to: int, seq: int = 0):
+        """Rows [frm, to) of K and V as f32 (exact upcast of the stored bf16)."""
+        d = self._config.head_dim
+        k = np.zeros((to - frm, d), dtype=np.float32)
+        v = np.zeros((to - frm, d), dtype=np.float32)
+        check(lib().sinkr_kv_read(self._h, C.c_size_t(seq), C.c_size_t(layer),
+                                  C.c_size_t(kv_head), C.c_size_t(frm), C.c_size_t(to),
+                                  k.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p)))
+        return k, v
+
+
+# ----------------------------------------------------------------------------
+def _step_buffers(cache: KvCache):
+    cc = cache.config()
+    B = cache.B
+    out = np.zeros((B, cc.num_q_heads, cc.head_dim), dtype=np.float32)
+    groups = (_abi.GroupInfoC * (B * cc.num_kv_heads))()
+    hs = np.zeros(B * cc.num_q_heads, dtype=np.float64)
+    ctr = _abi.LoadCountersC()
+    return out, groups, hs, ctr
+
+
+def _to_result(cache: KvCache, out, groups, hs, ctr, batched: bool) -> LayerStepResult:
+    cc = cache.config()
+    r = cc.group_width()
+    infos = []
+    for u in range(cache.B * cc.num_kv_heads):
+        g = groups[u]
+        seq = u // cc.num_kv_heads
+        h0 = seq * cc.num_q_heads + g.kv_head * r
+        dec = RouteDecision(group_score=g.group_score, threshold=g.threshold, sink=bool(g.sink),
+                            degenerate=bool(g.degenerate), head_scores=list(hs[h0:h0 + r]))
+        infos.append(GroupStepInfo(layer=g.layer, kv_head=g.kv_head, decision=dec,
+                                   kv_floats_loaded=int(g.kv_floats_loaded),
+                                   tokens_loaded=int(g.tokens_loaded), seq=seq))
+    counters = LoadCounters(int(ctr.kv_floats_loaded), int(ctr.anchor_floats_loaded),
+                            int(ctr.groups_active), int(ctr.groups_skipped),
+                            ctr.routing_seconds, ctr.attention_seconds, ctr.merge_seconds)
+    return LayerStepResult(outputs=out if batched else out[0], groups=infos, counters=counters)
+
+
+def routed_decode_step(queries, layer: int, cache: KvCache, config: RoutingConfig,
+                       options: Optional[EngineOptions] = None) -> LayerStepResult:
+    """router.hpp:84-86 — one decode step for one layer (all B sequences).
+
+    queries: f32 [H_q, D] (or [B, H_q, D] for a batched cache), host memory.
+    """
+    cc = cache.config()
+    q = np.ascontiguousarray(queries, dtype=np.float32)
+    if q.size != cache.B * cc.num_q_heads * cc.head_dim:
+        raise ValueError("queries span must be H_q x D for one layer")
+    out, groups, hs, ctr = _step_buffers(cache)
+    c, keep = config._c()
+    o = (options or EngineOptions())._c()
+    check(lib().sinkr_routed_decode_batch(cache.handle, q.ctypes.data_as(C.c_void_p),
+                                          C.c_size_t(layer), C.byref(c), C.byref(o),
+                                          out.ctypes.data_as(C.c_void_p), groups,
+                                          hs.ctypes.data_as(C.c_void_p), C.byref(ctr)))
+    del keep
+    return _to_result(cache, out, groups, hs, ctr, batched=cache.B > 1 or q.ndim == 3)
+
+
+def routed_decode_async(d_queries: int, layer: int, cache: KvCache, config: RoutingConfig,
+                        options: Optional[EngineOptions] = None, d_outputs: int = 0) -> None:
+    """Device-resident step: enqueue on the engine stream, no host sync."""
+    c, keep = config._c()
+    o = (options or EngineOptions())._c()
+    check(lib().sinkr_routed_decode_async(cache.handle, C.c_void_p(d_queries),
+                                          C.c_size_t(layer), C.byref(c), C.byref(o),
+                                          C.c_void_p(d_outputs)))
+    del keep
+
+
+def fetch_step_info(cache: KvCache) -> LayerStepResult:
+    out, groups, hs, ctr = _step_buffers(cache)
+    check(lib().sinkr_fetch_step_info(cache.handle, groups, hs.ctypes.data_as(C.c_void_p),
+                                      C.byref(ctr)))
+    return _to_result(cache, None, groups, hs, ctr, batched=True)
+
+
+def last_step_stats(cache: KvCache):
+    n = C.c_uint32()
+    dms, sms = C.c_float(), C.c_float()
+    check(lib().sinkr_last_step_stats(cache.handle, C.byref(n), C.byref(dms), C.byref(sms)))
+    return int(n.value), float(dms.value), float(sms.value)
+
+
+def set_timing(cache: KvCache, enabled: bool) -> None:
+    check(lib().sinkr_set_timing(cache.handle, C.c_int(int(enabled))))

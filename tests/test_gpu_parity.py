@@ -1,0 +1,282 @@
+"""Parity of the sm_100a engine (through the C-ABI) with the CPU oracle.
+
+Bar (north star): route bitmaps, group/head scores and per-group loaded-token
+counts bit-exact; outputs within max-abs 2e-3 and rel-L2 1e-3 of the
+reference; Sink rows bitwise zero.  The oracle is the C restatement, itself
+pinned bit-exactly to the compiled reference in tests/test_oracle.py; a few
+cases also run the compiled reference (oracle/_ref) directly.
+"""
+import numpy as np
+import pytest
+
+import paper_2604_16883_b200 as P
+from paper_2604_16883_b200.workload import WorkloadSpec
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-3
+REL_L2 = 1e-3
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / den if den > 0 else np.linalg.norm(a - b)
+
+
+def oracle_profile(prof):
+    import oracle
+
+    return oracle.Profile(tuple(prof.coeffs), prof.length_normalizer, prof.clamp_lo,
+                          prof.clamp_hi)
+
+
+def make_cache(spec: WorkloadSpec):
+    cc = P.CacheConfig(spec.num_layers, spec.num_q_heads, spec.num_kv_heads, spec.head_dim,
+                       spec.capacity or spec.length, spec.num_seqs)
+    cache = P.KvCache(cc)
+    spec.fill(cache)
+    return cache
+
+
+def oracle_step(orc, spec, seq, q, cfg: P.RoutingConfig, opts: P.EngineOptions, kv=None,
+                length=None):
+    k, v = kv if kv is not None else spec.host_cache(seq)
+    k0 = k[:, 0, :].copy()
+    k0n = np.array([orc.anchor_norm(k0[g]) for g in range(k.shape[0])], dtype=np.float32)
+    return orc.routed_decode_step(
+        k, v, k0, k0n, q, spec.layer, oracle_profile(cfg.profile),
+        excluded=tuple(cfg.excluded_layers), sink_on_tie=cfg.sink_on_tie,
+        num_splits=opts.num_splits, block=opts.block_size, observe_only=opts.observe_only,
+        threads=8)
+
+
+def assert_parity(res, ref, r, D, seq_groups):
+    # routing: bit-exact
+    sink = np.array([g.decision.sink for g in seq_groups], dtype=np.int32)
+    np.testing.assert_array_equal(sink, ref.sink)
+    np.testing.assert_array_equal([g.decision.degenerate for g in seq_groups], ref.degenerate)
+    gs = np.array([g.decision.group_score for g in seq_groups])
+    assert gs.tobytes() == ref.group_scores.tobytes(), (gs, ref.group_scores)
+    th = np.array([g.decision.threshold for g in seq_groups])
+    assert th.tobytes() == ref.thresholds.tobytes()
+    hs = np.concatenate([g.decision.head_scores for g in seq_groups])
+    assert hs.tobytes() == ref.head_scores.tobytes()
+    # skipped-block record: per-group loaded floats exact
+    np.testing.assert_array_equal([g.kv_floats_loaded for g in seq_groups], ref.group_kv_floats)
+    # outputs
+    out = np.asarray(res, np.float32)
+    for gi, g in enumerate(seq_groups):
+        rows = slice(gi * r, (gi + 1) * r)
+        if ref.sink[gi] and not ref.group_kv_floats[gi]:
+            assert not np.any(out[rows].view(np.uint32)), "Sink rows must be bitwise +0"
+    err = np.abs(out - ref.outputs).max()
+    assert err <= MAX_ABS, err
+    assert rel_l2(out, ref.outputs) <= REL_L2
+
+
+CASES = [
+    # (hq, hkv, D, L, p)
+    (32, 8, 128, 1, 0.0),
+    (32, 8, 128, 7, 0.0),
+    (32, 8, 128, 64, 0.5),
+    (32, 8, 128, 1000, 0.5),
+    (32, 8, 128, 4096, 0.625),
+    (32, 4, 128, 3000, 0.5),     # r = 8 (Yi / 70B width)
+    (40, 40, 128, 2048, 0.5),    # r = 1 (MHA, LLaVA)
+    (8, 8, 64, 1500, 0.25),      # D = 64
+    (16, 4, 32, 777, 0.5),       # D = 32
+    (12, 4, 128, 333, 0.5),      # r = 3 (padded MMA rows)
+]
+
+
+@pytest.mark.parametrize("hq,hkv,D,L,p", CASES)
+def test_planted_parity(oracle_libs, hq, hkv, D, L, p):
+    _, orc = oracle_libs
+    spec = WorkloadSpec(num_q_heads=hq, num_kv_heads=hkv, head_dim=D, length=L, sink_fraction=p,
+                        seed=L + hq)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    opts = P.EngineOptions()
+    q = spec.queries()[0]
+    with make_cache(spec) as cache:
+        res = P.routed_decode_step(q, spec.layer, cache, cfg, opts)
+        ref = oracle_step(orc, spec, 0, q, cfg, opts)
+        assert_parity(res.outputs, ref, spec.r, D, res.groups)
+        assert res.counters.kv_floats_loaded == ref.counters["kv_floats_loaded"]
+        assert res.counters.groups_active == ref.counters["groups_active"]
+        assert res.counters.groups_skipped == ref.counters["groups_skipped"]
+        assert res.counters.anchor_floats_loaded == ref.counters["anchor_floats_loaded"]
+
+
+def test_device_generator_matches_host(oracle_libs):
+    spec = WorkloadSpec(num_q_heads=8, num_kv_heads=2, head_dim=128, length=300, seed=7)
+    with make_cache(spec) as cache:
+        for g in range(2):
+            k, v = cache.historical(spec.layer, g, 0, spec.length)
+            hk, hv = spec.host_slot(0, g)
+            assert k.tobytes() == hk.tobytes() and v.tobytes() == hv.tobytes()
+            k0, n = cache.anchor(spec.layer, g)
+            assert k0.tobytes() == hk[0].tobytes()
+            assert n == np.float32(oracle_libs[1].anchor_norm(hk[0]))
+
+
+def test_random_dense_vs_reference(oracle_libs):
+    """Diffuse random caches (no planted sink), tau > 1: compare with the
+    compiled reference's routed_decode_step directly."""
+    import oracle
+
+    ref_lib, _ = oracle_libs
+    if ref_lib is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(3)
+    hq, hkv, D, L = 32, 8, 128, 2500
+    k = rng.standard_normal((hkv, L, D)).astype(np.float32)
+    v = rng.standard_normal((hkv, L, D)).astype(np.float32)
+    from paper_2604_16883_b200.workload import round_bf16
+
+    k, v = round_bf16(k).reshape(k.shape), round_bf16(v).reshape(v.shape)
+    q = rng.standard_normal((hq, D)).astype(np.float32) * 3
+    rc = oracle.RefCache(ref_lib, 1, hq, hkv, D, L)
+    with P.KvCache(P.CacheConfig(1, hq, hkv, D, L)) as cache:
+        for g in range(hkv):
+            cache.append(0, g, k[g], v[g])
+            rc.append_rows(0, g, k[g], v[g])
+        cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(2.0))
+        res = P.routed_decode_step(q, 0, cache, cfg)
+        ref = rc.routed_decode_step(q, 0, oracle.Profile.constant(2.0), workers=8)
+        assert_parity(res.outputs, ref, hq // hkv, D, res.groups)
+
+
+@pytest.mark.parametrize("tau,expect_all_sink", [(2.0, False), (-2.0, True)])
+def test_routing_limits(oracle_libs, tau, expect_all_sink):
+    """tau > 1 -> all Active; tau < -1 -> all Sink, zeros,
+    kv_floats == 0."""
+    spec = WorkloadSpec(num_q_heads=32, num_kv_heads=8, head_dim=128, length=513,
+                        sink_fraction=0.5)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(tau), excluded_layers=())
+    with make_cache(spec) as cache:
+        res = P.routed_decode_step(spec.queries()[0], 0, cache, cfg)
+        sinks = res.route_bitmap
+        assert sinks.all() == expect_all_sink and sinks.any() == expect_all_sink
+        if expect_all_sink:
+            assert not np.any(res.outputs.view(np.uint32))
+            assert res.counters.kv_floats_loaded == 0
+            assert res.counters.groups_skipped == 8
+        else:
+            assert res.counters.kv_floats_loaded == 8 * 2 * 513 * 128
+
+
+def test_excluded_layers_and_observe_only(oracle_libs):
+    _, orc = oracle_libs
+    spec = WorkloadSpec(num_q_heads=32, num_kv_heads=8, head_dim=128, length=900,
+                        sink_fraction=0.5)
+    q = spec.queries()[0]
+    with make_cache(spec) as cache:
+        # default RoutingConfig excludes layers {0,1}: nothing skips on layer 0
+        cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5))
+        res = P.routed_decode_step(q, 0, cache, cfg)
+        assert not res.route_bitmap.any()
+        ref = oracle_step(orc, spec, 0, q, cfg, P.EngineOptions())
+        assert_parity(res.outputs, ref, 4, 128, res.groups)
+        # observe_only: decisions recorded, every group attends, none skipped
+        cfg2 = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+        opts = P.EngineOptions(observe_only=True)
+        res2 = P.routed_decode_step(q, 0, cache, cfg2, opts)
+        ref2 = oracle_step(orc, spec, 0, q, cfg2, opts)
+        assert res2.route_bitmap.sum() == 4
+        assert res2.counters.groups_skipped == 0 and res2.counters.groups_active == 8
+        assert_parity(res2.outputs, ref2, 4, 128, res2.groups)
+
+
+def test_tie_and_sink_on_tie(oracle_libs):
+    """q=[3,4,...], k0=[1,0,...] gives S == 0.6 exactly; tau = 0.6 ties."""
+    _, orc = oracle_libs
+    D, hq, hkv, L = 64, 4, 1, 80
+    k0 = np.zeros(D, np.float32)
+    k0[0] = 1.0
+    rng = np.random.default_rng(5)
+    k = np.vstack([k0, rng.standard_normal((L - 1, D)).astype(np.float32)])
+    v = rng.standard_normal((L, D)).astype(np.float32)
+    from paper_2604_16883_b200.workload import round_bf16
+
+    k, v = round_bf16(k).reshape(L, D), round_bf16(v).reshape(L, D)
+    q = np.zeros((hq, D), np.float32)
+    q[:, 0], q[:, 1] = 3.0, 4.0
+    with P.KvCache(P.CacheConfig(1, hq, hkv, D, L)) as cache:
+        cache.append(0, 0, k, v)
+        for tie in (False, True):
+            cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.6), excluded_layers=(),
+                                  sink_on_tie=tie)
+            res = P.routed_decode_step(q, 0, cache, cfg)
+            assert res.groups[0].decision.group_score == 0.6
+            assert res.groups[0].decision.sink == tie
+            ref = orc.routed_decode_step(k[None], v[None], k[None, 0], [orc.anchor_norm(k[0])], q,
+                                         0, __import__("oracle").Profile.constant(0.6),
+                                         excluded=(), sink_on_tie=tie)
+            assert_parity(res.outputs, ref, hq, D, res.groups)
+
+
+def test_degenerate_query_forces_active(oracle_libs):
+    _, orc = oracle_libs
+    spec = WorkloadSpec(num_q_heads=8, num_kv_heads=2, head_dim=128, length=200,
+                        sink_fraction=1.0)
+    q = spec.queries()[0]
+    q[1] = 0.0  # head 1 of group 0 degenerate
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    with make_cache(spec) as cache:
+        res = P.routed_decode_step(q, 0, cache, cfg)
+        assert res.groups[0].decision.degenerate and not res.groups[0].decision.sink
+        assert res.groups[0].decision.head_scores[1] == 0.0
+        assert res.groups[1].decision.sink
+        ref = oracle_step(orc, spec, 0, q, cfg, P.EngineOptions())
+        assert_parity(res.outputs, ref, 4, 128, res.groups)
+
+
+def test_batched_sequences(oracle_libs):
+    """B independent caches in one launch."""
+    _, orc = oracle_libs
+    spec = WorkloadSpec(num_q_heads=16, num_kv_heads=4, head_dim=128, length=640, num_seqs=3,
+                        sink_fraction=0.5, seed=11)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    qs = spec.queries()
+    with make_cache(spec) as cache:
+        res = P.routed_decode_step(qs, 0, cache, cfg)
+        assert res.outputs.shape == (3, 16, 128)
+        for s in range(3):
+            ref = oracle_step(orc, spec, s, qs[s], cfg, P.EngineOptions())
+            assert_parity(res.outputs[s], ref, 4, 128, res.groups[s * 4:(s + 1) * 4])
+
+
+def test_errors_mirror_reference():
+    spec = WorkloadSpec(num_q_heads=8, num_kv_heads=2, head_dim=64, length=10)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5))
+    with P.KvCache(P.CacheConfig(2, 8, 2, 64, 16)) as cache:
+        q = spec.queries()[0]
+        with pytest.raises(RuntimeError, match="empty cache"):
+            P.routed_decode_step(q, 0, cache, cfg)
+        with pytest.raises(IndexError):
+            P.routed_decode_step(q, 5, cache, cfg)
+        with pytest.raises(ValueError):
+            P.routed_decode_step(q[:3], 0, cache, cfg)
+        with pytest.raises(RuntimeError, match="degenerate anchor"):
+            cache.append(0, 0, np.zeros(64), np.ones(64))
+        cache.append(0, 0, np.ones((3, 64)), np.ones((3, 64)))
+        from paper_2604_16883_b200._abi import LogicError
+
+        with pytest.raises(LogicError):
+            cache.token_count()
+        with pytest.raises(RuntimeError, match="overflow"):
+            cache.append(0, 0, np.ones((14, 64)), np.ones((14, 64)))
+
+
+def test_timings_and_launch_count():
+    spec = WorkloadSpec(num_q_heads=32, num_kv_heads=8, head_dim=128, length=4096,
+                        sink_fraction=0.5)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    with make_cache(spec) as cache:
+        res = P.routed_decode_step(spec.queries()[0], 0, cache, cfg)
+        c = res.counters
+        assert c.routing_seconds > 0 and c.attention_seconds > 0 and c.merge_seconds > 0
+        n, dms, sms = P.last_step_stats(cache)
+        assert n == 3 and 0 < dms <= sms
