@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""bench.py — SinkRouter sink-aware decode attention on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the headline): Llama-3.1-8B attention shape
+(32 q / 8 KV heads, D=128), batch 1, one layer, L=524,288 synthetic tokens with a
+planted BOS sink in every group; routed fraction 5/8 (62.5 %, the paper's ~60 %
+operating point) under tau = 0.5, versus the engine's own dense path (tau = 2,
+routing disabled).  One "step" = probe -> Split-K flash-decode -> LSE combine for
+one decode token.
+
+  value  = routed decode-step latency, us/step, inputs resident in HBM
+           (engine-owned KV cache, device queries), CUDA-graph replay timed with
+           CUDA events on the engine stream over K back-to-back steps.
+  e2e    = the same step through the public C-ABI call (sinkr_routed_decode_step)
+           with HOST queries/outputs: H2D of queries+params and D2H of the
+           outputs+routing record inside the timed region, wall clock.
+  roofline: decode kernel, algorithmic bytes (Active groups' bf16 K+V + q) per
+           launch / its CUDA-event duration, vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline: the compiled reference (oracle/_ref, routed_decode_step with
+           ThreadPool(nproc)) on the same workload, bounded sample of steps.
+
+`--impl reference` times the reference's own CPU implementation on this box's
+host cores at the same config.  Multi-GPU (torchrun, N>1): the sequence is
+sharded across ranks (each rank streams L/N tokens of every Active group), the
+per-rank LSE partials are all-gathered with NCCL and merged on device; value is
+the max over ranks (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("decode-attn µs/step & KV GB/s (% HBM peak) at 512K; "
+          "speedup vs own dense path")
+UNIT = "us/step"
+SHAPE = dict(num_q_heads=32, num_kv_heads=8, head_dim=128)  # Llama-3.1-8B
+L2_BYTES = 126 * 1024 * 1024
+FALLBACK_PEAK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--length", type=int, default=524288)
+    ap.add_argument("--sink-fraction", type=float, default=0.625)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_PEAK_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# reference (CPU) side: the compiled reference on identical inputs
+def fill_ref_cache(spec, threads):
+    """Build the reference KvCache (oracle/_ref) holding exactly the tokens the
+    GPU engine holds: planted row 0 + rows generated by the C restatement of
+    the device generator (bit-identical bf16 values)."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    ref, orc = oracle.ref(), oracle.orc()
+    D, L = spec.head_dim, spec.length
+    rc = oracle.RefCache(ref, 1, spec.num_q_heads, spec.num_kv_heads, D, L)
+
+    def slot(g):
+        k0, v0 = spec.first_rows(0, g)
+        kk, kv = spec.slot_keys(0, g)
+        k = np.empty((L, D), np.float32)
+        v = np.empty((L, D), np.float32)
+        k[0], v[0] = k0, v0
+        if L > 1:
+            for key, dst in ((kk, k), (kv, v)):
+                orc.lib.orc_fill_rows(C.c_uint64(key), C.c_size_t(1), C.c_size_t(L - 1),
+                                      C.c_size_t(D), C.c_float(1.0),
+                                      dst[1:].ctypes.data_as(C.c_void_p))
+        return g, k, v
+
+    with ThreadPoolExecutor(max_workers=min(threads, spec.num_kv_heads)) as ex:
+        for g, k, v in ex.map(slot, range(spec.num_kv_heads)):
+            rc.append_rows(0, g, k, v)
+            del k, v
+    return rc
+
+
+def time_reference(spec, steps, warmup, threads):
+    import oracle
+
+    rc = fill_ref_cache(spec, threads)
+    q = spec.queries()[0]
+    prof = oracle.Profile.constant(0.5)
+    for _ in range(warmup):
+        rc.routed_decode_step(q, 0, prof, excluded=(), workers=threads)
+    ts = []
+    res = None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        res = rc.routed_decode_step(q, 0, prof, excluded=(), workers=threads)
+        ts.append(time.perf_counter() - t0)
+    return rc, res, ts
+
+
+# ----------------------------------------------------------------------------
+def run_reference_arm(args, world, rank):
+    from paper_2604_16883_b200.workload import WorkloadSpec
+
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    spec = WorkloadSpec(**SHAPE, length=args.length, sink_fraction=args.sink_fraction,
+                        seed=args.seed)
+    steps = max(1, min(args.steps, 10))
+    warm = max(0, min(args.warmup, 1))
+    _, res, ts = time_reference(spec, steps, warm, threads)
+    us = sum(ts) / len(ts) * 1e6
+    n_act = int(res.counters["groups_active"])
+    kv_bytes = n_act * 2 * args.length * SHAPE["head_dim"] * 4  # f32 as the reference stores
+    line = {
+        "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": warm, "ms_per_step": round(us / 1e3, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic planted-sink KV (seeded), host f32",
+        "config": {"workload": f"llama3.1-8b-attn L={args.length} B=1 routed={args.sink_fraction}",
+                   "shape": "32q/8kv/D128", "context": args.length,
+                   "sink_fraction": args.sink_fraction, "tau": 0.5},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{steps} routed_decode_step calls of the compiled reference "
+                                   f"(oracle/_ref, ThreadPool({threads})) at the full config"},
+        "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "kv_gbs_f32": round(kv_bytes / (us * 1e-6) / 1e9, 2),
+        "groups_active": n_act,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+def time_async(P, torch, cache, cfg, dq, dout, steps):
+    """K back-to-back graph replays, CUDA events on the engine stream."""
+    stream = torch.cuda.ExternalStream(cache.stream)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps  # ms
+
+
+def decode_kernel_ms(P, cache, cfg, dq, dout, steps):
+    """Average decode-kernel launch duration (CUDA events around the kernel on
+    the engine stream; eager launches, one step at a time)."""
+    P.set_timing(cache, True)
+    ds = []
+    for _ in range(steps):
+        P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+        _, dms, _ = P.last_step_stats(cache)
+        ds.append(dms)
+    P.set_timing(cache, False)
+    return float(np.mean(ds)), float(np.median(ds))
+
+
+def l2_flush(torch, buf):
+    buf.zero_()
+
+
+def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
+    """Context x routed-fraction sweep (BASELINE.json configs[1]); per-step
+    CUDA events with an L2 flush (256 MiB write) between steps."""
+    out = []
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for L in (65536, 131072, 524288):
+        if L == args.length and main_cache is not None:
+            cache = main_cache
+        else:
+            spec0 = spec_cls(**SHAPE, length=L, seed=args.seed)
+            cache = P.KvCache(P.CacheConfig(1, 32, 8, 128, L))
+            spec0.fill(cache)
+        stream = torch.cuda.ExternalStream(cache.stream)
+        P.set_timing(cache, False)
+        row = {"context": L, "points": []}
+        for k in range(0, 8):
+            p = k / 8
+            spec = spec_cls(**SHAPE, length=L, sink_fraction=p, seed=args.seed)
+            dq = torch.from_numpy(spec.queries()[0]).cuda()
+            dout = torch.empty_like(dq)
+            res = {}
+            for name, cfg in (("dense", dense_cfg), ("routed", routed_cfg)):
+                if name == "dense" and k > 0:
+                    continue
+                for _ in range(3):
+                    P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+                ts = []
+                for _ in range(10):
+                    l2_flush(torch, flush)
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    torch.cuda.synchronize()
+                    e0.record(stream)
+                    P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+                    e1.record(stream)
+                    e1.synchronize()
+                    ts.append(e0.elapsed_time(e1) * 1e3)
+                res[name] = statistics.median(ts)
+            info = P.fetch_step_info(cache)
+            n_act = info.counters.groups_active
+            if k == 0:
+                row["dense_us"] = round(res["dense"], 2)
+                dense_us = res["dense"]
+            kvb = n_act * 2 * L * 128 * 2
+            row["points"].append({
+                "routed_fraction": p, "groups_active": n_act, "us": round(res["routed"], 2),
+                "kv_gbs": round(kvb / (res["routed"] * 1e-6) / 1e9, 1),
+                "speedup_vs_dense": round(dense_us / res["routed"], 3)})
+        out.append(row)
+        if cache is not main_cache:
+            cache.close()
+    del flush
+    return out
+
+
+def run_ours(args, world, rank, local_rank):
+    import torch
+
+    import paper_2604_16883_b200 as P
+    from paper_2604_16883_b200.workload import WorkloadSpec
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    L = args.length
+    D = SHAPE["head_dim"]
+    spec = WorkloadSpec(**SHAPE, length=L, sink_fraction=args.sink_fraction, seed=args.seed)
+    routed_cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    dense_cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(2.0), excluded_layers=())
+    peak, peak_src = peak_hbm()
+
+    if world > 1:
+        from paper_2604_16883_b200 import sharding
+
+        result = sharding.bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg,
+                                                 args, rank, world, dev)
+        if rank == 0:
+            print(json.dumps(result), flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+
+    cache = P.KvCache(P.CacheConfig(1, 32, 8, D, L), device=dev)
+    spec.fill(cache)
+    q_host = spec.queries()[0]
+    dq = torch.from_numpy(q_host).cuda()
+    dout = torch.empty_like(dq)
+    P.set_timing(cache, False)
+
+    # warm-up (also instantiates the CUDA graphs)
+    for cfg in (routed_cfg, dense_cfg):
+        for _ in range(max(3, args.warmup)):
+            P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+    torch.cuda.synchronize()
+
+    # ---- headline timed region: routed
+    with ClockSampler(dev) as clk:
+        routed_ms = time_async(P, torch, cache, routed_cfg, dq, dout, args.steps)
+    info_r = P.fetch_step_info(cache)
+    dense_ms = time_async(P, torch, cache, dense_cfg, dq, dout, args.steps)
+    info_d = P.fetch_step_info(cache)
+    n_act = info_r.counters.groups_active
+    kv_routed = n_act * 2 * L * D * 2
+    kv_dense = info_d.counters.groups_active * 2 * L * D * 2
+
+    # ---- decode kernel launch duration (roofline numerator)
+    dec_mean_r, dec_med_r = decode_kernel_ms(P, cache, routed_cfg, dq, dout, args.steps)
+    dec_mean_d, dec_med_d = decode_kernel_ms(P, cache, dense_cfg, dq, dout, args.steps)
+    q_bytes = 32 * D * 4
+    alg_r = kv_routed + n_act * 4 * D * 4
+    alg_d = kv_dense + q_bytes
+    achieved = alg_r / (dec_mean_r * 1e-3) / 1e9
+    achieved_d = alg_d / (dec_mean_d * 1e-3) / 1e9
+
+    # ---- e2e through the public C-ABI call, host buffers
+    for _ in range(3):
+        P.routed_decode_step(q_host, 0, cache, routed_cfg)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res_host = P.routed_decode_step(q_host, 0, cache, routed_cfg)
+    e2e_us = (time.perf_counter() - t0) / args.steps * 1e6
+    h2d, d2h = cache.step_io_bytes()
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tr = json.load(f)
+            traffic = tr.get(f"routed_{L}_{args.sink_fraction}")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC,
+        "value": round(routed_ms * 1e3, 2),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(routed_ms, 5),
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic planted-sink KV (device generator, seeded); fp32 queries",
+        "config": {
+            "workload": f"llama3.1-8b-attn L={L} B=1 routed={args.sink_fraction}",
+            "shape": "32q/8kv/D128", "context": L, "batch": 1, "layers": 1,
+            "sink_fraction": args.sink_fraction, "tau": 0.5, "dense_tau": 2.0,
+            "parallelism": "single GPU",
+            "l2": f"inputs larger than L2 ({kv_routed >> 20} MiB routed / "
+                  f"{kv_dense >> 20} MiB dense KV vs 126 MB L2); sweep flushes L2",
+        },
+        "dense_us_per_step": round(dense_ms * 1e3, 2),
+        "speedup_vs_dense": round(dense_ms / routed_ms, 3),
+        "groups_active": n_act,
+        "kv_gbs_routed_step": round(kv_routed / (routed_ms * 1e-3) / 1e9, 1),
+        "kv_gbs_dense_step": round(kv_dense / (dense_ms * 1e-3) / 1e9, 1),
+        "dense_decode_kernel": {"us": round(dec_mean_d * 1e3, 2),
+                                "achieved_gbs": round(achieved_d, 1),
+                                "frac": round(achieved_d / peak, 4)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": "decode_kernel<128> (routed)",
+                     "kernel_us": round(dec_mean_r * 1e3, 2),
+                     "alg_bytes_per_launch": alg_r, "peak_source": peak_src},
+        "e2e": {"value": round(e2e_us, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk.summary(),
+    }
+
+    # ---- CPU baseline: the compiled reference on this host, same workload
+    if not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            _, ref, ts = time_reference(spec, args.cpu_steps, 0, threads)
+            cpu_us = statistics.median(ts) * 1e6
+            line["cpu_baseline"] = {
+                "value": round(cpu_us, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"{args.cpu_steps} routed_decode_step calls of the compiled reference "
+                          f"(oracle/_ref, ThreadPool({threads})) at the full config, median"}
+            out = res_host.outputs
+            sink = np.array([g.decision.sink for g in res_host.groups], dtype=np.int32)
+            err = float(np.abs(out - ref.outputs).max())
+            rel = float(np.linalg.norm(out - ref.outputs) / max(np.linalg.norm(ref.outputs), 1e-30))
+            line["parity_vs_reference"] = {
+                "bitmap_equal": bool(np.array_equal(sink, ref.sink)),
+                "group_scores_bit_exact": bool(np.array_equal(
+                    np.array([g.decision.group_score for g in res_host.groups]),
+                    ref.group_scores)),
+                "kv_floats_equal": bool(np.array_equal(
+                    [g.kv_floats_loaded for g in res_host.groups], ref.group_kv_floats)),
+                "max_abs": err, "rel_l2": rel}
+        except Exception as e:  # reported, never silently replaced
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"failed: {e}"}
+
+    if not args.no_sweep:
+        line["sweep"] = sweep(P, torch, args, WorkloadSpec, dense_cfg, routed_cfg, cache)
+    cache.close()
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+    run_ours(args, world, rank, local_rank)
+
+
+if __name__ == "__main__":
+    main()

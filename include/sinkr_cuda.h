@@ -138,10 +138,13 @@ sinkr_status sinkr_kv_append_device_bf16(sinkr_engine* e, size_t seq, size_t lay
                                          size_t rows);
 /* Appends `rows` synthetic rows generated on the device (see
  * oracle/sinkr_oracle.c:orc_fill_rows for the bit-identical CPU restatement):
- * value(row, j) = bf16(scale * gauss12(key, row * D + j)). */
+ * value(row, j) = bf16(scale * gauss12(key, row * D + j)) for global rows
+ * row = global_row0 .. global_row0 + rows - 1 (a sequence shard passes the
+ * global index of its first row so every shard sees the same tokens). */
 sinkr_status sinkr_kv_append_synthetic(sinkr_engine* e, size_t seq, size_t layer,
                                        size_t kv_head, uint64_t key_k, uint64_t key_v,
-                                       float k_scale, float v_scale, size_t rows);
+                                       float k_scale, float v_scale, size_t global_row0,
+                                       size_t rows);
 /* KvCache::length / token_count (kv_cache.cpp:86-96); token_count throws
  * LOGIC_ERROR when the sequence's slots are ragged. */
 sinkr_status sinkr_kv_length(sinkr_engine* e, size_t seq, size_t layer, size_t kv_head,
@@ -218,6 +221,9 @@ sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gat
  * time (ms) of its decode kernel, measured with events on the engine stream. */
 sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches,
                                    float* decode_ms, float* step_ms);
+/* Bytes one sinkr_routed_decode_step call copies host->device (queries +
+ * step parameters) and device->host (outputs + routing record). */
+sinkr_status sinkr_step_io_bytes(sinkr_engine* e, size_t* h2d, size_t* d2h);
 /* Enables per-kernel event timing on the async path (costs two event records). */
 sinkr_status sinkr_set_timing(sinkr_engine* e, int enabled);
 /* Number of SMs / persistent CTAs used by the decode kernel. */

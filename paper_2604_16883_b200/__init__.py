@@ -17,6 +17,9 @@ from .router import (  # noqa: F401
     RoutingConfig,
     ThresholdProfile,
     auto_num_splits,
+    decode_rank_partial_async,
+    merge_rank_partials_async,
+    rank_partial_floats,
     fetch_step_info,
     kDefaultBlockSize,
     last_step_stats,

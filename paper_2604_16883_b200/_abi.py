@@ -82,7 +82,7 @@ EXPORTS = (
     "sinkr_routed_decode_batch", "sinkr_routed_decode_async", "sinkr_fetch_step_info",
     "sinkr_rank_partial_floats", "sinkr_decode_rank_partial_async",
     "sinkr_merge_rank_partials_async", "sinkr_last_step_stats", "sinkr_set_timing",
-    "sinkr_decode_grid",
+    "sinkr_decode_grid", "sinkr_step_io_bytes",
 )
 
 _lib = None

@@ -650,7 +650,8 @@ sinkr_status sinkr_kv_append_device_bf16(sinkr_engine* e, size_t seq, size_t lay
 
 sinkr_status sinkr_kv_append_synthetic(sinkr_engine* e, size_t seq, size_t layer,
                                        size_t kv_head, uint64_t key_k, uint64_t key_v,
-                                       float k_scale, float v_scale, size_t rows) {
+                                       float k_scale, float v_scale, size_t global_row0,
+                                       size_t rows) {
     return guard([&] {
         if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
         check_slot(e, seq, layer, kv_head);
@@ -664,8 +665,8 @@ sinkr_status sinkr_kv_append_synthetic(sinkr_engine* e, size_t seq, size_t layer
         const uint64_t n = (uint64_t)rows * D;
         const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 64);
         dev::synth_rows_kernel<<<blocks, 256, 0, e->stream>>>(e->d_k + off, e->d_v + off, key_k,
-                                                             key_v, k_scale, v_scale, row0, rows,
-                                                             (uint32_t)D);
+                                                             key_v, k_scale, v_scale, global_row0,
+                                                             rows, (uint32_t)D);
         CK(cudaGetLastError());
         if (row0 == 0) capture_anchor_device(e, idx);
         CK(cudaStreamSynchronize(e->stream));
@@ -891,6 +892,14 @@ sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches, f
             if (e->timing) CK(cudaEventElapsedTime(decode_ms, e->ev[1], e->ev[2]));
         }
         if (step_ms) CK(cudaEventElapsedTime(step_ms, e->ev[0], e->ev[3]));
+    });
+}
+
+sinkr_status sinkr_step_io_bytes(sinkr_engine* e, size_t* h2d, size_t* d2h) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        if (h2d) *h2d = e->in_bytes;
+        if (d2h) *d2h = e->res_bytes;
     });
 }
 

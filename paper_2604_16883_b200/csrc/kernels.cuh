@@ -334,7 +334,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     pdl_launch();  // let the combine grid get resident early; it waits on us
     pdl_wait();    // the probe's work list must be complete and visible
-    const uint32_t layer = t.hdr->layer;
     const uint32_t PS = t.r * (D + 2);
 
     if (warp == 0) {

@@ -260,11 +260,21 @@ class KvCache:
                                                 C.c_void_p(v_ptr), C.c_size_t(rows)))
 
     def append_synthetic(self, layer: int, kv_head: int, key_k: int, key_v: int, rows: int,
-                         k_scale: float = 1.0, v_scale: float = 1.0, seq: int = 0) -> None:
+                         k_scale: float = 1.0, v_scale: float = 1.0, seq: int = 0,
+                         global_row0: int = None) -> None:
+        """Append `rows` device-generated rows; their values are those of global
+        rows global_row0.. (default: the slot's current length)."""
+        if global_row0 is None:
+            global_row0 = self.length(layer, kv_head, seq)
         check(lib().sinkr_kv_append_synthetic(
             self._h, C.c_size_t(seq), C.c_size_t(layer), C.c_size_t(kv_head),
             C.c_uint64(key_k), C.c_uint64(key_v), C.c_float(k_scale), C.c_float(v_scale),
-            C.c_size_t(rows)))
+            C.c_size_t(global_row0), C.c_size_t(rows)))
+
+    def step_io_bytes(self):
+        h2d, d2h = C.c_size_t(), C.c_size_t()
+        check(lib().sinkr_step_io_bytes(self._h, C.byref(h2d), C.byref(d2h)))
+        return h2d.value, d2h.value
 
     def length(self, layer: int, kv_head: int, seq: int = 0) -> int:
         out = C.c_size_t()
@@ -380,3 +390,28 @@ def last_step_stats(cache: KvCache):
 
 def set_timing(cache: KvCache, enabled: bool) -> None:
     check(lib().sinkr_set_timing(cache.handle, C.c_int(int(enabled))))
+
+
+# ----------------------------------------------------------------------------
+# sequence-sharded multi-GPU split (sharding.py)
+def rank_partial_floats(cache: KvCache) -> int:
+    return int(lib().sinkr_rank_partial_floats(cache.handle))
+
+
+def decode_rank_partial_async(d_queries: int, layer: int, cache: KvCache, config: RoutingConfig,
+                              options: Optional[EngineOptions], d_partial: int) -> None:
+    c, keep = config._c()
+    o = (options or EngineOptions())._c()
+    check(lib().sinkr_decode_rank_partial_async(cache.handle, C.c_void_p(d_queries),
+                                                C.c_size_t(layer), C.byref(c), C.byref(o),
+                                                C.c_void_p(d_partial)))
+    del keep
+
+
+def merge_rank_partials_async(cache: KvCache, d_gathered: int, num_ranks: int,
+                              d_outputs: int) -> None:
+    check(lib().sinkr_merge_rank_partials_async(cache.handle, C.c_void_p(d_gathered),
+                                                C.c_size_t(num_ranks), C.c_void_p(d_outputs)))
+
+
+KvCache.rank_partial_floats = rank_partial_floats

@@ -1,0 +1,141 @@
+"""Multi-GPU partitioning of the decode step.
+
+Two ways to use N GPUs of one node, one process per GPU:
+
+* KV-head (unit) sharding — units (seq, kv_head) are independent
+  (SPEC.md:336): rank k owns a contiguous range of units and the query heads
+  that read them.  No collective on the step path.  `unit_shard` gives the
+  range; each rank simply builds its engine over its own heads.
+
+* Sequence sharding — for 512K+ contexts every rank owns the token range
+  `split_ranges(L, N)[rank]` (the reference's even-remainder rule,
+  attention.cpp:185-202) of every KV group.  Anchors (token 0's key and norm)
+  are replicated to every rank, so each rank computes the identical route
+  bitmap with tau(L_global).  A rank's engine writes one un-normalised LSE
+  partial per (unit, head); the N partials are all-gathered (NCCL over NVLink,
+  33 KB per rank for the 70B shape) and LSE-merged on device
+  (merge_partials, attention.cpp:159-183).
+
+torch.distributed is the plumbing (process group, NCCL all-gather on the
+engine's stream); the math runs in the engine's CUDA kernels.
+"""
+from __future__ import annotations
+
+from typing import List, Tuple
+
+
+def split_ranges(length: int, n: int) -> List[Tuple[int, int]]:
+    """attention.cpp:185-202 (host integer logic, also usable without a GPU)."""
+    if n <= 0 or n > length:
+        raise ValueError(f"num_splits must be in [1, len], got {n} for len {length}")
+    base, rem = divmod(length, n)
+    out, start = [], 0
+    for c in range(n):
+        sz = base + (1 if c < rem else 0)
+        out.append((start, start + sz))
+        start += sz
+    return out
+
+
+def sequence_shard(length: int, world: int, rank: int) -> Tuple[int, int]:
+    return split_ranges(length, world)[rank]
+
+
+def unit_shard(num_units: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous (seq, kv_head) unit range owned by `rank` (KV-head sharding)."""
+    return split_ranges(num_units, world)[rank] if num_units >= world else (
+        (rank, rank + 1) if rank < num_units else (num_units, num_units))
+
+
+def build_sequence_shard(P, spec, rank: int, world: int, device: int):
+    """Engine holding this rank's token slice of every (layer, kv_head) slot,
+    with the global token-0 anchor installed (replicated metadata)."""
+    lo, hi = sequence_shard(spec.length, world, rank)
+    cache = P.KvCache(P.CacheConfig(spec.num_layers, spec.num_q_heads, spec.num_kv_heads,
+                                    spec.head_dim, hi - lo, spec.num_seqs), device=device)
+    for s in range(spec.num_seqs):
+        for g in range(spec.num_kv_heads):
+            k0, v0 = spec.first_rows(s, g)
+            kk, kv = spec.slot_keys(s, g)
+            if lo == 0:
+                cache.append(spec.layer, g, k0, v0, seq=s)
+                if hi > 1:
+                    cache.append_synthetic(spec.layer, g, kk, kv, hi - 1, seq=s, global_row0=1)
+            else:
+                cache.append_synthetic(spec.layer, g, kk, kv, hi - lo, seq=s, global_row0=lo)
+                cache.set_anchor(spec.layer, g, k0, anchor_norm(k0), seq=s)
+    return cache, (lo, hi)
+
+
+def anchor_norm(k0) -> float:
+    """kv_cache.cpp:19-23,76: (float) sqrt(sum (double) k^2), index order."""
+    import math
+
+    import numpy as np
+
+    s = 0.0
+    for x in np.asarray(k0, dtype=np.float32).tolist():
+        s += x * x
+    return float(np.float32(math.sqrt(s)))
+
+
+def sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world: int):
+    """One sequence-sharded decode step on this rank's engine stream."""
+    P.decode_rank_partial_async(dq.data_ptr(), 0, cache, cfg, opts, partial.data_ptr())
+    stream = torch.cuda.ExternalStream(cache.stream)
+    with torch.cuda.stream(stream):
+        dist.all_gather_into_tensor(gathered, partial)
+    P.merge_rank_partials_async(cache, gathered.data_ptr(), world, dout.data_ptr())
+
+
+def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev):
+    """bench.py's N>1 path: strong scaling of the headline workload."""
+    import json
+
+    cache, (lo, hi) = build_sequence_shard(P, spec, rank, world, dev)
+    P.set_timing(cache, False)
+    opts = P.EngineOptions(global_context_len=spec.length)
+    dq = torch.from_numpy(spec.queries()[0]).cuda()
+    dout = torch.empty_like(dq)
+    nf = cache.rank_partial_floats()
+    partial = torch.empty(nf, dtype=torch.float32, device="cuda")
+    gathered = torch.empty(world * nf, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.ExternalStream(cache.stream)
+    res = {}
+    for name, cfg in (("routed", routed_cfg), ("dense", dense_cfg)):
+        for _ in range(max(3, args.warmup)):
+            sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        res[name] = float(t.item())
+    info = P.fetch_step_info(cache)
+    n_act = info.counters.groups_active
+    kv = n_act * 2 * spec.length * spec.head_dim * 2
+    return {
+        "metric": ("decode-attn µs/step & KV GB/s (% HBM peak) at 512K; "
+                   "speedup vs own dense path"),
+        "value": round(res["routed"] * 1e3, 2), "unit": "us/step", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["routed"], 5),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic planted-sink KV (device generator, seeded); fp32 queries",
+        "config": {"workload": f"llama3.1-8b-attn L={spec.length} B=1 "
+                               f"routed={spec.sink_fraction} sequence-sharded",
+                   "parallelism": f"sequence-shard x{world} + NCCL all-gather LSE merge",
+                   "context": spec.length, "tokens_per_rank": hi - lo},
+        "dense_us_per_step": round(res["dense"] * 1e3, 2),
+        "speedup_vs_dense": round(res["dense"] / res["routed"], 3),
+        "kv_gbs_routed_step": round(kv / (res["routed"] * 1e-3) / 1e9, 1),
+        "gpu_launches": 4 * args.steps,
+        "note": json.dumps({"partial_bytes_per_rank": nf * 4}),
+    }

@@ -1,0 +1,75 @@
+"""Sequence-sharded decode, N shards simulated on one GPU: each shard engine
+holds its token slice + the replicated anchor, writes its LSE partial, the
+partials are concatenated (what NCCL all-gather produces) and merged on device.
+Must equal the single-engine step: bitmap identical, outputs within tolerance.
+Also KV-head (unit) sharding: disjoint head ranges reproduce the full step."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_16883_b200 as P
+from paper_2604_16883_b200 import sharding
+from paper_2604_16883_b200.workload import WorkloadSpec
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,L,hq,hkv", [(2, 4096, 32, 8), (4, 10001, 64, 8), (8, 65536, 64, 8)])
+def test_sequence_shards_match_single(world, L, hq, hkv):
+    spec = WorkloadSpec(num_q_heads=hq, num_kv_heads=hkv, head_dim=128, length=L,
+                        sink_fraction=0.625, seed=world)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    q = spec.queries()[0]
+    with P.KvCache(P.CacheConfig(1, hq, hkv, 128, L)) as full:
+        spec.fill(full)
+        ref = P.routed_decode_step(q, 0, full, cfg)
+    dq = torch.from_numpy(q).cuda()
+    parts, caches = [], []
+    opts = P.EngineOptions(global_context_len=L)
+    for rank in range(world):
+        cache, (lo, hi) = sharding.build_sequence_shard(P, spec, rank, world, 0)
+        caches.append(cache)
+        part = torch.empty(cache.rank_partial_floats(), dtype=torch.float32, device="cuda")
+        P.decode_rank_partial_async(dq.data_ptr(), 0, cache, cfg, opts, part.data_ptr())
+        torch.cuda.synchronize()
+        info = P.fetch_step_info(cache)
+        assert np.array_equal(info.route_bitmap, ref.route_bitmap)
+        for g, gr in zip(info.groups, ref.groups):
+            assert g.decision.group_score == gr.decision.group_score
+            assert g.tokens_loaded == (0 if gr.decision.sink else hi - lo)
+        parts.append(part)
+    gathered = torch.cat(parts)
+    out = torch.zeros_like(dq)
+    P.merge_rank_partials_async(caches[0], gathered.data_ptr(), world, out.data_ptr())
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert np.abs(o - ref.outputs).max() <= 2e-3
+    assert np.linalg.norm(o - ref.outputs) <= 1e-3 * np.linalg.norm(ref.outputs)
+    r = hq // hkv
+    for gi, g in enumerate(ref.groups):
+        if g.decision.sink:
+            assert not np.any(o[gi * r:(gi + 1) * r].view(np.uint32))
+    for c in caches:
+        c.close()
+
+
+def test_unit_shards_match_single():
+    """KV-head sharding: rank k owns kv heads [a, b) and their query heads."""
+    hq, hkv, L, world = 32, 8, 3000, 4
+    spec = WorkloadSpec(num_q_heads=hq, num_kv_heads=hkv, head_dim=128, length=L,
+                        sink_fraction=0.5, seed=9)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    q = spec.queries()[0]
+    with P.KvCache(P.CacheConfig(1, hq, hkv, 128, L)) as full:
+        spec.fill(full)
+        ref = P.routed_decode_step(q, 0, full, cfg)
+        r = hq // hkv
+        for rank in range(world):
+            a, b = sharding.unit_shard(hkv, world, rank)
+            with P.KvCache(P.CacheConfig(1, (b - a) * r, b - a, 128, L)) as part:
+                for g in range(a, b):
+                    k, v = full.historical(0, g, 0, L)
+                    part.append(0, g - a, k, v)
+                res = P.routed_decode_step(q[a * r:b * r], 0, part, cfg)
+                assert np.array_equal(res.route_bitmap, ref.route_bitmap[a:b])
+                np.testing.assert_allclose(res.outputs, ref.outputs[a * r:b * r], atol=1e-6)
