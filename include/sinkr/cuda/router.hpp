@@ -1,0 +1,285 @@
+// sinkr/cuda/router.hpp — header-only C++20 shim over the C-ABI
+// (include/sinkr_cuda.h) with the reference's own operator API:
+//
+//   reference (/root/reference/proj/include/sinkr/...)   here (namespace sinkr::cuda)
+//   CacheConfig, KvCache            kv_cache.hpp:13-80    CacheConfig, KvCache (HBM, bf16)
+//   GroupAnchor                     kv_cache.hpp:27-30    GroupAnchor
+//   ThresholdProfile::constant      calibration.hpp:21-34 ThresholdProfile::constant
+//   RoutingConfig                   router.hpp:16-26      RoutingConfig
+//   RouteDecision, GroupStepInfo,   router.hpp:28-67      same names, same fields
+//   LayerStepResult
+//   LoadCounters                    counters.hpp:9-28     LoadCounters
+//   EngineOptions                   router.hpp:69-76      EngineOptions (no ThreadPool*;
+//                                                         + global_context_len)
+//   threshold_for_length, route,    router.hpp:47-54,78   same
+//   auto_num_splits
+//   split_ranges                    attention.hpp:82-85   same
+//   routed_decode_step              router.hpp:84-86      same signature
+//
+// Status codes are rethrown as the reference's exception classes
+// (std::invalid_argument / out_of_range / runtime_error / logic_error), so a
+// caller of the reference sees identical error behaviour.  A caller switches
+// by replacing `sinkr::` with `sinkr::cuda::` and linking libsinkr_cuda.so.
+#pragma once
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../sinkr_cuda.h"
+
+namespace sinkr::cuda {
+
+inline void check(sinkr_status s) {
+    if (s == SINKR_OK) return;
+    const std::string msg = sinkr_last_error();
+    switch (s) {
+        case SINKR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case SINKR_OUT_OF_RANGE: throw std::out_of_range(msg);
+        case SINKR_LOGIC_ERROR: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+constexpr std::size_t kDefaultBlockSize = 128;
+
+struct CacheConfig {
+    std::size_t num_layers = 0;
+    std::size_t num_q_heads = 0;
+    std::size_t num_kv_heads = 0;
+    std::size_t head_dim = 0;
+    std::size_t capacity = 0;
+    std::size_t num_seqs = 1;  // B independent caches served by one launch
+    std::size_t group_width() const { return num_q_heads / num_kv_heads; }
+};
+
+struct GroupAnchor {
+    std::vector<float> k0;
+    float k0_norm = 0.0f;
+};
+
+struct ThresholdProfile {
+    std::array<double, 4> coeffs{0.0, 0.0, 0.0, 0.0};
+    double length_normalizer = 1.0;
+    double clamp_lo = 0.0;
+    double clamp_hi = 1.0;
+    double target_skip = 0.60;
+    double gamma = 0.65;
+    std::vector<std::size_t> excluded_layers{0, 1};
+
+    static ThresholdProfile constant(double tau) {  // calibration.cpp:29-35
+        ThresholdProfile p;
+        p.coeffs = {0.0, 0.0, 0.0, tau};
+        p.clamp_lo = tau < 0.0 ? tau : 0.0;
+        p.clamp_hi = 1.0 < tau ? tau : 1.0;
+        return p;
+    }
+    sinkr_threshold_profile c() const {
+        sinkr_threshold_profile p{};
+        for (int i = 0; i < 4; ++i) p.coeffs[i] = coeffs[i];
+        p.length_normalizer = length_normalizer;
+        p.clamp_lo = clamp_lo;
+        p.clamp_hi = clamp_hi;
+        return p;
+    }
+};
+
+struct RoutingConfig {
+    double gamma = 0.65;
+    ThresholdProfile profile;
+    std::vector<std::size_t> excluded_layers{0, 1};
+    bool sink_on_tie = false;
+
+    static RoutingConfig from_profile(ThresholdProfile profile) {  // router.cpp:23-29
+        RoutingConfig c;
+        c.gamma = profile.gamma;
+        c.excluded_layers = profile.excluded_layers;
+        c.profile = std::move(profile);
+        return c;
+    }
+    bool layer_excluded(std::size_t layer) const {
+        for (auto l : excluded_layers)
+            if (l == layer) return true;
+        return false;
+    }
+    sinkr_routing_config c() const {
+        sinkr_routing_config r{};
+        r.gamma = gamma;
+        r.profile = profile.c();
+        r.excluded_layers = excluded_layers.data();
+        r.num_excluded_layers = excluded_layers.size();
+        r.sink_on_tie = sink_on_tie ? 1 : 0;
+        return r;
+    }
+};
+
+struct RouteDecision {
+    double group_score = 0.0;
+    double threshold = 0.0;
+    bool sink = false;
+    bool degenerate = false;
+    std::vector<double> head_scores;
+};
+
+struct LoadCounters {
+    std::uint64_t kv_floats_loaded = 0;
+    std::uint64_t anchor_floats_loaded = 0;
+    std::uint64_t groups_active = 0;
+    std::uint64_t groups_skipped = 0;
+    double routing_seconds = 0.0;
+    double attention_seconds = 0.0;
+    double merge_seconds = 0.0;
+};
+
+struct GroupStepInfo {
+    std::size_t layer = 0;
+    std::size_t kv_head = 0;
+    RouteDecision decision;
+    std::uint64_t kv_floats_loaded = 0;
+    std::uint64_t tokens_loaded = 0;  // rows the decode kernel streamed
+};
+
+struct LayerStepResult {
+    std::vector<float> outputs;  // B x H_q x D, query-head order
+    std::vector<GroupStepInfo> groups;
+    LoadCounters counters;
+};
+
+struct EngineOptions {
+    std::size_t num_splits = 0;
+    std::size_t block_size = kDefaultBlockSize;
+    bool observe_only = false;
+    std::size_t global_context_len = 0;
+    sinkr_engine_options c() const {
+        return sinkr_engine_options{num_splits, block_size, observe_only ? 1 : 0,
+                                    global_context_len};
+    }
+};
+
+class KvCache {
+public:
+    explicit KvCache(CacheConfig config, int device = 0) : config_(config) {
+        const sinkr_cache_config c{config.num_layers, config.num_q_heads, config.num_kv_heads,
+                                   config.head_dim,   config.capacity,    config.num_seqs};
+        check(sinkr_engine_create(&c, device, &e_));
+    }
+    ~KvCache() { sinkr_engine_destroy(e_); }
+    KvCache(const KvCache&) = delete;
+    KvCache& operator=(const KvCache&) = delete;
+
+    const CacheConfig& config() const { return config_; }
+    sinkr_engine* handle() const { return e_; }
+
+    void append(std::size_t layer, std::size_t kv_head, std::span<const float> k,
+                std::span<const float> v, std::size_t seq = 0) {
+        const std::size_t d = config_.head_dim;
+        if (k.size() != v.size() || k.empty() || k.size() % d != 0)
+            throw std::invalid_argument("k/v row size does not match head_dim");
+        check(sinkr_kv_append(e_, seq, layer, kv_head, k.data(), v.data(), k.size() / d));
+    }
+    std::size_t length(std::size_t layer, std::size_t kv_head, std::size_t seq = 0) const {
+        std::size_t n = 0;
+        check(sinkr_kv_length(e_, seq, layer, kv_head, &n));
+        return n;
+    }
+    std::size_t token_count(std::size_t seq = 0) const {
+        std::size_t n = 0;
+        check(sinkr_kv_token_count(e_, seq, &n));
+        return n;
+    }
+    GroupAnchor anchor(std::size_t layer, std::size_t kv_head, std::size_t seq = 0) const {
+        GroupAnchor a;
+        a.k0.resize(config_.head_dim);
+        check(sinkr_kv_anchor(e_, seq, layer, kv_head, a.k0.data(), &a.k0_norm));
+        return a;
+    }
+    // KvCache::historical as a copy (exact f32 upcast of the stored bf16 rows)
+    std::pair<std::vector<float>, std::vector<float>> historical(std::size_t layer,
+                                                                 std::size_t kv_head,
+                                                                 std::size_t from, std::size_t to,
+                                                                 std::size_t seq = 0) const {
+        std::vector<float> k((to > from ? to - from : 0) * config_.head_dim), v(k.size());
+        check(sinkr_kv_read(e_, seq, layer, kv_head, from, to, k.data(), v.data()));
+        return {std::move(k), std::move(v)};
+    }
+
+private:
+    CacheConfig config_;
+    sinkr_engine* e_ = nullptr;
+};
+
+inline double threshold_for_length(std::size_t context_len, const ThresholdProfile& profile) {
+    const auto p = profile.c();
+    double out = 0.0;
+    check(sinkr_threshold_for_length(context_len, &p, &out));
+    return out;
+}
+
+inline RouteDecision route(std::size_t layer, double score, std::size_t context_len,
+                           const RoutingConfig& config) {
+    const auto c = config.c();
+    int sink = 0;
+    RouteDecision d;
+    d.group_score = score;
+    check(sinkr_route(layer, score, context_len, &c, &sink, &d.threshold));
+    d.sink = sink != 0;
+    return d;
+}
+
+inline std::size_t auto_num_splits(std::size_t context_len) {
+    return sinkr_auto_num_splits(context_len);
+}
+
+inline std::vector<std::pair<std::size_t, std::size_t>> split_ranges(std::size_t len,
+                                                                     std::size_t num_splits) {
+    std::vector<std::size_t> buf(2 * (num_splits ? num_splits : 1));
+    check(sinkr_split_ranges(len, num_splits, buf.data()));
+    std::vector<std::pair<std::size_t, std::size_t>> out;
+    for (std::size_t i = 0; i < num_splits; ++i) out.emplace_back(buf[2 * i], buf[2 * i + 1]);
+    return out;
+}
+
+// router.hpp:84-86 — one decode step for one layer (all B sequences).
+inline LayerStepResult routed_decode_step(std::span<const float> queries, std::size_t layer,
+                                          const KvCache& cache, const RoutingConfig& config,
+                                          const EngineOptions& options = {}) {
+    const CacheConfig& cc = cache.config();
+    const std::size_t B = cc.num_seqs ? cc.num_seqs : 1;
+    if (queries.size() != B * cc.num_q_heads * cc.head_dim)
+        throw std::invalid_argument("queries span must be H_q x D for one layer");
+    const auto rc = config.c();
+    const auto oc = options.c();
+    LayerStepResult r;
+    r.outputs.resize(queries.size());
+    std::vector<sinkr_group_info> gi(B * cc.num_kv_heads);
+    std::vector<double> hs(B * cc.num_q_heads);
+    sinkr_load_counters ctr{};
+    check(sinkr_routed_decode_batch(cache.handle(), queries.data(), layer, &rc, &oc,
+                                    r.outputs.data(), gi.data(), hs.data(), &ctr));
+    const std::size_t w = cc.group_width();
+    r.groups.resize(gi.size());
+    for (std::size_t u = 0; u < gi.size(); ++u) {
+        auto& g = r.groups[u];
+        g.layer = gi[u].layer;
+        g.kv_head = gi[u].kv_head;
+        g.decision.group_score = gi[u].group_score;
+        g.decision.threshold = gi[u].threshold;
+        g.decision.sink = gi[u].sink != 0;
+        g.decision.degenerate = gi[u].degenerate != 0;
+        g.decision.head_scores.assign(hs.begin() + u * w, hs.begin() + (u + 1) * w);
+        g.kv_floats_loaded = gi[u].kv_floats_loaded;
+        g.tokens_loaded = gi[u].tokens_loaded;
+    }
+    r.counters = LoadCounters{ctr.kv_floats_loaded, ctr.anchor_floats_loaded,
+                              ctr.groups_active,    ctr.groups_skipped,
+                              ctr.routing_seconds,  ctr.attention_seconds,
+                              ctr.merge_seconds};
+    return r;
+}
+
+}  // namespace sinkr::cuda

@@ -2,7 +2,7 @@
  * sinkr_cuda.h — C-ABI of the B200-native (sm_100a) SinkRouter decode engine.
  *
  * This is the drop-in boundary for the reference's C++ operator API
- * (/root/reference/proj/include/sinkr/*.hpp).  Every entry point below names
+ * (/root/reference/proj/include/sinkr/ *.hpp).  Every entry point below names
  * the reference interface it replaces.  Plain pointers and sizes only; no
  * torch or C++ types cross the boundary.  A C++ shim with the reference's own
  * signatures and exception types sits on top: include/sinkr/cuda/router.hpp.

@@ -1,0 +1,81 @@
+// C++ caller of the drop-in API (include/sinkr/cuda/router.hpp): the same
+// code a user of sinkr::routed_decode_step writes, with sinkr:: -> sinkr::cuda::.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include "sinkr/cuda/router.hpp"
+
+namespace sc = sinkr::cuda;
+
+#define REQUIRE(c)                                                       \
+    do {                                                                 \
+        if (!(c)) {                                                      \
+            std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #c); \
+            return 1;                                                    \
+        }                                                                \
+    } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int main() {
+    const std::size_t L = 777, D = 128, hq = 32, hkv = 8;
+    sc::KvCache cache(sc::CacheConfig{2, hq, hkv, D, 1024, 1});
+    std::mt19937 rng(7);
+    std::normal_distribution<float> n01;
+    std::vector<float> q(hq * D);
+    for (auto& x : q) x = n01(rng);
+    REQUIRE(throws<std::runtime_error>([&] {
+        sc::routed_decode_step(q, 0, cache, sc::RoutingConfig{});
+    }));  // empty cache (router.cpp:90)
+    for (std::size_t layer = 0; layer < 2; ++layer)
+        for (std::size_t g = 0; g < hkv; ++g) {
+            std::vector<float> k(L * D), v(L * D);
+            for (auto& x : k) x = n01(rng);
+            for (auto& x : v) x = n01(rng);
+            cache.append(layer, g, k, v);
+        }
+    REQUIRE(cache.token_count() == L);
+    REQUIRE(std::fabs(cache.anchor(0, 0).k0_norm) > 0.0f);
+
+    // routing disabled: every group attends the whole cache
+    auto cfg = sc::RoutingConfig::from_profile(sc::ThresholdProfile::constant(2.0));
+    auto r = sc::routed_decode_step(q, 1, cache, cfg);
+    REQUIRE(r.counters.groups_active == hkv && r.counters.groups_skipped == 0);
+    REQUIRE(r.counters.kv_floats_loaded == hkv * 2 * L * D);
+    for (auto& g : r.groups) REQUIRE(!g.decision.sink && g.decision.head_scores.size() == 4);
+
+    // full skip on a routable layer: bitwise-zero outputs, no KV traffic
+    sc::RoutingConfig skip;
+    skip.profile = sc::ThresholdProfile::constant(-2.0);
+    auto s = sc::routed_decode_step(q, 1, cache, skip);
+    REQUIRE(s.counters.groups_skipped == hkv && s.counters.kv_floats_loaded == 0);
+    for (float x : s.outputs) REQUIRE(x == 0.0f && !std::signbit(x));
+    // ... but never on an excluded layer (router.hpp:19)
+    auto e = sc::routed_decode_step(q, 0, cache, skip);
+    REQUIRE(e.counters.groups_active == hkv);
+
+    REQUIRE(throws<std::out_of_range>([&] { sc::routed_decode_step(q, 2, cache, cfg); }));
+    REQUIRE(throws<std::invalid_argument>([&] {
+        sc::routed_decode_step(std::span<const float>(q.data(), 5), 0, cache, cfg);
+    }));
+    REQUIRE(throws<std::invalid_argument>([&] { sc::split_ranges(3, 4); }));
+    const auto sr = sc::split_ranges(10, 3);
+    REQUIRE(sr[1].first == 4 && sr[1].second == 7);
+    REQUIRE(sc::threshold_for_length(5, sc::ThresholdProfile{{1, 0, 0, 0}, 10.0, 0.0, 1.0}) ==
+            0.125);
+    std::printf("shim OK (%.1f us attention)\n", r.counters.attention_seconds * 1e6);
+    return 0;
+}

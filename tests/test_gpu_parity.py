@@ -280,3 +280,38 @@ def test_timings_and_launch_count():
         assert c.routing_seconds > 0 and c.attention_seconds > 0 and c.merge_seconds > 0
         n, dms, sms = P.last_step_stats(cache)
         assert n == 3 and 0 < dms <= sms
+
+
+# ---- golden fixtures from the compiled reference (tests/golden) ------------------
+from golden_cases import case_ids, load_cases  # noqa: E402
+
+
+@pytest.mark.parametrize("name", case_ids())
+def test_golden_fixture_engine(name):
+    meta, k, v, z = next(c for c in load_cases() if c[0]["name"] == name)
+    hkv, L, D = k.shape
+    hq = z["q"].shape[0]
+    layers = max(2, meta["layer"] + 1)
+    c, n, lo, hi = meta["prof"]
+    prof = P.ThresholdProfile(coeffs=tuple(c), length_normalizer=n, clamp_lo=lo, clamp_hi=hi)
+    cfg = P.RoutingConfig(profile=prof, excluded_layers=tuple(meta["excluded"]),
+                          sink_on_tie=meta["sink_on_tie"])
+    opts = P.EngineOptions(num_splits=meta["num_splits"], observe_only=meta["observe_only"])
+    with P.KvCache(P.CacheConfig(layers, hq, hkv, D, L)) as cache:
+        for layer in range(layers):
+            for g in range(hkv):
+                cache.append(layer, g, k[g], v[g])
+        res = P.routed_decode_step(z["q"], meta["layer"], cache, cfg, opts)
+
+    class Ref:
+        pass
+
+    ref = Ref()
+    for f in ("outputs", "group_scores", "thresholds", "sink", "degenerate", "group_kv_floats",
+              "head_scores"):
+        setattr(ref, f, z[f])
+    assert_parity(res.outputs, ref, hq // hkv, D, res.groups)
+    cnt = z["counters"]
+    assert res.counters.kv_floats_loaded == cnt[0]
+    assert res.counters.anchor_floats_loaded == cnt[1]
+    assert res.counters.groups_active == cnt[2] and res.counters.groups_skipped == cnt[3]
