@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -147,7 +148,16 @@ struct sinkr_engine {
     bool timing = true;
     bool params_valid = false;
     std::vector<uint8_t> last_params;
-    std::map<std::tuple<const void*, void*, int>, cudaGraphExec_t> graphs;
+    struct GraphEntry {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t probe = nullptr;
+        cudaKernelNodeParams probe_kp{};
+        dev::DevTables probe_t{};
+        dev::ProbeParams pp{};
+    };
+    std::map<std::tuple<const void*, void*, int>, GraphEntry> graphs;
+    dev::ProbeParams pp{};  // this step's probe parameters (staged by stage_params)
     uint32_t last_launches = 0;
     int last_mode = 0;
 
@@ -245,22 +255,34 @@ void launch_combine(sinkr_engine* e, const dev::DevTables& t, const float* src, 
 }
 
 // Enqueues probe -> decode -> combine on the engine stream (graph-captured).
+// SINKR_DEBUG_KERNELS (bitmask probe=1, decode=2, combine=4; default 7) lets a
+// profiling run drop kernels from the step to attribute fixed costs.  Results
+// are meaningless unless all three run; never set it outside profiling.
+static int debug_kernel_mask() {
+    static int m = [] {
+        const char* v = std::getenv("SINKR_DEBUG_KERNELS");
+        return v ? std::atoi(v) : 7;
+    }();
+    return m;
+}
+
 void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
     const dev::DevTables t = e->tables(d_q);
+    const int km = debug_kernel_mask();
     if (e->timing) CK(cudaEventRecord(e->ev[0], e->stream));
-    switch (e->D) {
-        case 32: dev::probe_kernel<32><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t); break;
-        case 64: dev::probe_kernel<64><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t); break;
-        default: dev::probe_kernel<128><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t); break;
+    if (km & 1) switch (e->D) {
+        case 32: dev::probe_kernel<32><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+        case 64: dev::probe_kernel<64><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+        default: dev::probe_kernel<128><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
     }
     if (e->timing) CK(cudaEventRecord(e->ev[1], e->stream));
-    switch (e->D) {
+    if (km & 2) switch (e->D) {
         case 32: launch_decode<32>(e, t); break;
         case 64: launch_decode<64>(e, t); break;
         default: launch_decode<128>(e, t); break;
     }
     if (e->timing) CK(cudaEventRecord(e->ev[2], e->stream));
-    launch_combine(e, t, e->d_partials, e->S * e->PS, e->PS, 0u, d_out, mode, e->S);
+    if (km & 4) launch_combine(e, t, e->d_partials, e->S * e->PS, e->PS, 0u, d_out, mode, e->S);
     if (e->timing) CK(cudaEventRecord(e->ev[3], e->stream));
     CK(cudaGetLastError());
 }
@@ -278,22 +300,53 @@ void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
     const auto key = std::make_tuple((const void*)d_q, (void*)d_out, mode);
     auto it = e->graphs.find(key);
     if (it == e->graphs.end()) {
-        cudaGraph_t g;
+        sinkr_engine::GraphEntry ge;
         CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
         try {
             enqueue_step(e, d_q, d_out, mode);
         } catch (...) {
-            cudaStreamEndCapture(e->stream, &g);
+            cudaStreamEndCapture(e->stream, &ge.graph);
+            if (ge.graph) cudaGraphDestroy(ge.graph);
             throw;
         }
-        CK(cudaStreamEndCapture(e->stream, &g));
-        cudaGraphExec_t ex;
-        CK(cudaGraphInstantiate(&ex, g, 0));
-        CK(cudaGraphDestroy(g));
-        it = e->graphs.emplace(key, ex).first;
+        CK(cudaStreamEndCapture(e->stream, &ge.graph));
+        CK(cudaGraphInstantiate(&ge.exec, ge.graph, 0));
+        // the probe node: its by-value ProbeParams are patched every step
+        size_t n = 0;
+        CK(cudaGraphGetNodes(ge.graph, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        CK(cudaGraphGetNodes(ge.graph, nodes.data(), &n));
+        const void* probe_fn = e->D == 32 ? (const void*)dev::probe_kernel<32>
+                             : e->D == 64 ? (const void*)dev::probe_kernel<64>
+                                          : (const void*)dev::probe_kernel<128>;
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp{};
+            CK(cudaGraphKernelNodeGetParams(nd, &kp));
+            if (kp.func == probe_fn) {
+                ge.probe = nd;
+                ge.probe_kp = kp;
+            }
+        }
+        if (!ge.probe && (debug_kernel_mask() & 1))
+            fail(SINKR_CUDA_ERROR, "probe node not found in the captured graph");
+        ge.probe_t = e->tables(d_q);
+        ge.pp = e->pp;
+        it = e->graphs.emplace(key, ge).first;
+    }
+    auto& ge = it->second;
+    if (ge.probe && std::memcmp(&ge.pp, &e->pp, sizeof(e->pp)) != 0) {
+        ge.pp = e->pp;
+        void* args[2] = {&ge.probe_t, &ge.pp};
+        cudaKernelNodeParams kp = ge.probe_kp;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        CK(cudaGraphExecKernelNodeSetParams(ge.exec, ge.probe, &kp));
     }
     CK(cudaEventRecord(e->ev[0], e->stream));
-    CK(cudaGraphLaunch(it->second, e->stream));
+    CK(cudaGraphLaunch(ge.exec, e->stream));
     CK(cudaEventRecord(e->ev[3], e->stream));
 }
 
@@ -336,6 +389,15 @@ void stage_params(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg
         tau[s] = threshold_for_length(Lg, cfg->profile);
         len[s] = (uint32_t)L;
     }
+    std::memset(&e->pp, 0, sizeof(e->pp));
+    e->pp.layer = hdr->layer;
+    e->pp.flags = hdr->flags;
+    e->pp.inline_seqs = e->B <= (size_t)dev::kParamSeqs ? 1u : 0u;
+    if (e->pp.inline_seqs)
+        for (size_t s = 0; s < e->B; ++s) {
+            e->pp.tau[s] = tau[s];
+            e->pp.len[s] = len[s];
+        }
     const size_t pbytes = e->off_q;
     const bool same = e->params_valid && e->last_params.size() == pbytes &&
                       std::memcmp(e->last_params.data(), e->h_in, pbytes) == 0;
@@ -511,6 +573,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->S = std::min<size_t>(e->grid, (e->cap + dev::kStageTok - 1) / dev::kStageTok);
             e->PS = e->r * (e->D + 2);
             CK(cudaMalloc(&e->d_partials, e->U * e->S * e->PS * 4));
+            // combine reads candidate slots speculatively: keep them finite
+            CK(cudaMemsetAsync(e->d_partials, 0, e->U * e->S * e->PS * 4, e->stream));
 
             make_tmap(&e->tmk, e->d_k, rows, e->D);
             make_tmap(&e->tmv, e->d_v, rows, e->D);
@@ -527,6 +591,14 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
             CK(cudaFuncSetAttribute(dev::probe_kernel<128>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
+            // one shared-memory carveout for all step kernels: switching the
+            // L1/smem split between back-to-back kernels stalls the SMs
+            for (const void* fn : {(const void*)dev::probe_kernel<32>, (const void*)dev::probe_kernel<64>,
+                                   (const void*)dev::probe_kernel<128>, (const void*)dev::combine_kernel,
+                                   (const void*)dev::decode_kernel<32>, (const void*)dev::decode_kernel<64>,
+                                   (const void*)dev::decode_kernel<128>})
+                CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        cudaSharedmemCarveoutMaxShared));
             for (auto& ev : e->ev) CK(cudaEventCreate(&ev));
             CK(cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming));
             CK(cudaEventRecord(e->ev_in, e->stream));
@@ -543,7 +615,10 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     if (!e) return SINKR_OK;
     cudaSetDevice(e->device);
     if (e->stream) cudaStreamSynchronize(e->stream);
-    for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : e->graphs) {
+        cudaGraphExecDestroy(kv.second.exec);
+        cudaGraphDestroy(kv.second.graph);
+    }
     for (auto& ev : e->ev)
         if (ev) cudaEventDestroy(ev);
     if (e->ev_in) cudaEventDestroy(e->ev_in);

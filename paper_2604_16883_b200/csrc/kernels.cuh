@@ -33,7 +33,8 @@ constexpr int kThreads = 32 * (1 + kCWarps);          // + 1 TMA producer warp
 constexpr int kMaxR = 8;                              // GQA width per MMA row tile (hi/lo split)
 constexpr uint32_t kEnd = 0xFFFFFFFFu;
 constexpr int kProbeThreads = 256;
-constexpr int kChunksPerCta = 32;                     // dynamic-scheduling granularity target
+constexpr int kChunksPerCta = 128;                    // dynamic-scheduling granularity target
+constexpr int kMinChunkTok = 256;                     // >= claim latency of one chunk
 
 // unit_flags bits
 constexpr uint32_t kSink = 1u, kDegenerate = 2u, kActive = 4u;
@@ -44,6 +45,19 @@ struct StepHdr {
     uint32_t layer;
     uint32_t flags;
     uint32_t pad[2];
+};
+
+// Per-step scalars handed to the probe by value (kernel parameters live in the
+// constant bank: no global-memory round trip before routing can start).  The
+// engine patches them into the captured graph node each step.
+constexpr int kParamSeqs = 64;
+struct ProbeParams {
+    uint32_t layer;
+    uint32_t flags;
+    uint32_t inline_seqs;  // 1: tau/len below; 0: B > kParamSeqs, read DevTables.tau/len
+    uint32_t pad;
+    double tau[kParamSeqs];
+    uint32_t len[kParamSeqs];
 };
 
 struct WorkState {
@@ -102,7 +116,7 @@ __device__ __forceinline__ void pdl_launch() {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t) {
+__global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t, const ProbeParams p) {
     using Scan = cub::BlockScan<uint32_t, kProbeThreads>;
     using Reduce = cub::BlockReduce<unsigned long long, kProbeThreads>;
     __shared__ union {
@@ -137,7 +151,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t) {
             qv[a][b] = (i < NH && j < D) ? __ldg(t.q + size_t(i) * D + j) : 0.f;
         }
     }
-    const uint32_t layer = __ldg(&t.hdr->layer), flags = __ldg(&t.hdr->flags);
+    const uint32_t layer = p.layer, flags = p.flags;
     float kv[kHW][kJL];
 #pragma unroll
     for (int a = 0; a < kHW; ++a) {
@@ -220,7 +234,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t) {
             degen |= single ? s_degen[h0 + i] : __ldcg(&t.head_degen[h0 + i]);
         }
         const double S = __ddiv_rn(sum, (double)t.r);
-        const double tau = __ldg(&t.tau[seq]);
+        const double tau = p.inline_seqs ? p.tau[seq] : __ldg(&t.tau[seq]);
         const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
         bool sink = over && !(flags & kLayerExcluded);
         if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
@@ -233,7 +247,7 @@ __global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t) {
         t.tokens[u] = 0ull;
         if (active) {
             ++my_active;
-            my_tokens += __ldg(&t.len[seq]);
+            my_tokens += p.inline_seqs ? p.len[seq] : __ldg(&t.len[seq]);
         }
         if (u - u0 < 32) my_flags |= (active ? 1u : 0u) << (u - u0);
     }
@@ -247,12 +261,12 @@ __global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t) {
     unsigned long long cc = (T + (unsigned long long)t.grid * kChunksPerCta - 1) /
                             ((unsigned long long)t.grid * kChunksPerCta);
     cc = ((cc + kStageTok - 1) / kStageTok) * kStageTok;
-    if (cc < kStageTok) cc = kStageTok;
+    if (cc < kMinChunkTok) cc = kMinChunkTok;
     const uint32_t Ck = (uint32_t)cc;
     for (uint32_t u = u0; u < u1; ++u) {
         const bool act = (u - u0 < 32) ? ((my_flags >> (u - u0)) & 1u) : (t.unit_flags[u] & kActive);
         if (!act) continue;
-        const uint32_t L = __ldg(&t.len[u / t.Hkv]);
+        const uint32_t L = p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len[u / t.Hkv]);
         // decode CTAs c with c % a_tot == a_off take chunk c / a_tot statically
         t.unit_next[a_off] = a_off < t.grid ? (t.grid - a_off + a_tot - 1) / a_tot : 0u;
         t.act_info[a_off] = make_uint4(u, L, (L + Ck - 1) / Ck, layer * U + u);
@@ -332,6 +346,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
 
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmk);
+        ptx::tma_prefetch_desc(&tmv);
+    }
     pdl_launch();  // let the combine grid get resident early; it waits on us
     pdl_wait();    // the probe's work list must be complete and visible
     const uint32_t PS = t.r * (D + 2);
@@ -339,8 +357,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ------------------------------ producer ------------------------------
         if (lane == 0) {
-            ptx::tma_prefetch_desc(&tmk);
-            ptx::tma_prefetch_desc(&tmv);
             const uint64_t pol = ptx::policy_evict_first();
             // Unit-affine dynamic scheduling: CTA c starts on active unit
             // c mod n_active and claims chunks from that unit's cursor; when
@@ -584,7 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // slot count is slot_count[u] (fixed_n == 0) or fixed_n.
 // ============================================================================
 constexpr int kCombineGroups = 8;
-constexpr int kCombineUnroll = 8;
+constexpr int kCombineUnroll = 19;        // 8 * 19 = 152 >= 148 partial slots in one round trip
+constexpr int kCombineMaxWarpSlots = 5;   // 5 * 32 = 160 m values held by warp 0
 
 __global__ void __launch_bounds__(32 * kCombineGroups)
     combine_kernel(DevTables t, const float* __restrict__ src, uint32_t unit_stride,
@@ -598,9 +615,27 @@ __global__ void __launch_bounds__(32 * kCombineGroups)
     const uint32_t lane = threadIdx.x & 31, sg = threadIdx.x >> 5;
     const uint32_t d = blockIdx.z * 32 + lane;
     const uint32_t seq = u / t.Hkv, g = u % t.Hkv;
+    const uint32_t cap_n = fixed_n ? fixed_n : t.S;  // slots that may hold a partial
+    const float* base = src + size_t(u) * unit_stride;
     pdl_wait();  // decode partials complete and visible
-    const bool active = __ldcg(&t.unit_flags[u]) & kActive;
-    const uint32_t n = active ? (fixed_n ? fixed_n : __ldcg(&t.slot_count[u])) : 0u;
+    // one round trip: flags, count and every candidate partial are fetched
+    // together (slots beyond the count hold stale but finite data and are
+    // masked below; the partial buffer is zeroed at engine creation)
+    const uint32_t flag = __ldcg(&t.unit_flags[u]);
+    const uint32_t cnt = fixed_n ? fixed_n : __ldcg(&t.slot_count[u]);
+    float vals[kCombineUnroll], ls[kCombineUnroll], mv[kCombineMaxWarpSlots];
+#pragma unroll
+    for (int k = 0; k < kCombineUnroll; ++k) {
+        const uint32_t j = sg + k * kCombineGroups;
+        vals[k] = j < cap_n ? __ldcg(base + j * slot_stride + 2 * r + h * D + d) : 0.f;
+        ls[k] = j < cap_n ? __ldcg(base + j * slot_stride + r + h) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kCombineMaxWarpSlots; ++k) {
+        const uint32_t j = lane + 32 * k;
+        mv[k] = (sg == 0 && j < cap_n) ? __ldcg(base + j * slot_stride + h) : -INFINITY;
+    }
+    const uint32_t n = (flag & kActive) ? cnt : 0u;
     if (n == 0) {
         if (sg != 0) return;
         if (mode == 0) {
@@ -615,20 +650,21 @@ __global__ void __launch_bounds__(32 * kCombineGroups)
         }
         return;
     }
-    const float* base = src + size_t(u) * unit_stride;
-    float vals[kCombineUnroll], ls[kCombineUnroll];
-#pragma unroll
-    for (int k = 0; k < kCombineUnroll; ++k) {
-        const uint32_t j = sg + k * kCombineGroups;
-        vals[k] = j < n ? __ldcg(base + j * slot_stride + 2 * r + h * D + d) : 0.f;
-        ls[k] = j < n ? __ldcg(base + j * slot_stride + r + h) : 0.f;
-    }
     // max over the partials' m (warp 0), weights into smem
     if (sg == 0) {
         float mx = -INFINITY;
-        for (uint32_t j = lane; j < n; j += 32) mx = fmaxf(mx, __ldcg(base + j * slot_stride + h));
+#pragma unroll
+        for (int k = 0; k < kCombineMaxWarpSlots; ++k)
+            if (lane + 32 * k < n) mx = fmaxf(mx, mv[k]);
+        for (uint32_t j = lane + 32 * kCombineMaxWarpSlots; j < n; j += 32)
+            mx = fmaxf(mx, __ldcg(base + j * slot_stride + h));
         for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        for (uint32_t j = lane; j < n; j += 32) {
+#pragma unroll
+        for (int k = 0; k < kCombineMaxWarpSlots; ++k) {
+            const uint32_t j = lane + 32 * k;
+            if (j < n) s_w[j] = mv[k] == -INFINITY ? 0.f : ptx::ex2(mv[k] - mx);
+        }
+        for (uint32_t j = lane + 32 * kCombineMaxWarpSlots; j < n; j += 32) {
             const float m = __ldcg(base + j * slot_stride + h);
             s_w[j] = m == -INFINITY ? 0.f : ptx::ex2(m - mx);
         }

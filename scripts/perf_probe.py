@@ -13,7 +13,7 @@ t0 = time.time(); spec.fill(cache); print("fill s", time.time() - t0, flush=True
 q = torch.from_numpy(spec.queries()[0]).cuda()
 out = torch.zeros_like(q)
 stream = torch.cuda.ExternalStream(cache.stream)
-for tau, name in ((2.0, "dense"), (0.5, "routed")):
+for tau, name in ((2.0, "dense"), (0.5, "routed"), (-2.0, "allsink")):
     cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(tau), excluded_layers=())
     for _ in range(5):
         P.routed_decode_async(q.data_ptr(), 0, cache, cfg, d_outputs=out.data_ptr())
@@ -44,6 +44,6 @@ for tau, name in ((2.0, "dense"), (0.5, "routed")):
     step_us = e0.elapsed_time(e1) / 20 * 1e3
     nact = info.counters.groups_active
     bytes_ = nact * 2 * L * 128 * 2
-    dmed = np.median(dec[:, 0]) * 1e3
+    dmed = max(np.median(dec[:, 0]) * 1e3, 1e-3)
     print(f"{name}: active={nact} step_us={step_us:.1f} decode_us_med={dmed:.1f} stepev_us={np.median(dec[:,1])*1e3:.1f} "
           f"GB/s(decode)={bytes_/dmed/1e3:.0f} GB/s(step)={bytes_/step_us/1e3:.0f}", flush=True)

@@ -60,6 +60,7 @@ int main() {
     // full skip on a routable layer: bitwise-zero outputs, no KV traffic
     sc::RoutingConfig skip;
     skip.profile = sc::ThresholdProfile::constant(-2.0);
+    skip.excluded_layers = {0};  // layer 1 routable, layer 0 excluded
     auto s = sc::routed_decode_step(q, 1, cache, skip);
     REQUIRE(s.counters.groups_skipped == hkv && s.counters.kv_floats_loaded == 0);
     for (float x : s.outputs) REQUIRE(x == 0.0f && !std::signbit(x));
