@@ -19,7 +19,7 @@
 #include <vector>
 
 #include "../../include/sinkr_cuda.h"
-#include "kernels.cuh"
+#include "step.cuh"
 
 namespace {
 
@@ -131,7 +131,7 @@ struct sinkr_engine {
     uint8_t* d_in = nullptr;
     uint8_t* h_in = nullptr;
     // step result block: out | head_scores | group_scores | tokens | flags
-    size_t off_hs = 0, off_gs = 0, off_tok = 0, off_fl = 0, res_bytes = 0;
+    size_t off_hs = 0, off_gs = 0, off_tok = 0, off_fl = 0, off_status = 0, res_bytes = 0;
     uint8_t* d_res = nullptr;
     uint8_t* h_res = nullptr;
 
@@ -141,6 +141,13 @@ struct sinkr_engine {
     uint32_t* d_slot_count = nullptr;
     float* d_partials = nullptr;
     size_t S = 0, PS = 0;
+    // fused single-kernel step (step.cuh); the 3-kernel pipeline remains for
+    // A/B profiling (SINKR_FUSED=0) and serves the multi-rank merge.
+    bool fused = true;
+    dev::StepState* d_ss = nullptr;
+    uint32_t* d_cursor = nullptr;
+    uint32_t* d_tokens_done = nullptr;
+    unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
 
     CUtensorMap tmk{}, tmv{};
     cudaEvent_t ev[4] = {};
@@ -151,9 +158,11 @@ struct sinkr_engine {
     struct GraphEntry {
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
-        cudaGraphNode_t probe = nullptr;
+        cudaGraphNode_t probe = nullptr;  // the node whose ProbeParams are patched
         cudaKernelNodeParams probe_kp{};
         dev::DevTables probe_t{};
+        dev::StepTables step_t{};
+        bool fused = false;
         dev::ProbeParams pp{};
     };
     std::map<std::tuple<const void*, void*, int>, GraphEntry> graphs;
@@ -196,6 +205,36 @@ struct sinkr_engine {
         t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
         return t;
     }
+    dev::StepTables step_tables(const float* q, float* out, int mode) const {
+        dev::StepTables t{};
+        t.q = q;
+        t.anchors = d_anchor;
+        t.anchor_norm = d_anchor_norm;
+        t.tau_g = reinterpret_cast<const double*>(d_in + off_tau);
+        t.len_g = reinterpret_cast<const uint32_t*>(d_in + off_len);
+        t.head_scores = reinterpret_cast<double*>(d_res + off_hs);
+        t.group_scores = reinterpret_cast<double*>(d_res + off_gs);
+        t.unit_flags = reinterpret_cast<uint32_t*>(d_res + off_fl);
+        t.tokens = reinterpret_cast<unsigned long long*>(d_res + off_tok);
+        t.status = reinterpret_cast<uint32_t*>(d_res + off_status);
+        t.ss = d_ss;
+        t.cursor = d_cursor;
+        t.slot_count = d_slot_count;
+        t.tokens_done = d_tokens_done;
+        t.partials = d_partials;
+        t.out = out;
+        t.B = (uint32_t)B;
+        t.Hq = (uint32_t)cfg.num_q_heads;
+        t.Hkv = (uint32_t)cfg.num_kv_heads;
+        t.r = (uint32_t)r;
+        t.cap = (uint32_t)cap;
+        t.S = (uint32_t)S;
+        t.mode = (uint32_t)mode;
+        t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
+        t.trace = d_trace;
+        return t;
+    }
+    uint32_t* clocks() const { return reinterpret_cast<uint32_t*>(d_res + off_status) + 4; }
 };
 
 namespace {
@@ -266,7 +305,35 @@ static int debug_kernel_mask() {
     return m;
 }
 
+template <int D>
+void launch_step(sinkr_engine* e, const dev::StepTables& st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(e->grid);
+    cfg.blockDim = dim3(dev::kThreads);
+    cfg.dynamicSmemBytes = dev::StepCfg<D>::kSmemBytes;
+    cfg.stream = e->stream;
+    // cooperative: the merge phase waits on other CTAs, so all must be resident
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, dev::step_kernel<D>, e->tmk, e->tmv, st, e->pp));
+}
+
 void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
+    if (e->fused) {
+        const dev::StepTables st = e->step_tables(d_q, d_out, mode);
+        if (e->timing) CK(cudaEventRecord(e->ev[0], e->stream));
+        switch (e->D) {
+            case 32: launch_step<32>(e, st); break;
+            case 64: launch_step<64>(e, st); break;
+            default: launch_step<128>(e, st); break;
+        }
+        if (e->timing) CK(cudaEventRecord(e->ev[3], e->stream));
+        CK(cudaGetLastError());
+        return;
+    }
     const dev::DevTables t = e->tables(d_q);
     const int km = debug_kernel_mask();
     if (e->timing) CK(cudaEventRecord(e->ev[0], e->stream));
@@ -291,7 +358,7 @@ void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
 // (per-phase seconds, like the reference's phase timers).  Otherwise the step
 // is one CUDA-graph replay, bracketed by events outside the graph.
 void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
-    e->last_launches = 3;
+    e->last_launches = e->fused ? 1 : 3;
     e->last_mode = mode;
     if (e->timing) {
         enqueue_step(e, d_q, d_out, mode);
@@ -316,9 +383,13 @@ void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
         CK(cudaGraphGetNodes(ge.graph, nullptr, &n));
         std::vector<cudaGraphNode_t> nodes(n);
         CK(cudaGraphGetNodes(ge.graph, nodes.data(), &n));
-        const void* probe_fn = e->D == 32 ? (const void*)dev::probe_kernel<32>
-                             : e->D == 64 ? (const void*)dev::probe_kernel<64>
-                                          : (const void*)dev::probe_kernel<128>;
+        const void* probe_fn =
+            e->fused ? (e->D == 32 ? (const void*)dev::step_kernel<32>
+                        : e->D == 64 ? (const void*)dev::step_kernel<64>
+                                     : (const void*)dev::step_kernel<128>)
+                     : (e->D == 32 ? (const void*)dev::probe_kernel<32>
+                        : e->D == 64 ? (const void*)dev::probe_kernel<64>
+                                     : (const void*)dev::probe_kernel<128>);
         for (auto nd : nodes) {
             cudaGraphNodeType ty;
             CK(cudaGraphNodeGetType(nd, &ty));
@@ -333,15 +404,18 @@ void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
         if (!ge.probe && (debug_kernel_mask() & 1))
             fail(SINKR_CUDA_ERROR, "probe node not found in the captured graph");
         ge.probe_t = e->tables(d_q);
+        ge.step_t = e->step_tables(d_q, d_out, mode);
+        ge.fused = e->fused;
         ge.pp = e->pp;
         it = e->graphs.emplace(key, ge).first;
     }
     auto& ge = it->second;
     if (ge.probe && std::memcmp(&ge.pp, &e->pp, sizeof(e->pp)) != 0) {
         ge.pp = e->pp;
-        void* args[2] = {&ge.probe_t, &ge.pp};
+        void* args3[2] = {&ge.probe_t, &ge.pp};
+        void* args1[4] = {&e->tmk, &e->tmv, &ge.step_t, &ge.pp};
         cudaKernelNodeParams kp = ge.probe_kp;
-        kp.kernelParams = args;
+        kp.kernelParams = ge.fused ? args1 : args3;
         kp.extra = nullptr;
         CK(cudaGraphExecKernelNodeSetParams(ge.exec, ge.probe, &kp));
     }
@@ -440,7 +514,17 @@ void fill_info(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg,
     }
     c.anchor_floats_loaded = (uint64_t)(e->U * e->D);
     if (head_scores) std::memcpy(head_scores, hs, e->B * Hq * sizeof(double));
-    if (e->timing) {
+    if (e->fused) {
+        // device-side phase stamps (%globaltimer, ns) written by the step kernel
+        const auto* st = reinterpret_cast<const uint32_t*>(e->h_res + e->off_status);
+        const auto* clk = reinterpret_cast<const unsigned long long*>(st + 4);
+        if (st[0]) fail(SINKR_RUNTIME_ERROR, "decode partial-slot overflow");
+        if (clk[1] >= clk[0] && clk[2] >= clk[1] && clk[3] >= clk[2]) {
+            c.routing_seconds = (clk[1] - clk[0]) * 1e-9;
+            c.attention_seconds = (clk[2] - clk[1]) * 1e-9;
+            c.merge_seconds = (clk[3] - clk[2]) * 1e-9;
+        }
+    } else if (e->timing) {
         float ms[3] = {0, 0, 0};
         for (int i = 0; i < 3; ++i) CK(cudaEventElapsedTime(&ms[i], e->ev[i], e->ev[i + 1]));
         c.routing_seconds = ms[0] * 1e-3;
@@ -557,18 +641,35 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->off_gs = align_up(e->off_hs + e->B * Hq * 8, 128);
             e->off_tok = align_up(e->off_gs + e->U * 8, 128);
             e->off_fl = align_up(e->off_tok + e->U * 8, 128);
-            e->res_bytes = align_up(e->off_fl + e->U * 4, 128);
+            e->off_status = align_up(e->off_fl + e->U * 4, 128);  // status[4] + clocks
+            e->res_bytes = align_up(e->off_status + 64 + 256, 128);
             CK(cudaMalloc(&e->d_res, e->res_bytes));
             CK(cudaMallocHost(&e->h_res, e->res_bytes));
             CK(cudaMemsetAsync(e->d_res, 0, e->res_bytes, e->stream));
 
             CK(cudaMalloc(&e->d_head_degen, e->B * Hq * 4));
             e->probe_grid = (int)((e->B * Hq + dev::kProbeHeads - 1) / dev::kProbeHeads);
+            CK(cudaMalloc(&e->d_ss, sizeof(dev::StepState)));
+            CK(cudaMemsetAsync(e->d_ss, 0, sizeof(dev::StepState), e->stream));
+            CK(cudaMalloc(&e->d_cursor, e->U * 4));
+            CK(cudaMemsetAsync(e->d_cursor, 0, e->U * 4, e->stream));
+            CK(cudaMalloc(&e->d_tokens_done, e->U * 4));
+            CK(cudaMemsetAsync(e->d_tokens_done, 0, e->U * 4, e->stream));
+            if (const char* tr = std::getenv("SINKR_TRACE"); tr && tr[0] == '1') {
+                CK(cudaMalloc(&e->d_trace, e->grid * 4 * 8));
+                CK(cudaMemsetAsync(e->d_trace, 0, e->grid * 4 * 8, e->stream));
+            }
+            {
+                const char* f = std::getenv("SINKR_FUSED");
+                e->fused = !(f && f[0] == '0') && e->U <= (size_t)dev::kMaxUnits &&
+                           e->B * Hq <= (size_t)dev::kMaxStepHeads;
+            }
             CK(cudaMalloc(&e->d_ws, sizeof(dev::WorkState)));
             CK(cudaMemsetAsync(e->d_ws, 0, sizeof(dev::WorkState), e->stream));
             CK(cudaMalloc(&e->d_active, e->U * 16));
             CK(cudaMalloc(&e->d_prefix, (e->U + 1) * 4));  // unit_next cursors
             CK(cudaMalloc(&e->d_slot_count, e->U * 4));
+            CK(cudaMemsetAsync(e->d_slot_count, 0, e->U * 4, e->stream));
             // one flush per (CTA, unit) at most: S = min(grid, stages per slot)
             e->S = std::min<size_t>(e->grid, (e->cap + dev::kStageTok - 1) / dev::kStageTok);
             e->PS = e->r * (e->D + 2);
@@ -585,6 +686,13 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaFuncSetAttribute(dev::decode_kernel<128>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem_bytes<128>()));
+            CK(cudaFuncSetAttribute(dev::step_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dev::StepCfg<32>::kSmemBytes));
+            CK(cudaFuncSetAttribute(dev::step_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dev::StepCfg<64>::kSmemBytes));
+            CK(cudaFuncSetAttribute(dev::step_kernel<128>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dev::StepCfg<128>::kSmemBytes));
             CK(cudaFuncSetAttribute(dev::probe_kernel<32>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
             CK(cudaFuncSetAttribute(dev::probe_kernel<64>,
@@ -630,6 +738,9 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_in);
     cudaFree(e->d_res);
     cudaFree(e->d_ws);
+    cudaFree(e->d_ss);
+    cudaFree(e->d_cursor);
+    cudaFree(e->d_tokens_done);
     cudaFree(e->d_head_degen);
     cudaFree(e->d_active);
     cudaFree(e->d_prefix);
@@ -885,9 +996,11 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
         run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, 0);
         CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
-        dev::WorkState ws;
-        CK(cudaMemcpy(&ws, e->d_ws, sizeof(ws), cudaMemcpyDeviceToHost));
-        if (ws.error) fail(SINKR_RUNTIME_ERROR, "decode partial-slot overflow");
+        if (!e->fused) {
+            dev::WorkState ws;
+            CK(cudaMemcpy(&ws, e->d_ws, sizeof(ws), cudaMemcpyDeviceToHost));
+            if (ws.error) fail(SINKR_RUNTIME_ERROR, "decode partial-slot overflow");
+        }
         if (outputs) std::memcpy(outputs, e->h_res, qbytes);
         fill_info(e, layer, config, groups, head_scores, counters, options);
     });
@@ -923,7 +1036,10 @@ sinkr_status sinkr_fetch_step_info(sinkr_engine* e, sinkr_group_info* groups,
         if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
         CK(cudaMemcpyAsync(e->h_res + e->off_hs, e->d_res + e->off_hs, e->res_bytes - e->off_hs,
                            cudaMemcpyDeviceToHost, e->stream));
-        check_error_flag(e);
+        if (e->fused)
+            CK(cudaStreamSynchronize(e->stream));
+        else
+            check_error_flag(e);
         const auto* hdr = reinterpret_cast<const dev::StepHdr*>(e->h_in);
         fill_info(e, hdr->layer, nullptr, groups, head_scores, counters, nullptr);
     });
@@ -964,7 +1080,8 @@ sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches, f
         if (kernel_launches) *kernel_launches = e->last_launches;
         if (decode_ms) {
             *decode_ms = 0.f;
-            if (e->timing) CK(cudaEventElapsedTime(decode_ms, e->ev[1], e->ev[2]));
+            if (e->timing)
+                CK(cudaEventElapsedTime(decode_ms, e->ev[e->fused ? 0 : 1], e->ev[e->fused ? 3 : 2]));
         }
         if (step_ms) CK(cudaEventElapsedTime(step_ms, e->ev[0], e->ev[3]));
     });
@@ -975,6 +1092,23 @@ sinkr_status sinkr_step_io_bytes(sinkr_engine* e, size_t* h2d, size_t* d2h) {
         if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
         if (h2d) *h2d = e->in_bytes;
         if (d2h) *d2h = e->res_bytes;
+    });
+}
+
+// debug: cycle stamps of the last fused step (lead CTA), valid after fetch_step_info
+extern "C" sinkr_status sinkr_debug_trace(sinkr_engine* e, unsigned long long* out) {
+    return guard([&] {
+        if (!e->d_trace) fail(SINKR_INVALID_ARGUMENT, "tracing disabled (SINKR_TRACE=1)");
+        CK(cudaStreamSynchronize(e->stream));
+        CK(cudaMemcpy(out, e->d_trace, e->grid * 4 * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemset(e->d_trace, 0, e->grid * 4 * 8));
+    });
+}
+
+extern "C" sinkr_status sinkr_debug_stamps(sinkr_engine* e, unsigned long long* out, int n) {
+    return guard([&] {
+        const auto* st = reinterpret_cast<const unsigned long long*>(e->h_res + e->off_status + 48);
+        for (int i = 0; i < n && i < 32; ++i) out[i] = st[i];
     });
 }
 

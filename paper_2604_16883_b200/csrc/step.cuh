@@ -1,0 +1,795 @@
+// step.cuh — the whole SinkRouter decode step in ONE persistent, cooperative
+// sm_100a kernel (one CTA per SM):
+//
+//   phase R  routing (router.cpp:36-75,100-125): every CTA redundantly scores
+//            the query heads against the cached token-0 keys (exact fp64
+//            products, sequential sums, IEEE sqrt/div — bit-exact with the
+//            reference), takes the sequential group mean, compares with tau
+//            and compacts the Active groups into a work list in its own shared
+//            memory.  No inter-CTA traffic; CTA 0 publishes the routing record.
+//   phase S  Split-K flash-decode (attend_chunk, attention.cpp:101-142) over the
+//            Active groups only: TMA producer warp + 4 mma.sync consumer warps
+//            per CTA, unit-affine dynamic chunk claims (or one flat cursor when
+//            there are more Active groups than SMs).
+//   phase M  LSE merge (merge_partials, attention.cpp:159-183): with few Active
+//            groups the (group, head, 32-dim) merge tasks are spread over all
+//            CTAs once a group's last row has been streamed; with many groups
+//            the CTA that streams a group's last rows merges it.
+//
+// The last CTA to leave restores the cross-CTA counters to zero for the next
+// step, so the launch needs no memset and replays as a single graph node.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace sinkr {
+namespace dev {
+
+constexpr int kMaxUnits = 1536;      // B * H_kv per step
+constexpr int kMaxStepHeads = 4096;  // B * H_q per step
+constexpr int kRouteTile = 64;       // heads per routing tile
+constexpr int kRouteSub = 32;        // heads per load batch
+
+struct StepState {
+    unsigned int flat_counter;
+    unsigned int merge_next;
+    unsigned int exit_count;
+    unsigned int error;
+    unsigned int pad[4];
+};
+
+struct StepTables {
+    const float* q;                // [B][Hq][D]
+    const float* anchors;          // [layers][B][Hkv][D]
+    const float* anchor_norm;      // [layers][B][Hkv]
+    const double* tau_g;           // [B] (when params are not inline)
+    const uint32_t* len_g;         // [B]
+    double* head_scores;           // result [B*Hq]
+    double* group_scores;          // result [U]
+    uint32_t* unit_flags;          // result [U]
+    unsigned long long* tokens;    // result [U] rows streamed (the skipped-block record)
+    uint32_t* status;              // result: nonzero = partial-slot overflow
+    StepState* ss;
+    uint32_t* cursor;              // [U] chunk cursor per active-list entry
+    uint32_t* slot_count;          // [U]
+    uint32_t* tokens_done;         // [U]
+    float* partials;               // [U][S][r*(D+2)]: m[r], l[r], acc[r][D]
+    float* out;                    // mode 0: [B][Hq][D]; mode 1: [U][r][D+2]
+    uint32_t B, Hq, Hkv, r, cap, S, mode;
+    float qscale;                  // (1/sqrt(D)) * log2(e)
+    unsigned long long* trace;     // optional [grid][4] per-CTA globaltimer stamps
+};
+
+template <int D>
+struct StepCfg {
+    using C = Cfg<D>;
+    static constexpr int kRing = C::kStages * C::kStageBytes;
+    static constexpr int kOffBars = kRing;
+    static constexpr int kOffMeta = kOffBars + 2 * C::kStages * 8;
+    static constexpr int kOffO = kOffMeta + C::kStages * 16;
+    static constexpr int kOffML = kOffO + kCWarps * kMaxR * C::kOStride * 4;
+    static constexpr int kOffMisc = kOffML + kCWarps * kMaxR * 2 * 4;
+    static constexpr int kOffAct = kOffMisc + 64;
+    static constexpr int kOffPrefix = kOffAct + kMaxUnits * 2;
+    static constexpr int kBytes = kOffPrefix + (kMaxUnits + 1) * 4;
+    static constexpr int kSmemBytes = 1024 + kBytes;
+    // routing overlay (inside the ring, before streaming starts)
+    static constexpr int kDP = D + 1;
+    static constexpr int kOvProd = 0;  // q, k0 [2][kRouteTile][D+1] f32 + chains [2][kRouteTile] f64
+    static constexpr int kOvScore = (2 * kRouteTile * kDP * 8 + 2 * kRouteTile * 8 + 15) / 16 * 16;
+    static constexpr int kOvDegen = kOvScore + kMaxStepHeads * 8;         // [kMaxStepHeads] u8
+    static_assert(kOvDegen + kMaxStepHeads <= kRing, "routing overlay exceeds the ring");
+    static_assert(kSmemBytes <= 232448, "step kernel shared memory");
+};
+
+// misc smem words
+enum : int { kMiscNact = 0, kMiscChunk, kMiscQueue, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat };
+
+// Split-K chunk plan of one unit of L rows: big chunks of C rows, then a tail
+// of `tail` (or more) rows cut into small chunks of c rows so the last claims
+// are short and every SM finishes within ~one small chunk of the others.
+struct ChunkPlan {
+    uint32_t C, c, tail;
+};
+__device__ __forceinline__ uint32_t plan_nb(uint32_t L, const ChunkPlan& cp) {
+    return L > cp.tail ? (L - cp.tail) / cp.C : 0u;
+}
+__device__ __forceinline__ uint32_t plan_nch(uint32_t L, const ChunkPlan& cp) {
+    const uint32_t nb = plan_nb(L, cp);
+    return nb + (L - nb * cp.C + cp.c - 1) / cp.c;
+}
+__device__ __forceinline__ void plan_range(uint32_t L, uint32_t k, const ChunkPlan& cp,
+                                           uint32_t& t0, uint32_t& t1) {
+    const uint32_t nb = plan_nb(L, cp);
+    if (k < nb) {
+        t0 = k * cp.C;
+        t1 = t0 + cp.C;
+    } else {
+        t0 = nb * cp.C + (k - nb) * cp.c;
+        t1 = min(t0 + cp.c, L);
+    }
+}
+constexpr uint32_t kTailChunkTok = 64;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+    return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    step_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                StepTables t, const ProbeParams p) {
+    using C = Cfg<D>;
+    using SC = StepCfg<D>;
+    using Scan = cub::BlockScan<uint32_t, kThreads>;
+    using Reduce = cub::BlockReduce<unsigned long long, kThreads>;
+    __shared__ union {
+        typename Scan::TempStorage scan;
+        typename Reduce::TempStorage reduce;
+    } tmp;
+    __shared__ unsigned long long s_tok_total;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + SC::kOffBars);
+    uint64_t* empty = full + C::kStages;
+    StageMeta* meta = reinterpret_cast<StageMeta*>(smem + SC::kOffMeta);
+    float* sm_o = reinterpret_cast<float*>(smem + SC::kOffO);
+    float* sm_ml = reinterpret_cast<float*>(smem + SC::kOffML);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + SC::kOffMisc);
+    uint16_t* act_unit = reinterpret_cast<uint16_t*>(smem + SC::kOffAct);
+    uint32_t* act_prefix = reinterpret_cast<uint32_t*>(smem + SC::kOffPrefix);
+    double* s_score = reinterpret_cast<double*>(ring + SC::kOvScore);
+    uint8_t* s_degen = ring + SC::kOvDegen;
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t G = gridDim.x, bid = blockIdx.x;
+    const uint32_t U = t.B * t.Hkv, NH = t.B * t.Hq, r = t.r;
+    const uint32_t layer = p.layer, flags = p.flags;
+    const bool lead = bid == 0;
+    unsigned long long* clk = reinterpret_cast<unsigned long long*>(t.status + 4);
+    if (lead && tid == 0) clk[0] = globaltimer();
+    unsigned long long* dbg = clk + 4;  // debug cycle stamps (lead CTA, thread 0)
+#define STAMP(i) do { if (lead && tid == 0) dbg[i] = clock64(); } while (0)
+    STAMP(0);
+
+    if (tid == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], kCWarps);
+        }
+        ptx::fence_mbar_init();
+        ptx::tma_prefetch_desc(&tmk);
+        ptx::tma_prefetch_desc(&tmv);
+    }
+
+    STAMP(1);
+    // ======================= phase R: routing ================================
+    // proxy_score (router.cpp:36-48): head i belongs to unit i / r.  q and k0
+    // rows are staged in smem as f32 (coalesced loads, all issued up front);
+    // then thread h runs the dot chain and thread 64+h the |q|^2 chain, each a
+    // sequential fp64 FMA chain in index order.  A product of two floats is
+    // exact in fp64, so fma(q_j, k_j, s) == round(s + q_j*k_j): bit-identical to
+    // the reference's `s += (double)q[i] * k0[i]`.
+    {
+        double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1] f64
+        double* sk = sq + kRouteTile * SC::kDP;
+        double* s_chain = sk + kRouteTile * SC::kDP;  // [2][kRouteTile]
+        for (uint32_t h_base = 0; h_base < NH; h_base += kRouteTile) {
+            const uint32_t nh = min((uint32_t)kRouteTile, NH - h_base);
+            // warp w loads heads w, w+5, ...; lane l loads dims l, l+32, ... (coalesced;
+            // one integer division per head)
+            constexpr int kW = kThreads / 32;
+            constexpr int kHPW = (kRouteTile + kW - 1) / kW;
+            constexpr int kJL = D / 32;
+            float qv[kHPW][kJL], kv[kHPW][kJL];
+#pragma unroll
+            for (int a = 0; a < kHPW; ++a) {
+                const uint32_t hl = warp + a * kW;
+                const bool ok = hl < nh;
+                const uint32_t i = h_base + (ok ? hl : 0);
+                const float* qrow = t.q + size_t(i) * D;
+                const float* krow = t.anchors + (size_t(layer) * U + i / r) * D;
+#pragma unroll
+                for (int b = 0; b < kJL; ++b) {
+                    qv[a][b] = ok ? __ldg(qrow + lane + 32 * b) : 0.f;
+                    kv[a][b] = ok ? __ldg(krow + lane + 32 * b) : 0.f;
+                }
+            }
+            double kn = 1.0;
+            if (tid < nh) kn = (double)__ldg(&t.anchor_norm[size_t(layer) * U + (h_base + tid) / r]);
+            // exact fp64 products (f32 x f32 fits in 53 bits), off the chain
+#pragma unroll
+            for (int a = 0; a < kHPW; ++a) {
+                const uint32_t hl = warp + a * kW;
+                if (hl < nh) {
+#pragma unroll
+                    for (int b = 0; b < kJL; ++b) {
+                        const double qd = (double)qv[a][b];
+                        sq[hl * SC::kDP + lane + 32 * b] = __dmul_rn(qd, (double)kv[a][b]);
+                        sk[hl * SC::kDP + lane + 32 * b] = __dmul_rn(qd, qd);
+                    }
+                }
+            }
+            __syncthreads();
+            STAMP(2);
+            if (tid < 2 * kRouteTile && (tid % kRouteTile) < nh) {
+                const uint32_t hl = tid % kRouteTile;
+                // thread h: the dot chain; thread 64+h: the |q|^2 chain, each a
+                // sequential sum in index order (router.cpp:40-43)
+                const double* a = (tid < (uint32_t)kRouteTile ? sq : sk) + hl * SC::kDP;
+                double acc = 0.0;
+#pragma unroll 16
+                for (uint32_t j = 0; j < D; ++j) acc = __dadd_rn(acc, a[j]);
+                s_chain[tid] = acc;
+            }
+            __syncthreads();
+            if (tid < nh) {
+                const double dot = s_chain[tid], qsq = s_chain[kRouteTile + tid];
+                const double qn = __dsqrt_rn(qsq);
+                double sc = 0.0;
+                uint8_t dg = 0;
+                if (qn < 1e-12) {
+                    dg = 1;
+                } else {
+                    sc = __ddiv_rn(dot, __dmul_rn(qn, kn));
+                    sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
+                }
+                s_score[h_base + tid] = sc;
+                s_degen[h_base + tid] = dg;
+            }
+            __syncthreads();
+            STAMP(3);
+        }
+    }
+
+    // group_score + route (router.cpp:50-57,67-75,113-120) on contiguous unit
+    // runs per thread, then an order-preserving scan builds the Active list.
+    const uint32_t per = (U + kThreads - 1) / kThreads;
+    const uint32_t u0 = min(U, tid * per), u1 = min(U, u0 + per);
+    uint32_t my_active = 0;
+    unsigned long long my_tok = 0;
+    uint64_t my_bits = 0;  // active bits of this thread's run (per <= 64 guaranteed)
+    for (uint32_t u = u0; u < u1; ++u) {
+        const uint32_t seq = u / t.Hkv;
+        double sum = 0.0;
+        uint32_t degen = 0;
+        for (uint32_t i = 0; i < r; ++i) {
+            sum = __dadd_rn(sum, s_score[u * r + i]);
+            degen |= s_degen[u * r + i];
+        }
+        const double S = __ddiv_rn(sum, (double)r);
+        const double tau = p.inline_seqs ? p.tau[seq] : __ldg(&t.tau_g[seq]);
+        const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
+        bool sink = over && !(flags & kLayerExcluded);
+        if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
+        const bool active = (flags & kObserveOnly) || !sink;
+        if (active) {
+            ++my_active;
+            my_tok += p.inline_seqs ? p.len[seq] : __ldg(&t.len_g[seq]);
+            my_bits |= 1ull << (u - u0);
+        }
+        if (lead) {
+            t.group_scores[u] = S;
+            t.unit_flags[u] =
+                (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
+            if (!active) {
+                t.tokens[u] = 0ull;
+                if (t.mode == 1) {  // rank partial of a skipped group: empty
+                    float* P = t.out + size_t(u) * r * (D + 2);
+                    for (uint32_t h = 0; h < r; ++h) {
+                        P[h] = -INFINITY;
+                        P[r + h] = 0.f;
+                    }
+                    for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+                }
+            }
+        }
+    }
+    const unsigned long long tok_all = Reduce(tmp.reduce).Sum(my_tok);
+    STAMP(4);
+    if (tid == 0) s_tok_total = tok_all;
+    __syncthreads();
+    STAMP(5);
+    uint32_t a_off, nact;
+    Scan(tmp.scan).ExclusiveSum(my_active, a_off, nact);
+    STAMP(6);
+    // chunk size: ~kChunksPerCta chunks per CTA, >= kMinChunkTok, stage multiple
+    const unsigned long long T = s_tok_total;
+    const uint32_t gdiv = G * kChunksPerCta;
+    unsigned long long cc = T < (1ull << 32)
+                                ? (unsigned long long)(((uint32_t)T + gdiv - 1) / gdiv)
+                                : (T + gdiv - 1) / gdiv;
+    cc = ((cc + kStageTok - 1) / kStageTok) * kStageTok;
+    if (cc < kMinChunkTok) cc = kMinChunkTok;
+    const uint32_t Ck = (uint32_t)cc;
+    const bool flat = nact > G;
+    ChunkPlan cp;
+    cp.C = Ck;
+    cp.c = kTailChunkTok;
+    cp.tail = ((G + nact - 1) / max(nact, 1u) + 1) * 2 * kTailChunkTok;
+    uint32_t my_chunks = 0;
+    {
+        uint32_t a = a_off;
+        for (uint32_t u = u0; u < u1; ++u) {
+            if (!((my_bits >> (u - u0)) & 1ull)) continue;
+            act_unit[a++] = (uint16_t)u;
+            const uint32_t L = p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
+            my_chunks += plan_nch(L, cp);
+        }
+    }
+    if (flat) {
+        __syncthreads();
+        uint32_t c_off, c_tot;
+        Scan(tmp.scan).ExclusiveSum(my_chunks, c_off, c_tot);
+        uint32_t a = a_off;
+        for (uint32_t u = u0; u < u1; ++u) {
+            if (!((my_bits >> (u - u0)) & 1ull)) continue;
+            act_prefix[a++] = c_off;
+            const uint32_t L = p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
+            c_off += plan_nch(L, cp);
+        }
+        if (tid == 0) act_prefix[nact] = c_tot;
+    }
+    if (tid == 0) {
+        misc[kMiscNact] = nact;
+        misc[kMiscChunk] = Ck;
+        // few, long Active groups: merge tasks spread over all CTAs at the end;
+        // many groups: the CTA that streams a group's last rows merges it.
+        misc[kMiscQueue] = (4 * nact <= G) ? 1u : 0u;
+        misc[kMiscFlat] = flat ? 1u : 0u;
+    }
+    if (lead)
+        for (uint32_t i = tid; i < NH; i += kThreads) t.head_scores[i] = s_score[i];
+    STAMP(7);
+    // zero surrogate rows of Sink groups (router.cpp:97): sink unit u is
+    // written by CTA u mod G (binary search of the sorted Active list)
+    if (t.mode == 0 && nact < U) {
+        for (uint32_t u = bid; u < U; u += G) {
+            uint32_t lo = 0, hi = nact;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (act_unit[mid] < u) lo = mid + 1; else hi = mid;
+            }
+            if (lo < nact && act_unit[lo] == u) continue;
+            float4* row = reinterpret_cast<float4*>(t.out + size_t(u) * r * D);
+            for (uint32_t k = tid; k < r * D / 4; k += kThreads) row[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __syncthreads();  // routing overlay dead from here on; the ring is free
+    STAMP(8);
+    if (t.trace && tid == 0) t.trace[bid * 4 + 0] = globaltimer();
+    const bool queue_mode = misc[kMiscQueue] != 0;
+    if (lead && tid == 0) clk[1] = globaltimer();
+
+    // ======================= phase S: stream + attend ==========================
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol = ptx::policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            auto emit = [&](uint32_t u, uint32_t L, uint32_t t0, uint32_t t1) {
+                const int32_t row0 = (int32_t)((size_t(layer) * U + u) * t.cap);
+                for (uint32_t tk = t0; tk < t1; tk += kStageTok) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
+                    meta[stage].unit = u;
+                    meta[stage].tok0 = tk;
+                    meta[stage].ntok = min((uint32_t)kStageTok, t1 - tk);
+                    meta[stage].pad = L;
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    uint8_t* kd = ring + stage * C::kStageBytes;
+                    uint8_t* vd = kd + C::kTileBytes;
+#pragma unroll
+                    for (int h = 0; h < C::kHalves; ++h) {
+                        ptx::tma_load_2d(kd + h * kStageTok * 128, &tmk, h * C::kBoxDim,
+                                         row0 + (int32_t)tk, &full[stage], pol);
+                        ptx::tma_load_2d(vd + h * kStageTok * 128, &tmv, h * C::kBoxDim,
+                                         row0 + (int32_t)tk, &full[stage], pol);
+                    }
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            };
+            auto unit_len = [&](uint32_t u) {
+                return p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
+            };
+            if (nact > 0 && !flat) {
+                // Unit-affine guided self-scheduling over TOKEN cursors.  CTA c
+                // starts on Active entry c mod nact with the static range
+                // [k*Ck, (k+1)*Ck), k = c / nact.  Later claims take tokens past
+                // the statically covered prefix base(a)*Ck; their size shrinks
+                // with the unit's remaining rows (guided), down to one 64-token
+                // stage, so all SMs finish within about one stage of each other.
+                // An exhausted unit hands the CTA on to the next entry.
+                const uint32_t cpu = (G + nact - 1) / nact;  // CTAs per unit
+                uint32_t a = bid % nact, visited = 1;
+                uint32_t u = act_unit[a], L = unit_len(u);
+                uint32_t first = ((G - a + nact - 1) / nact) * Ck;
+                uint32_t t0 = (bid / nact) * Ck, t1 = min(t0 + Ck, L);
+                auto guided = [&](uint32_t hint) {
+                    const uint32_t rem = L > hint ? L - hint : 0u;
+                    uint32_t sz = rem / (3 * cpu);
+                    sz = sz / kStageTok * kStageTok;
+                    return sz < (uint32_t)kStageTok ? (uint32_t)kStageTok : (sz > Ck ? Ck : sz);
+                };
+                for (;;) {
+                    if (t0 >= L) {
+                        if (visited == nact) break;
+                        ++visited;
+                        a = (a + 1 == nact) ? 0 : a + 1;
+                        u = act_unit[a];
+                        L = unit_len(u);
+                        first = ((G - a + nact - 1) / nact) * Ck;
+                        const uint32_t sz = guided(first);
+                        t0 = first + atomicAdd(&t.cursor[a], sz);
+                        t1 = min(t0 + sz, L);
+                        continue;
+                    }
+                    // prefetch the next claim of this unit (sized from our position)
+                    const uint32_t sz = guided(max(t0, first));
+                    const uint32_t n0 = first + atomicAdd(&t.cursor[a], sz);
+                    emit(u, L, t0, t1);
+                    t0 = n0;
+                    t1 = min(n0 + sz, L);
+                }
+            } else if (nact > 0) {
+                // many Active groups: one flat chunk cursor over the active list
+                const uint32_t total = act_prefix[nact];
+                uint32_t chunk = bid, a = 0;
+                while (chunk < total) {
+                    const uint32_t next = G + atomicAdd(&t.ss->flat_counter, 1u);
+                    // act_prefix is sorted: advance (chunk ids of one CTA increase)
+                    uint32_t lo = a, hi = nact;
+                    while (hi - lo > 1) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (act_prefix[mid] <= chunk) lo = mid; else hi = mid;
+                    }
+                    a = lo;
+                    const uint32_t u = act_unit[a], L = unit_len(u);
+                    const uint32_t k = chunk - act_prefix[a];
+                    uint32_t t0, t1;
+                    plan_range(L, k, cp, t0, t1);
+                    emit(u, L, t0, t1);
+                    chunk = next;
+                }
+            }
+            ptx::mbar_wait(&empty[stage], phase ^ 1u);
+            meta[stage].unit = kEnd;
+            ptx::mbar_arrive(&full[stage]);
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------ consumers ------------------------------
+        const int cw = warp - 1;
+        const uint32_t ctid = tid - 32;
+        const int tb = cw * kWarpTok;
+        const int grp = lane >> 2, qd = lane & 3;
+        const int lj = lane >> 3, li = lane & 7;
+        const uint32_t k_tok = tb + ((lj >> 1) << 3) + li, k_csel = lj & 1;
+        const uint32_t v_tok = tb + ((lj & 1) << 3) + li, v_csel = lj >> 1;
+        const uint32_t PS = r * (D + 2);
+
+        uint32_t qa[C::kNK][4];
+        float o[2 * C::kNK][4];
+        float m_used = -INFINITY, l_acc = 0.f;
+        uint32_t cur = kEnd, cur_len = 0, run_tokens = 0;
+
+        auto reset_state = [&]() {
+#pragma unroll
+            for (int i = 0; i < 2 * C::kNK; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+            m_used = -INFINITY;
+            l_acc = 0.f;
+        };
+        auto load_q = [&](uint32_t u) {
+            const bool live = grp < (int)r;
+            const float* qrow = t.q + (size_t(u) * r + (live ? grp : 0)) * D;
+#pragma unroll
+            for (int kk = 0; kk < C::kNK; ++kk) {
+                float2 x = make_float2(0.f, 0.f), y = make_float2(0.f, 0.f);
+                if (live) {
+                    x = *reinterpret_cast<const float2*>(qrow + 16 * kk + 2 * qd);
+                    y = *reinterpret_cast<const float2*>(qrow + 16 * kk + 8 + 2 * qd);
+                }
+                x.x *= t.qscale; x.y *= t.qscale; y.x *= t.qscale; y.y *= t.qscale;
+                const uint32_t xh = ptx::pack_bf16(x.x, x.y), yh = ptx::pack_bf16(y.x, y.y);
+                qa[kk][0] = xh;
+                qa[kk][1] = ptx::pack_bf16(x.x - ptx::bf16_lo_as_f32(xh), x.y - ptx::bf16_hi_as_f32(xh));
+                qa[kk][2] = yh;
+                qa[kk][3] = ptx::pack_bf16(y.x - ptx::bf16_lo_as_f32(yh), y.y - ptx::bf16_hi_as_f32(yh));
+            }
+        };
+        // merge every partial of unit u (consumers only; few partials)
+        auto merge_unit = [&](uint32_t u, uint32_t L) {
+            const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
+            const float* base = t.partials + size_t(u) * t.S * PS;
+            for (uint32_t idx = ctid; idx < r * D; idx += kCWarps * 32) {
+                const uint32_t h = idx / D, d = idx % D;
+                float mx = -INFINITY;
+                for (uint32_t j = 0; j < n; ++j) mx = fmaxf(mx, __ldcg(base + j * PS + h));
+                float acc = 0.f, lsum = 0.f;
+                for (uint32_t j = 0; j < n; ++j) {
+                    const float m = __ldcg(base + j * PS + h);
+                    const float w = m == -INFINITY ? 0.f : ptx::ex2(m - mx);
+                    acc += __ldcg(base + j * PS + 2 * r + h * D + d) * w;
+                    lsum += __ldcg(base + j * PS + r + h) * w;
+                }
+                if (t.mode == 0) {
+                    t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
+                } else {
+                    float* P = t.out + size_t(u) * PS;
+                    if (d == 0) {
+                        P[h] = mx;
+                        P[r + h] = lsum;
+                    }
+                    P[2 * r + h * D + d] = acc;
+                }
+            }
+            if (ctid == 0) t.tokens[u] = L;
+        };
+        auto flush = [&](uint32_t u, uint32_t L) {
+            float l_tot = l_acc + __shfl_xor_sync(0xffffffffu, l_acc, 1);
+            l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
+            if (grp < (int)r) {
+                float* so = sm_o + (cw * kMaxR + grp) * C::kOStride;
+#pragma unroll
+                for (int nt = 0; nt < 2 * C::kNK; ++nt) {
+                    so[8 * nt + 2 * qd] = o[nt][0] + o[nt][2];
+                    so[8 * nt + 2 * qd + 1] = o[nt][1] + o[nt][3];
+                }
+                if (qd == 0) {
+                    sm_ml[(cw * kMaxR + grp) * 2] = m_used;
+                    sm_ml[(cw * kMaxR + grp) * 2 + 1] = l_tot;
+                }
+            }
+            if (ctid == 0) misc[kMiscSlot] = atomicAdd(&t.slot_count[u], 1u);
+            ptx::named_bar_sync(1, kCWarps * 32);
+            const uint32_t slot = misc[kMiscSlot];
+            if (slot < t.S) {
+                float* P = t.partials + (size_t(u) * t.S + slot) * PS;
+                for (uint32_t idx = ctid; idx < r * D; idx += kCWarps * 32) {
+                    const uint32_t h = idx / D, d = idx % D;
+                    float mx = -INFINITY;
+#pragma unroll
+                    for (int w = 0; w < kCWarps; ++w) mx = fmaxf(mx, sm_ml[(w * kMaxR + h) * 2]);
+                    float acc = 0.f, lsum = 0.f;
+#pragma unroll
+                    for (int w = 0; w < kCWarps; ++w) {
+                        const float sc = ptx::ex2(sm_ml[(w * kMaxR + h) * 2] - mx);
+                        acc += sm_o[(w * kMaxR + h) * C::kOStride + d] * sc;
+                        lsum += sm_ml[(w * kMaxR + h) * 2 + 1] * sc;
+                    }
+                    P[2 * r + h * D + d] = acc;
+                    if (d == 0) {
+                        P[h] = mx;
+                        P[r + h] = lsum;
+                    }
+                }
+            } else if (ctid == 0) {
+                atomicExch(&t.ss->error, 1u);
+            }
+            __threadfence();  // partial visible before this run's rows are counted
+            ptx::named_bar_sync(1, kCWarps * 32);
+            if (ctid == 0) {
+                const uint32_t done = atomicAdd(&t.tokens_done[u], run_tokens) + run_tokens;
+                misc[kMiscLast] = (done == L) ? 1u : 0u;
+            }
+            ptx::named_bar_sync(1, kCWarps * 32);
+            if (misc[kMiscLast] && !queue_mode) {
+                __threadfence();
+                merge_unit(u, L);
+            }
+            ptx::named_bar_sync(1, kCWarps * 32);
+        };
+
+        int stage = 0;
+        uint32_t phase = 0;
+        for (;;) {
+            ptx::mbar_wait(&full[stage], phase);
+            const uint32_t unit = meta[stage].unit;
+            if (unit == kEnd) break;
+            const uint32_t ntok = meta[stage].ntok;
+            if (unit != cur) {
+                if (cur != kEnd) flush(cur, cur_len);
+                cur = unit;
+                cur_len = meta[stage].pad;
+                run_tokens = 0;
+                load_q(unit);
+                reset_state();
+            }
+            run_tokens += ntok;
+            const int n = (int)ntok - tb;
+            if (n > 0) {
+                const uint32_t kbase = ptx::smem_u32(ring + stage * C::kStageBytes);
+                const uint32_t vbase = kbase + C::kTileBytes;
+                float sacc[2][2][4];
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int b = 0; b < 2; ++b)
+                        sacc[a][b][0] = sacc[a][b][1] = sacc[a][b][2] = sacc[a][b][3] = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < C::kNK; ++kk) {
+                    uint32_t b[4];
+                    ptx::ldsm_x4(b, kbase + swz<D>(k_tok, 2 * kk + k_csel));
+                    ptx::mma_bf16(sacc[0][kk & 1], qa[kk], b[0], b[1]);
+                    ptx::mma_bf16(sacc[1][kk & 1], qa[kk], b[2], b[3]);
+                }
+                float sc[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int nt = j >> 1, col = j & 1;
+                    const float v = (sacc[nt][0][col] + sacc[nt][1][col]) +
+                                    (sacc[nt][0][col + 2] + sacc[nt][1][col + 2]);
+                    const int tok = nt * 8 + 2 * qd + col;
+                    sc[j] = tok < n ? v : -INFINITY;
+                }
+                float bm = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+                bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+                bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+                const bool need = bm > m_used + 8.0f;
+                if (__any_sync(0xffffffffu, need)) {
+                    const float m_new = need ? bm : m_used;
+                    const float alpha = need ? ptx::ex2(m_used - m_new) : 1.0f;
+                    l_acc *= alpha;
+#pragma unroll
+                    for (int i = 0; i < 2 * C::kNK; ++i) {
+                        o[i][0] *= alpha; o[i][1] *= alpha; o[i][2] *= alpha; o[i][3] *= alpha;
+                    }
+                    m_used = m_new;
+                }
+                float pr[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) pr[j] = ptx::ex2(sc[j] - m_used);
+                l_acc += (pr[0] + pr[1]) + (pr[2] + pr[3]);
+                uint32_t pa[4];
+                pa[0] = ptx::pack_bf16(pr[0], pr[1]);
+                pa[1] = ptx::pack_bf16(pr[0] - ptx::bf16_lo_as_f32(pa[0]), pr[1] - ptx::bf16_hi_as_f32(pa[0]));
+                pa[2] = ptx::pack_bf16(pr[2], pr[3]);
+                pa[3] = ptx::pack_bf16(pr[2] - ptx::bf16_lo_as_f32(pa[2]), pr[3] - ptx::bf16_hi_as_f32(pa[2]));
+#pragma unroll
+                for (int nn = 0; nn < C::kNK; ++nn) {
+                    uint32_t b[4];
+                    ptx::ldsm_x4_t(b, vbase + swz<D>(v_tok, 2 * nn + v_csel));
+                    ptx::mma_bf16(o[2 * nn], pa, b[0], b[1]);
+                    ptx::mma_bf16(o[2 * nn + 1], pa, b[2], b[3]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+            if (++stage == C::kStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+        if (cur != kEnd) flush(cur, cur_len);
+    }
+    __syncthreads();
+    STAMP(9);
+    const unsigned long long t_stream_end = globaltimer();
+    if (t.trace && tid == 0) {
+        t.trace[bid * 4 + 1] = t_stream_end;
+    }
+
+    // ======================= phase M: distributed merge ========================
+    if (queue_mode && nact > 0) {
+        constexpr int kW = kThreads / 32;     // 5 warps share one task's partials
+        constexpr int kPW = 16;               // partials per warp held in registers
+        const uint32_t nd = D / 32;
+        const uint32_t ntasks = nact * r * nd;
+        const uint32_t PS = r * (D + 2);
+        float* red = sm_o;                    // [kW][32] acc, [kW] l, [kW] max
+        for (;;) {
+            if (tid == 0) misc[kMiscTask] = atomicAdd(&t.ss->merge_next, 1u);
+            __syncthreads();
+            const uint32_t task = misc[kMiscTask];
+            if (task >= ntasks) break;
+            const uint32_t a = task / (r * nd), rem = task % (r * nd);
+            const uint32_t h = rem / nd, d = (rem % nd) * 32 + lane;
+            const uint32_t u = act_unit[a];
+            const uint32_t L = p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
+            if (tid == 0) {
+                while (ld_volatile(&t.tokens_done[u]) < L) {
+                }
+                if (t.trace) t.trace[bid * 4 + 3] = globaltimer();
+                __threadfence();
+            }
+            __syncthreads();
+            const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
+            const float* base = t.partials + size_t(u) * t.S * PS;
+            float mv[kPW], av[kPW], lv[kPW];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < kPW; ++k) {
+                const uint32_t j = warp + k * kW;
+                mv[k] = j < n ? __ldcg(base + j * PS + h) : -INFINITY;
+                lv[k] = j < n ? __ldcg(base + j * PS + r + h) : 0.f;
+                av[k] = j < n ? __ldcg(base + j * PS + 2 * r + h * D + d) : 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < kPW; ++k) mx = fmaxf(mx, mv[k]);
+            for (uint32_t j = warp + kPW * kW; j < n; j += kW) mx = fmaxf(mx, __ldcg(base + j * PS + h));
+            if (lane == 0) red[kW * 33 + warp] = mx;
+            __syncthreads();
+            mx = red[kW * 33];
+#pragma unroll
+            for (int w = 1; w < kW; ++w) mx = fmaxf(mx, red[kW * 33 + w]);
+            float acc = 0.f, lsum = 0.f;
+#pragma unroll
+            for (int k = 0; k < kPW; ++k) {
+                const float w = mv[k] == -INFINITY ? 0.f : ptx::ex2(mv[k] - mx);
+                acc += av[k] * w;
+                lsum += lv[k] * w;
+            }
+            for (uint32_t j = warp + kPW * kW; j < n; j += kW) {
+                const float m = __ldcg(base + j * PS + h);
+                const float w = m == -INFINITY ? 0.f : ptx::ex2(m - mx);
+                acc += __ldcg(base + j * PS + 2 * r + h * D + d) * w;
+                lsum += __ldcg(base + j * PS + r + h) * w;
+            }
+            red[warp * 33 + lane] = acc;
+            if (lane == 0) red[warp * 33 + 32] = lsum;
+            __syncthreads();
+            if (warp == 0) {
+#pragma unroll
+                for (int w = 1; w < kW; ++w) {
+                    acc += red[w * 33 + lane];
+                    lsum += red[w * 33 + 32];
+                }
+                if (t.mode == 0) {
+                    t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
+                } else {
+                    float* P = t.out + size_t(u) * PS;
+                    if (d == 0) {
+                        P[h] = mx;
+                        P[r + h] = lsum;
+                    }
+                    P[2 * r + h * D + d] = acc;
+                }
+                if (h == 0 && d == 0) t.tokens[u] = L;
+            }
+            __syncthreads();
+        }
+    }
+
+    // ======================= exit: last CTA restores the counters ================
+    __syncthreads();
+    STAMP(10);
+    if (t.trace && tid == 0) t.trace[bid * 4 + 2] = globaltimer();
+    if (tid == 0) {
+        __threadfence();
+        misc[kMiscLast] = (atomicAdd(&t.ss->exit_count, 1u) == G - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    STAMP(11);
+    if (misc[kMiscLast]) {
+        __threadfence();
+        for (uint32_t a = tid; a < nact; a += kThreads) {
+            const uint32_t u = act_unit[a];
+            t.cursor[a] = 0;
+            t.slot_count[u] = 0;
+            t.tokens_done[u] = 0;
+        }
+        if (tid == 0) {
+            clk[2] = t_stream_end;
+            clk[3] = globaltimer();
+            *t.status = t.ss->error;
+            t.ss->error = 0;
+            t.ss->flat_counter = 0;
+            t.ss->merge_next = 0;
+            t.ss->exit_count = 0;
+        }
+    }
+}
+
+}  // namespace dev
+}  // namespace sinkr

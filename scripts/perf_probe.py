@@ -25,6 +25,13 @@ for tau, name in ((2.0, "dense"), (0.5, "routed"), (-2.0, "allsink")):
         dec.append((dms, sms))
     dec = np.array(dec)
     info = P.fetch_step_info(cache)
+    import ctypes as C
+    from paper_2604_16883_b200 import _abi
+    st = (C.c_ulonglong * 12)()
+    if hasattr(_abi.lib(), "sinkr_debug_stamps"):
+        _abi.lib().sinkr_debug_stamps(cache.handle, st, 12)
+        d = [int(st[i + 1]) - int(st[i]) for i in range(11)]
+        print("  stamp deltas (cycles):", d)
     hq = spec.queries()[0]
     res = P.routed_decode_step(hq, 0, cache, cfg)
     c = res.counters
