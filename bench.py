@@ -237,25 +237,29 @@ def time_async(P, torch, cache, cfg, dq, dout, steps):
 
 
 def decode_kernel_ms(P, cache, cfg, dq, dout, steps):
-    """Average decode-kernel launch duration (CUDA events around the kernel on
-    the engine stream; eager launches, one step at a time)."""
+    """Average launch duration of the step's attention kernel (CUDA events
+    around the kernel on the engine stream, one launch at a time) and the
+    device-side phase split of the last launch (routing / streaming / merge,
+    %globaltimer stamps written by the kernel)."""
     P.set_timing(cache, True)
     ds = []
     for _ in range(steps):
         P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
-        _, dms, _ = P.last_step_stats(cache)
+        n, dms, _ = P.last_step_stats(cache)
         ds.append(dms)
+    c = P.fetch_step_info(cache).counters
     P.set_timing(cache, False)
-    return float(np.mean(ds)), float(np.median(ds))
-
-
-def l2_flush(torch, buf):
-    buf.zero_()
+    phases = {"routing_us": round(c.routing_seconds * 1e6, 2),
+              "stream_us": round(c.attention_seconds * 1e6, 2),
+              "merge_us": round(c.merge_seconds * 1e6, 2)}
+    return float(np.mean(ds)), float(np.median(ds)), phases, n
 
 
 def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
-    """Context x routed-fraction sweep (BASELINE.json configs[1]); per-step
-    CUDA events with an L2 flush (256 MiB write) between steps."""
+    """Context x routed-fraction sweep (BASELINE.json configs[1]).  Each timed
+    step follows an L2 flush (a 256 MiB write) on the same stream; CUDA events
+    bracket the step alone, and everything is enqueued ahead so no host gap is
+    timed."""
     out = []
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for L in (65536, 131072, 524288):
@@ -279,18 +283,20 @@ def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
                     continue
                 for _ in range(3):
                     P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
-                ts = []
-                for _ in range(10):
-                    l2_flush(torch, flush)
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    torch.cuda.synchronize()
-                    e0.record(stream)
-                    P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
-                    e1.record(stream)
-                    e1.synchronize()
-                    ts.append(e0.elapsed_time(e1) * 1e3)
-                res[name] = statistics.median(ts)
+                torch.cuda.synchronize()
+                evs = []
+                with torch.cuda.stream(stream):
+                    for _ in range(10):
+                        flush.sum()  # read-only flush: evicts L2 without dirty write-backs
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e0.record(stream)
+                        P.routed_decode_async(dq.data_ptr(), 0, cache, cfg,
+                                              d_outputs=dout.data_ptr())
+                        e1.record(stream)
+                        evs.append((e0, e1))
+                torch.cuda.synchronize()
+                res[name] = statistics.median(a.elapsed_time(b) * 1e3 for a, b in evs)
             info = P.fetch_step_info(cache)
             n_act = info.counters.groups_active
             if k == 0:
@@ -362,22 +368,27 @@ def run_ours(args, world, rank, local_rank):
     kv_routed = n_act * 2 * L * D * 2
     kv_dense = info_d.counters.groups_active * 2 * L * D * 2
 
-    # ---- decode kernel launch duration (roofline numerator)
-    dec_mean_r, dec_med_r = decode_kernel_ms(P, cache, routed_cfg, dq, dout, args.steps)
-    dec_mean_d, dec_med_d = decode_kernel_ms(P, cache, dense_cfg, dq, dout, args.steps)
+    # ---- step-kernel launch duration (roofline numerator)
+    dec_mean_r, dec_med_r, phases_r, nlaunch = decode_kernel_ms(P, cache, routed_cfg, dq, dout,
+                                                                 args.steps)
+    dec_mean_d, dec_med_d, phases_d, _ = decode_kernel_ms(P, cache, dense_cfg, dq, dout,
+                                                         args.steps)
     q_bytes = 32 * D * 4
     alg_r = kv_routed + n_act * 4 * D * 4
     alg_d = kv_dense + q_bytes
     achieved = alg_r / (dec_mean_r * 1e-3) / 1e9
     achieved_d = alg_d / (dec_mean_d * 1e-3) / 1e9
 
-    # ---- e2e through the public C-ABI call, host buffers
-    for _ in range(3):
-        P.routed_decode_step(q_host, 0, cache, routed_cfg)
+    # ---- e2e through the public C-ABI call (sinkr_routed_decode_batch via
+    # StepRunner), host queries in, host outputs + routing record out
+    runner = P.StepRunner(cache, routed_cfg)
+    for _ in range(5):
+        runner(q_host)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        res_host = P.routed_decode_step(q_host, 0, cache, routed_cfg)
+        runner(q_host)
     e2e_us = (time.perf_counter() - t0) / args.steps * 1e6
+    res_host = runner.result()
     h2d, d2h = cache.step_io_bytes()
 
     traffic = None
@@ -418,15 +429,18 @@ def run_ours(args, world, rank, local_rank):
         "kv_gbs_dense_step": round(kv_dense / (dense_ms * 1e-3) / 1e9, 1),
         "dense_decode_kernel": {"us": round(dec_mean_d * 1e3, 2),
                                 "achieved_gbs": round(achieved_d, 1),
-                                "frac": round(achieved_d / peak, 4)},
+                                "frac": round(achieved_d / peak, 4), "phases": phases_d},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "decode_kernel<128> (routed)",
+                     "kernel": ("step_kernel<128> (fused probe + Split-K decode + merge), routed"
+                                if nlaunch == 1 else "decode_kernel<128> (routed)"),
+                     "phases": phases_r,
+                     "stream_phase_gbs": round(kv_routed / max(phases_r["stream_us"], 1e-9) / 1e3, 1),
                      "kernel_us": round(dec_mean_r * 1e3, 2),
                      "alg_bytes_per_launch": alg_r, "peak_source": peak_src},
         "e2e": {"value": round(e2e_us, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": nlaunch * args.steps,
         "clocks": clk.summary(),
     }
 

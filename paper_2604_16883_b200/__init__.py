@@ -15,6 +15,7 @@ from .router import (  # noqa: F401
     LoadCounters,
     RouteDecision,
     RoutingConfig,
+    StepRunner,
     ThresholdProfile,
     auto_num_splits,
     decode_rank_partial_async,

@@ -150,6 +150,7 @@ struct sinkr_engine {
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
 
     CUtensorMap tmk{}, tmv{};
+    CUtensorMap* d_tmap = nullptr;  // device copies of tmk, tmv (fused kernel)
     cudaEvent_t ev[4] = {};
     cudaEvent_t ev_in = nullptr;
     bool timing = true;
@@ -207,6 +208,8 @@ struct sinkr_engine {
     }
     dev::StepTables step_tables(const float* q, float* out, int mode) const {
         dev::StepTables t{};
+        t.tmk = d_tmap;
+        t.tmv = d_tmap + 1;
         t.q = q;
         t.anchors = d_anchor;
         t.anchor_norm = d_anchor_norm;
@@ -318,7 +321,7 @@ void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, dev::step_kernel<D>, e->tmk, e->tmv, st, e->pp));
+    CK(cudaLaunchKernelEx(&cfg, dev::step_kernel<D>, st, e->pp));
 }
 
 void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
@@ -413,7 +416,7 @@ void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
     if (ge.probe && std::memcmp(&ge.pp, &e->pp, sizeof(e->pp)) != 0) {
         ge.pp = e->pp;
         void* args3[2] = {&ge.probe_t, &ge.pp};
-        void* args1[4] = {&e->tmk, &e->tmv, &ge.step_t, &ge.pp};
+        void* args1[2] = {&ge.step_t, &ge.pp};
         cudaKernelNodeParams kp = ge.probe_kp;
         kp.kernelParams = ge.fused ? args1 : args3;
         kp.extra = nullptr;
@@ -656,8 +659,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMalloc(&e->d_tokens_done, e->U * 4));
             CK(cudaMemsetAsync(e->d_tokens_done, 0, e->U * 4, e->stream));
             if (const char* tr = std::getenv("SINKR_TRACE"); tr && tr[0] == '1') {
-                CK(cudaMalloc(&e->d_trace, e->grid * 4 * 8));
-                CK(cudaMemsetAsync(e->d_trace, 0, e->grid * 4 * 8, e->stream));
+                CK(cudaMalloc(&e->d_trace, e->grid * 8 * 8));
+                CK(cudaMemsetAsync(e->d_trace, 0, e->grid * 8 * 8, e->stream));
             }
             {
                 const char* f = std::getenv("SINKR_FUSED");
@@ -679,6 +682,9 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
 
             make_tmap(&e->tmk, e->d_k, rows, e->D);
             make_tmap(&e->tmv, e->d_v, rows, e->D);
+            CK(cudaMalloc(&e->d_tmap, 2 * sizeof(CUtensorMap)));
+            CUtensorMap both[2] = {e->tmk, e->tmv};
+            CK(cudaMemcpy(e->d_tmap, both, sizeof(both), cudaMemcpyHostToDevice));
             CK(cudaFuncSetAttribute(dev::decode_kernel<32>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<32>()));
             CK(cudaFuncSetAttribute(dev::decode_kernel<64>,
@@ -739,6 +745,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_res);
     cudaFree(e->d_ws);
     cudaFree(e->d_ss);
+    cudaFree(e->d_tmap);
     cudaFree(e->d_cursor);
     cudaFree(e->d_tokens_done);
     cudaFree(e->d_head_degen);
@@ -1100,8 +1107,8 @@ extern "C" sinkr_status sinkr_debug_trace(sinkr_engine* e, unsigned long long* o
     return guard([&] {
         if (!e->d_trace) fail(SINKR_INVALID_ARGUMENT, "tracing disabled (SINKR_TRACE=1)");
         CK(cudaStreamSynchronize(e->stream));
-        CK(cudaMemcpy(out, e->d_trace, e->grid * 4 * 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemset(e->d_trace, 0, e->grid * 4 * 8));
+        CK(cudaMemcpy(out, e->d_trace, e->grid * 8 * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemset(e->d_trace, 0, e->grid * 8 * 8));
     });
 }
 

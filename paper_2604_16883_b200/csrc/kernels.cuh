@@ -50,7 +50,7 @@ struct StepHdr {
 // Per-step scalars handed to the probe by value (kernel parameters live in the
 // constant bank: no global-memory round trip before routing can start).  The
 // engine patches them into the captured graph node each step.
-constexpr int kParamSeqs = 64;
+constexpr int kParamSeqs = 8;  // keeps the launch parameter block small (launch latency)
 struct ProbeParams {
     uint32_t layer;
     uint32_t flags;

@@ -39,6 +39,11 @@ struct StepState {
 };
 
 struct StepTables {
+    // TMA descriptors live in global memory (written once at engine creation):
+    // keeping 256 B of descriptors out of the parameter block halves the
+    // launch latency of this kernel (scripts/micro/launch_cost2.cu)
+    const CUtensorMap* tmk;
+    const CUtensorMap* tmv;
     const float* q;                // [B][Hq][D]
     const float* anchors;          // [layers][B][Hkv][D]
     const float* anchor_norm;      // [layers][B][Hkv]
@@ -123,8 +128,7 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
-    step_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                StepTables t, const ProbeParams p) {
+    step_kernel(StepTables t, const ProbeParams p) {
     using C = Cfg<D>;
     using SC = StepCfg<D>;
     using Scan = cub::BlockScan<uint32_t, kThreads>;
@@ -157,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool lead = bid == 0;
     unsigned long long* clk = reinterpret_cast<unsigned long long*>(t.status + 4);
     if (lead && tid == 0) clk[0] = globaltimer();
+    if (t.trace && tid == 0) t.trace[bid * 8 + 4] = globaltimer();
     unsigned long long* dbg = clk + 4;  // debug cycle stamps (lead CTA, thread 0)
 #define STAMP(i) do { if (lead && tid == 0) dbg[i] = clock64(); } while (0)
     STAMP(0);
@@ -167,8 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&empty[s], kCWarps);
         }
         ptx::fence_mbar_init();
-        ptx::tma_prefetch_desc(&tmk);
-        ptx::tma_prefetch_desc(&tmv);
+        ptx::tma_prefetch_desc(t.tmk);
+        ptx::tma_prefetch_desc(t.tmv);
     }
 
     STAMP(1);
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
-    if (t.trace && tid == 0) t.trace[bid * 4 + 0] = globaltimer();
+    if (t.trace && tid == 0) t.trace[bid * 8 + 0] = globaltimer();
     const bool queue_mode = misc[kMiscQueue] != 0;
     if (lead && tid == 0) clk[1] = globaltimer();
 
@@ -389,9 +394,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* vd = kd + C::kTileBytes;
 #pragma unroll
                     for (int h = 0; h < C::kHalves; ++h) {
-                        ptx::tma_load_2d(kd + h * kStageTok * 128, &tmk, h * C::kBoxDim,
+                        ptx::tma_load_2d(kd + h * kStageTok * 128, t.tmk, h * C::kBoxDim,
                                          row0 + (int32_t)tk, &full[stage], pol);
-                        ptx::tma_load_2d(vd + h * kStageTok * 128, &tmv, h * C::kBoxDim,
+                        ptx::tma_load_2d(vd + h * kStageTok * 128, t.tmv, h * C::kBoxDim,
                                          row0 + (int32_t)tk, &full[stage], pol);
                     }
                     if (++stage == C::kStages) {
@@ -677,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     STAMP(9);
     const unsigned long long t_stream_end = globaltimer();
     if (t.trace && tid == 0) {
-        t.trace[bid * 4 + 1] = t_stream_end;
+        t.trace[bid * 8 + 1] = t_stream_end;
     }
 
     // ======================= phase M: distributed merge ========================
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (tid == 0) {
                 while (ld_volatile(&t.tokens_done[u]) < L) {
                 }
-                if (t.trace) t.trace[bid * 4 + 3] = globaltimer();
+                if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
                 __threadfence();
             }
             __syncthreads();
@@ -764,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= exit: last CTA restores the counters ================
     __syncthreads();
     STAMP(10);
-    if (t.trace && tid == 0) t.trace[bid * 4 + 2] = globaltimer();
+    if (t.trace && tid == 0) t.trace[bid * 8 + 2] = globaltimer();
     if (tid == 0) {
         __threadfence();
         misc[kMiscLast] = (atomicAdd(&t.ss->exit_count, 1u) == G - 1) ? 1u : 0u;
@@ -779,6 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             t.slot_count[u] = 0;
             t.tokens_done[u] = 0;
         }
+        if (tid == 0 && t.trace) t.trace[bid * 8 + 5] = globaltimer();
         if (tid == 0) {
             clk[2] = t_stream_end;
             clk[3] = globaltimer();

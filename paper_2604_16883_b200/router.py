@@ -415,3 +415,44 @@ def merge_rank_partials_async(cache: KvCache, d_gathered: int, num_ranks: int,
 
 
 KvCache.rank_partial_floats = rank_partial_floats
+
+
+class StepRunner:
+    """Lean repeated-call form of routed_decode_step for serving loops: all
+    host buffers and C structs are allocated once, each call is one C-ABI call
+    (sinkr_routed_decode_batch: H2D queries -> graph -> D2H results, blocking).
+    Returns the reused output buffer; `result()` builds the full
+    LayerStepResult of the last call on demand."""
+
+    def __init__(self, cache: KvCache, config: RoutingConfig, options: Optional[EngineOptions] = None,
+                 layer: int = 0):
+        self.cache = cache
+        self.layer = layer
+        self.out, self.groups, self.hs, self.ctr = _step_buffers(cache)
+        self._cfg, self._keep = config._c()
+        self._opt = (options or EngineOptions())._c()
+        L = lib()
+        self._fn = L.sinkr_routed_decode_batch
+        self._fn.restype = C.c_int
+        self._fn.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        self._args = (cache.handle, None, layer, C.addressof(self._cfg), C.addressof(self._opt),
+                      self.out.ctypes.data, C.addressof(self.groups), self.hs.ctypes.data,
+                      C.addressof(self.ctr))
+        self._qsize = self.out.size
+
+    def __call__(self, queries: np.ndarray) -> np.ndarray:
+        if queries.dtype != np.float32 or not queries.flags.c_contiguous or \
+                queries.size != self._qsize:
+            queries = np.ascontiguousarray(queries, dtype=np.float32)
+            if queries.size != self._qsize:
+                raise ValueError("queries span must be H_q x D for one layer")
+        h, _, layer, cfg, opt, out, groups, hs, ctr = self._args
+        rc = self._fn(h, queries.ctypes.data, layer, cfg, opt, out, groups, hs, ctr)
+        if rc:
+            check(rc)
+        return self.out
+
+    def result(self) -> LayerStepResult:
+        return _to_result(self.cache, self.out.copy(), self.groups, self.hs, self.ctr,
+                          batched=self.cache.B > 1)

@@ -17,15 +17,18 @@ for tau in (2.0, 0.5):
     torch.cuda.synchronize()
     G = cache.decode_grid()
     import ctypes as CC
-    _abi.lib().sinkr_debug_trace(cache.handle, (CC.c_ulonglong * (G * 4))())
+    _abi.lib().sinkr_debug_trace(cache.handle, (CC.c_ulonglong * (G * 8))())
     P.routed_decode_async(q.data_ptr(), 0, cache, cfg, d_outputs=out.data_ptr())
     torch.cuda.synchronize()
-    buf = (C.c_ulonglong * (G * 4))()
+    buf = (C.c_ulonglong * (G * 8))()
     _abi.lib().sinkr_debug_trace(cache.handle, buf)
-    a = np.array(buf, dtype=np.float64).reshape(G, 4)
+    a = np.array(buf, dtype=np.float64).reshape(G, 8)
     t0 = a[:, 0].min()
     rs, se, me = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3
-    print(f"tau={tau}: routing-end us  min {rs.min():.1f} max {rs.max():.1f}")
+    st = (a[:, 4] - t0) / 1e3
+    print(f"tau={tau}: start us min {st.min():.1f} max {st.max():.1f}; routing-end us  min {rs.min():.1f} max {rs.max():.1f}")
+    ex = a[:, 5][a[:, 5] > 0]
+    if len(ex): print(f"   last-CTA reset done us {(ex.max() - t0) / 1e3:.1f}")
     print(f"   stream-end us  min {se.min():.1f} p10 {np.percentile(se,10):.1f} med {np.median(se):.1f} p90 {np.percentile(se,90):.1f} max {se.max():.1f}")
     print(f"   merge-end  us  min {me.min():.1f} med {np.median(me):.1f} max {me.max():.1f}")
     sp = a[:, 3]
