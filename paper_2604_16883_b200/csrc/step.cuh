@@ -25,7 +25,7 @@
 namespace sinkr {
 namespace dev {
 
-constexpr int kMaxUnits = 1536;      // B * H_kv per step
+constexpr int kMaxUnits = 1280;      // B * H_kv per step (LLaVA-13B B=32 x 40)
 constexpr int kMaxStepHeads = 4096;  // B * H_q per step
 constexpr int kRouteTile = 64;       // heads per routing tile
 constexpr int kRouteSub = 32;        // heads per load batch
@@ -76,14 +76,16 @@ struct StepCfg {
     static constexpr int kOffMisc = kOffML + kCWarps * kMaxR * 2 * 4;
     static constexpr int kOffAct = kOffMisc + 64;
     static constexpr int kOffPrefix = kOffAct + kMaxUnits * 2;
-    static constexpr int kBytes = kOffPrefix + (kMaxUnits + 1) * 4;
+    static constexpr int kOffLen = kOffPrefix + (kMaxUnits + 1) * 4;
+    static constexpr int kBytes = kOffLen + kMaxUnits * 4;
     static constexpr int kSmemBytes = 1024 + kBytes;
     // routing overlay (inside the ring, before streaming starts)
     static constexpr int kDP = D + 1;
     static constexpr int kOvProd = 0;  // q, k0 [2][kRouteTile][D+1] f32 + chains [2][kRouteTile] f64
     static constexpr int kOvScore = (2 * kRouteTile * kDP * 8 + 2 * kRouteTile * 8 + 15) / 16 * 16;
     static constexpr int kOvDegen = kOvScore + kMaxStepHeads * 8;         // [kMaxStepHeads] u8
-    static_assert(kOvDegen + kMaxStepHeads <= kRing, "routing overlay exceeds the ring");
+    static constexpr int kOvSeq = kOvDegen + kMaxStepHeads;             // tau f64 [B], len u32 [B]
+    static_assert(kOvSeq + 12 * kMaxUnits <= kRing, "routing overlay exceeds the ring");
     static_assert(kSmemBytes <= 232448, "step kernel shared memory");
 };
 
@@ -139,9 +141,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     } tmp;
     __shared__ unsigned long long s_tok_total;
 
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    // 1024-B alignment for the 128B-swizzled TMA tiles, by offsetting the
+    // shared array itself so the compiler keeps shared-space (LDS/STS) access
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* ring = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + SC::kOffBars);
     uint64_t* empty = full + C::kStages;
@@ -151,8 +154,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + SC::kOffMisc);
     uint16_t* act_unit = reinterpret_cast<uint16_t*>(smem + SC::kOffAct);
     uint32_t* act_prefix = reinterpret_cast<uint32_t*>(smem + SC::kOffPrefix);
+    uint32_t* act_len = reinterpret_cast<uint32_t*>(smem + SC::kOffLen);  // rows per Active entry
     double* s_score = reinterpret_cast<double*>(ring + SC::kOvScore);
     uint8_t* s_degen = ring + SC::kOvDegen;
+    double* s_tau = reinterpret_cast<double*>(ring + SC::kOvSeq);                 // [B]
+    uint32_t* s_len = reinterpret_cast<uint32_t*>(ring + SC::kOvSeq + 8 * kMaxUnits);  // [B]
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t G = gridDim.x, bid = blockIdx.x;
@@ -177,6 +183,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     STAMP(1);
+    // per-sequence tau / length into smem once (no dynamic indexing of the
+    // parameter block in the loops below)
+    if (p.inline_seqs) {
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < kParamSeqs; ++k) {  // compile-time indices: plain LDC
+                s_tau[k] = p.tau[k];
+                s_len[k] = p.len[k];
+            }
+        }
+    } else {
+        for (uint32_t sq = tid; sq < t.B; sq += kThreads) {
+            s_tau[sq] = __ldg(&t.tau_g[sq]);
+            s_len[sq] = __ldg(&t.len_g[sq]);
+        }
+    }
     // ======================= phase R: routing ================================
     // proxy_score (router.cpp:36-48): head i belongs to unit i / r.  q and k0
     // rows are staged in smem as f32 (coalesced loads, all issued up front);
@@ -272,14 +294,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             degen |= s_degen[u * r + i];
         }
         const double S = __ddiv_rn(sum, (double)r);
-        const double tau = p.inline_seqs ? p.tau[seq] : __ldg(&t.tau_g[seq]);
+        const double tau = s_tau[seq];
         const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
         bool sink = over && !(flags & kLayerExcluded);
         if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
         const bool active = (flags & kObserveOnly) || !sink;
         if (active) {
             ++my_active;
-            my_tok += p.inline_seqs ? p.len[seq] : __ldg(&t.len_g[seq]);
+            my_tok += s_len[seq];
             my_bits |= 1ull << (u - u0);
         }
         if (lead) {
@@ -326,9 +348,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t a = a_off;
         for (uint32_t u = u0; u < u1; ++u) {
             if (!((my_bits >> (u - u0)) & 1ull)) continue;
+            const uint32_t L = s_len[u / t.Hkv];
+            act_len[a] = L;
             act_unit[a++] = (uint16_t)u;
-            const uint32_t L = p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
-            my_chunks += plan_nch(L, cp);
+            if (flat) my_chunks += plan_nch(L, cp);
         }
     }
     if (flat) {
@@ -338,9 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t a = a_off;
         for (uint32_t u = u0; u < u1; ++u) {
             if (!((my_bits >> (u - u0)) & 1ull)) continue;
-            act_prefix[a++] = c_off;
-            const uint32_t L = p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
-            c_off += plan_nch(L, cp);
+            act_prefix[a] = c_off;
+            c_off += plan_nch(act_len[a++], cp);
         }
         if (tid == 0) act_prefix[nact] = c_tot;
     }
@@ -405,9 +427,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             };
-            auto unit_len = [&](uint32_t u) {
-                return p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
-            };
             if (nact > 0 && !flat) {
                 // Unit-affine guided self-scheduling over TOKEN cursors.  CTA c
                 // starts on Active entry c mod nact with the static range
@@ -418,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // An exhausted unit hands the CTA on to the next entry.
                 const uint32_t cpu = (G + nact - 1) / nact;  // CTAs per unit
                 uint32_t a = bid % nact, visited = 1;
-                uint32_t u = act_unit[a], L = unit_len(u);
+                uint32_t u = act_unit[a], L = act_len[a];
                 uint32_t first = ((G - a + nact - 1) / nact) * Ck;
                 uint32_t t0 = (bid / nact) * Ck, t1 = min(t0 + Ck, L);
                 auto guided = [&](uint32_t hint) {
@@ -433,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ++visited;
                         a = (a + 1 == nact) ? 0 : a + 1;
                         u = act_unit[a];
-                        L = unit_len(u);
+                        L = act_len[a];
                         first = ((G - a + nact - 1) / nact) * Ck;
                         const uint32_t sz = guided(first);
                         t0 = first + atomicAdd(&t.cursor[a], sz);
@@ -460,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (act_prefix[mid] <= chunk) lo = mid; else hi = mid;
                     }
                     a = lo;
-                    const uint32_t u = act_unit[a], L = unit_len(u);
+                    const uint32_t u = act_unit[a], L = act_len[a];
                     const uint32_t k = chunk - act_prefix[a];
                     uint32_t t0, t1;
                     plan_range(L, k, cp, t0, t1);
@@ -601,16 +620,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (;;) {
             ptx::mbar_wait(&full[stage], phase);
             const uint32_t unit = meta[stage].unit;
-            if (unit == kEnd) break;
-            const uint32_t ntok = meta[stage].ntok;
-            if (unit != cur) {
-                if (cur != kEnd) flush(cur, cur_len);
+            if (unit != cur || unit == kEnd) {  // kEnd == cur when a CTA had no work
+                if (cur != kEnd) flush(cur, cur_len);  // the only flush site
+                if (unit == kEnd) break;
                 cur = unit;
                 cur_len = meta[stage].pad;
                 run_tokens = 0;
                 load_q(unit);
                 reset_state();
             }
+            const uint32_t ntok = meta[stage].ntok;
             run_tokens += ntok;
             const int n = (int)ntok - tb;
             if (n > 0) {
@@ -676,7 +695,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 phase ^= 1u;
             }
         }
-        if (cur != kEnd) flush(cur, cur_len);
     }
     __syncthreads();
     STAMP(9);
@@ -701,9 +719,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t a = task / (r * nd), rem = task % (r * nd);
             const uint32_t h = rem / nd, d = (rem % nd) * 32 + lane;
             const uint32_t u = act_unit[a];
-            const uint32_t L = p.inline_seqs ? p.len[u / t.Hkv] : __ldg(&t.len_g[u / t.Hkv]);
+            const uint32_t L = act_len[a];
             if (tid == 0) {
+                // watchdog: a unit that never completes (a bug) must not hang
+                // the GPU; after 2 s report an error and give up the task
+                const unsigned long long t_spin = globaltimer();
                 while (ld_volatile(&t.tokens_done[u]) < L) {
+                    if (globaltimer() - t_spin > 2000000000ull) {
+                        atomicExch(&t.ss->error, 2u);
+                        break;
+                    }
                 }
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
                 __threadfence();

@@ -50,6 +50,7 @@ int main() {
     REQUIRE(cache.token_count() == L);
     REQUIRE(std::fabs(cache.anchor(0, 0).k0_norm) > 0.0f);
 
+    std::fprintf(stderr, "step: dense layer 1\n");
     // routing disabled: every group attends the whole cache
     auto cfg = sc::RoutingConfig::from_profile(sc::ThresholdProfile::constant(2.0));
     auto r = sc::routed_decode_step(q, 1, cache, cfg);
@@ -61,10 +62,12 @@ int main() {
     sc::RoutingConfig skip;
     skip.profile = sc::ThresholdProfile::constant(-2.0);
     skip.excluded_layers = {0};  // layer 1 routable, layer 0 excluded
+    std::fprintf(stderr, "step: full skip layer 1\n");
     auto s = sc::routed_decode_step(q, 1, cache, skip);
     REQUIRE(s.counters.groups_skipped == hkv && s.counters.kv_floats_loaded == 0);
     for (float x : s.outputs) REQUIRE(x == 0.0f && !std::signbit(x));
     // ... but never on an excluded layer (router.hpp:19)
+    std::fprintf(stderr, "step: excluded layer 0\n");
     auto e = sc::routed_decode_step(q, 0, cache, skip);
     REQUIRE(e.counters.groups_active == hkv);
 
