@@ -154,6 +154,7 @@ struct sinkr_engine {
     cudaEvent_t ev[4] = {};
     cudaEvent_t ev_in = nullptr;
     bool timing = true;
+    bool step_events = false;  // events around graph replays (last_step_stats step_ms)
     bool params_valid = false;
     std::vector<uint8_t> last_params;
     struct GraphEntry {
@@ -422,9 +423,11 @@ void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
         kp.extra = nullptr;
         CK(cudaGraphExecKernelNodeSetParams(ge.exec, ge.probe, &kp));
     }
-    CK(cudaEventRecord(e->ev[0], e->stream));
+    // no event records around replays unless asked: each is an extra stream
+    // operation between back-to-back steps
+    if (e->step_events) CK(cudaEventRecord(e->ev[0], e->stream));
     CK(cudaGraphLaunch(ge.exec, e->stream));
-    CK(cudaEventRecord(e->ev[3], e->stream));
+    if (e->step_events) CK(cudaEventRecord(e->ev[3], e->stream));
 }
 
 size_t token_count(const sinkr_engine* e, size_t seq) {
@@ -1090,7 +1093,11 @@ sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches, f
             if (e->timing)
                 CK(cudaEventElapsedTime(decode_ms, e->ev[e->fused ? 0 : 1], e->ev[e->fused ? 3 : 2]));
         }
-        if (step_ms) CK(cudaEventElapsedTime(step_ms, e->ev[0], e->ev[3]));
+        if (step_ms) {
+            *step_ms = 0.f;
+            if (e->timing || e->step_events)
+                CK(cudaEventElapsedTime(step_ms, e->ev[0], e->ev[3]));
+        }
     });
 }
 

@@ -212,40 +212,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         double* s_chain = sk + kRouteTile * SC::kDP;  // [2][kRouteTile]
         for (uint32_t h_base = 0; h_base < NH; h_base += kRouteTile) {
             const uint32_t nh = min((uint32_t)kRouteTile, NH - h_base);
-            // warp w loads heads w, w+5, ...; lane l loads dims l, l+32, ... (coalesced;
-            // one integer division per head)
+            // warp w loads heads w, w+5, ...; lane l loads kV = D/32 consecutive
+            // floats of the row with one vector load.  The products go to smem
+            // rows of odd stride (D+1 doubles, conflict-free for the chains)
+            // with a lane-rotated element order, so the stores are conflict-free
+            // as well.
             constexpr int kW = kThreads / 32;
             constexpr int kHPW = (kRouteTile + kW - 1) / kW;
-            constexpr int kJL = D / 32;
-            float qv[kHPW][kJL], kv[kHPW][kJL];
+            constexpr int kV = D / 32;
+            float qv[kHPW][kV], kv[kHPW][kV];
+            const uint64_t keep = ptx::policy_evict_last();
 #pragma unroll
             for (int a = 0; a < kHPW; ++a) {
                 const uint32_t hl = warp + a * kW;
                 const bool ok = hl < nh;
                 const uint32_t i = h_base + (ok ? hl : 0);
-                const float* qrow = t.q + size_t(i) * D;
-                const float* krow = t.anchors + (size_t(layer) * U + i / r) * D;
-#pragma unroll
-                for (int b = 0; b < kJL; ++b) {
-                    qv[a][b] = ok ? __ldg(qrow + lane + 32 * b) : 0.f;
-                    kv[a][b] = ok ? __ldg(krow + lane + 32 * b) : 0.f;
+                const float* qrow = t.q + size_t(i) * D + kV * lane;
+                const float* krow = t.anchors + (size_t(layer) * U + i / r) * D + kV * lane;
+                if constexpr (kV == 4) {
+                    float4 x = make_float4(0.f, 0.f, 0.f, 0.f), y = x;
+                    if (ok) {
+                        x = ptx::ldg_last4(qrow, keep);
+                        y = ptx::ldg_last4(krow, keep);
+                    }
+                    qv[a][0] = x.x; qv[a][1] = x.y; qv[a][2] = x.z; qv[a][3] = x.w;
+                    kv[a][0] = y.x; kv[a][1] = y.y; kv[a][2] = y.z; kv[a][3] = y.w;
+                } else if constexpr (kV == 2) {
+                    float2 x = make_float2(0.f, 0.f), y = x;
+                    if (ok) {
+                        x = ptx::ldg_last2(qrow, keep);
+                        y = ptx::ldg_last2(krow, keep);
+                    }
+                    qv[a][0] = x.x; qv[a][1] = x.y;
+                    kv[a][0] = y.x; kv[a][1] = y.y;
+                } else {
+                    qv[a][0] = ok ? ptx::ldg_last(qrow, keep) : 0.f;
+                    kv[a][0] = ok ? ptx::ldg_last(krow, keep) : 0.f;
                 }
             }
             double kn = 1.0;
-            if (tid < nh) kn = (double)__ldg(&t.anchor_norm[size_t(layer) * U + (h_base + tid) / r]);
+            if (tid < nh)
+                kn = (double)ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + (h_base + tid) / r], keep);
             // exact fp64 products (f32 x f32 fits in 53 bits), off the chain
 #pragma unroll
             for (int a = 0; a < kHPW; ++a) {
                 const uint32_t hl = warp + a * kW;
                 if (hl < nh) {
 #pragma unroll
-                    for (int b = 0; b < kJL; ++b) {
-                        const double qd = (double)qv[a][b];
-                        sq[hl * SC::kDP + lane + 32 * b] = __dmul_rn(qd, (double)kv[a][b]);
-                        sk[hl * SC::kDP + lane + 32 * b] = __dmul_rn(qd, qd);
+                    for (int e = 0; e < kV; ++e) {
+                        const uint32_t idx = (e + lane) % kV;
+                        float qf = qv[a][0], kf = kv[a][0];
+#pragma unroll
+                        for (int c = 1; c < kV; ++c)
+                            if (idx == (uint32_t)c) {
+                                qf = qv[a][c];
+                                kf = kv[a][c];
+                            }
+                        const double qd = (double)qf;
+                        sq[hl * SC::kDP + kV * lane + idx] = __dmul_rn(qd, (double)kf);
+                        sk[hl * SC::kDP + kV * lane + idx] = __dmul_rn(qd, qd);
                     }
                 }
             }
+            if (h_base == 0) STAMP(12);
             __syncthreads();
             STAMP(2);
             if (tid < 2 * kRouteTile && (tid % kRouteTile) < nh) {
@@ -293,7 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             sum = __dadd_rn(sum, s_score[u * r + i]);
             degen |= s_degen[u * r + i];
         }
-        const double S = __ddiv_rn(sum, (double)r);
+        // sum / r (router.cpp:56); for power-of-two r the product with 1/r is
+        // the same correctly rounded value and avoids the division sequence
+        const double S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
         const double tau = s_tau[seq];
         const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
         bool sink = over && !(flags & kLayerExcluded);

@@ -27,11 +27,11 @@ for tau, name in ((2.0, "dense"), (0.5, "routed"), (-2.0, "allsink")):
     info = P.fetch_step_info(cache)
     import ctypes as C
     from paper_2604_16883_b200 import _abi
-    st = (C.c_ulonglong * 12)()
+    st = (C.c_ulonglong * 13)()
     if hasattr(_abi.lib(), "sinkr_debug_stamps"):
-        _abi.lib().sinkr_debug_stamps(cache.handle, st, 12)
+        _abi.lib().sinkr_debug_stamps(cache.handle, st, 13)
         d = [int(st[i + 1]) - int(st[i]) for i in range(11)]
-        print("  stamp deltas (cycles):", d)
+        print("  stamp deltas (cycles):", d, "loads+products(thread0):", int(st[12]) - int(st[1]))
     hq = spec.queries()[0]
     res = P.routed_decode_step(hq, 0, cache, cfg)
     c = res.counters
