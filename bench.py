@@ -150,15 +150,14 @@ def fill_ref_cache(spec, threads):
 
     def slot(g):
         k0, v0 = spec.first_rows(0, g)
-        kk, kv = spec.slot_keys(0, g)
         k = np.empty((L, D), np.float32)
         v = np.empty((L, D), np.float32)
         k[0], v[0] = k0, v0
-        if L > 1:
-            for key, dst in ((kk, k), (kv, v)):
-                orc.lib.orc_fill_rows(C.c_uint64(key), C.c_size_t(1), C.c_size_t(L - 1),
-                                      C.c_size_t(D), C.c_float(1.0),
-                                      dst[1:].ctypes.data_as(C.c_void_p))
+        for row0, rows, key_k, key_v, scale in spec.segments(0, g):
+            for key, dst in ((key_k, k), (key_v, v)):
+                orc.lib.orc_fill_rows(C.c_uint64(key), C.c_size_t(row0), C.c_size_t(rows),
+                                      C.c_size_t(D), C.c_float(scale),
+                                      dst[row0:row0 + rows].ctypes.data_as(C.c_void_p))
         return g, k, v
 
     with ThreadPoolExecutor(max_workers=min(threads, spec.num_kv_heads)) as ex:
@@ -310,6 +309,67 @@ def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
         out.append(row)
         if cache is not main_cache:
             cache.close()
+    del flush
+    return out
+
+
+OTHER_CONFIGS = [
+    ("C1 llama3.1-8b-attn L=32768 B=1", dict(num_q_heads=32, num_kv_heads=8, length=32768)),
+    ("C3 yi-9b-200k-attn L=204800 B=16", dict(num_q_heads=32, num_kv_heads=4, length=204800,
+                                             num_seqs=16)),
+    ("C4 llama3.1-70b-attn L=524288 B=1", dict(num_q_heads=64, num_kv_heads=8, length=524288)),
+    ("C5 llava-1.5-13b-attn L=8192 B=32 (576 image tokens)",
+     dict(num_q_heads=40, num_kv_heads=40, length=8192, num_seqs=32, image_tokens=576)),
+]
+
+
+def time_flushed(P, torch, cache, cfg, dq, dout, flush, reps=10):
+    """Median single-step time with a read-only L2 flush before each step."""
+    stream = torch.cuda.ExternalStream(cache.stream)
+    for _ in range(3):
+        P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+    torch.cuda.synchronize()
+    evs = []
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            flush.sum()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+            e1.record(stream)
+            evs.append((e0, e1))
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) * 1e3 for a, b in evs)
+
+
+def other_configs(P, torch, args, spec_cls, dense_cfg, routed_cfg):
+    """BASELINE.json configs other than the headline, single GPU, same step
+    (routed at the same fraction vs the own dense path), L2-flushed steps."""
+    out = []
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for name, kw in OTHER_CONFIGS:
+        spec = spec_cls(**kw, sink_fraction=args.sink_fraction, seed=args.seed)
+        cc = P.CacheConfig(1, spec.num_q_heads, spec.num_kv_heads, 128, spec.length,
+                           spec.num_seqs)
+        with P.KvCache(cc) as cache:
+            spec.fill(cache)
+            P.set_timing(cache, False)
+            dq = torch.from_numpy(spec.queries()).cuda()
+            dout = torch.empty_like(dq)
+            us = {n: time_flushed(P, torch, cache, c, dq, dout, flush)
+                  for n, c in (("dense", dense_cfg), ("routed", routed_cfg))}
+            info = P.fetch_step_info(cache)
+        n_act = info.counters.groups_active
+        kvb = n_act * 2 * spec.length * 128 * 2
+        row = {"config": name, "groups_active": n_act,
+               "groups_total": spec.num_seqs * spec.num_kv_heads,
+               "routed_us": round(us["routed"], 2), "dense_us": round(us["dense"], 2),
+               "speedup_vs_dense": round(us["dense"] / us["routed"], 3),
+               "kv_gbs_routed": round(kvb / (us["routed"] * 1e-6) / 1e9, 1)}
+        if spec.num_seqs > 1:
+            row["sequences_per_s_routed"] = round(spec.num_seqs / (us["routed"] * 1e-6), 1)
+        out.append(row)
     del flush
     return out
 
@@ -473,6 +533,8 @@ def run_ours(args, world, rank, local_rank):
     if not args.no_sweep:
         line["sweep"] = sweep(P, torch, args, WorkloadSpec, dense_cfg, routed_cfg, cache)
     cache.close()
+    if not args.no_sweep:
+        line["other_configs"] = other_configs(P, torch, args, WorkloadSpec, dense_cfg, routed_cfg)
     print(json.dumps(line), flush=True)
 
 

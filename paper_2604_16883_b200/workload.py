@@ -21,7 +21,7 @@ import numpy as np
 GOLDEN = np.uint64(0x9E3779B97F4A7C15)
 M1 = np.uint64(0xBF58476D1CE4E5B9)
 M2 = np.uint64(0x94D049BB133111EB)
-TAG_K, TAG_V, TAG_Q, TAG_ANCHOR = 1, 2, 3, 4
+TAG_K, TAG_V, TAG_Q, TAG_ANCHOR, TAG_IMG_K, TAG_IMG_V = 1, 2, 3, 4, 5, 6
 
 
 def _sm64_final(z):
@@ -85,6 +85,8 @@ class WorkloadSpec:
     v0_scale: float = 1e-3
     rho_sink: float = 0.8
     capacity: int = 0              # 0 -> length
+    image_tokens: int = 0          # LLaVA-style image block: rows 1..image_tokens
+    image_scale: float = 1.5       # ... drawn from a separate, wider stream
 
     @property
     def r(self) -> int:
@@ -134,16 +136,28 @@ class WorkloadSpec:
         return out
 
     # -- materialisation --------------------------------------------------------
+    def segments(self, seq: int, head: int):
+        """Row segments after the planted row 0: (row0, rows, key_k, key_v, scale)."""
+        kk, kv = self.slot_keys(seq, head)
+        n_img = max(0, min(self.image_tokens, self.length - 1))
+        out = []
+        if n_img:
+            out.append((1, n_img, mix_seed(self.seed, (self.layer, seq, head, TAG_IMG_K)),
+                        mix_seed(self.seed, (self.layer, seq, head, TAG_IMG_V)),
+                        self.image_scale))
+        if self.length > 1 + n_img:
+            out.append((1 + n_img, self.length - 1 - n_img, kk, kv, 1.0))
+        return out
+
     def host_slot(self, seq: int, head: int):
         """f32 K, V [L, D] exactly as stored by the device cache."""
         k0, v0 = self.first_rows(seq, head)
-        kk, kv = self.slot_keys(seq, head)
         k = np.empty((self.length, self.head_dim), dtype=np.float32)
         v = np.empty_like(k)
         k[0], v[0] = k0, v0
-        if self.length > 1:
-            k[1:] = host_rows(kk, 1, self.length - 1, self.head_dim)
-            v[1:] = host_rows(kv, 1, self.length - 1, self.head_dim)
+        for row0, rows, key_k, key_v, scale in self.segments(seq, head):
+            k[row0:row0 + rows] = host_rows(key_k, row0, rows, self.head_dim, scale)
+            v[row0:row0 + rows] = host_rows(key_v, row0, rows, self.head_dim, scale)
         return k, v
 
     def host_cache(self, seq: int = 0):
@@ -157,6 +171,6 @@ class WorkloadSpec:
             for g in range(self.num_kv_heads):
                 k0, v0 = self.first_rows(s, g)
                 cache.append(self.layer, g, k0, v0, seq=s)
-                if self.length > 1:
-                    kk, kv = self.slot_keys(s, g)
-                    cache.append_synthetic(self.layer, g, kk, kv, self.length - 1, seq=s)
+                for row0, rows, key_k, key_v, scale in self.segments(s, g):
+                    cache.append_synthetic(self.layer, g, key_k, key_v, rows, k_scale=scale,
+                                           v_scale=scale, seq=s, global_row0=row0)
