@@ -200,64 +200,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     // ======================= phase R: routing ================================
-    // proxy_score (router.cpp:36-48): head i belongs to unit i / r.  q and k0
-    // rows are staged in smem as f32 (coalesced loads, all issued up front);
-    // then thread h runs the dot chain and thread 64+h the |q|^2 chain, each a
-    // sequential fp64 FMA chain in index order.  A product of two floats is
-    // exact in fp64, so fma(q_j, k_j, s) == round(s + q_j*k_j): bit-identical to
-    // the reference's `s += (double)q[i] * k0[i]`.
-    {
-        double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1] f64
+    // proxy_score (router.cpp:36-48), group_score (50-57), route (67-75) and the
+    // task build (131-145).  Two forms with identical results:
+    //  * lean (B*H_q <= 64, B*H_kv <= 32: every single-sequence shape): all
+    //    warps form the exact fp64 products (a product of two floats is exact
+    //    in fp64, so s + p is bit-identical to the reference's
+    //    `s += (double)q[i] * k0[i]`); thread h then runs its head's dot and
+    //    |q|^2 chains interleaved (sequential DADDs in index order: ~8 cycles
+    //    each, the floor of this phase) and scores it.  Warp 0 routes one unit
+    //    per lane and builds the Active list with a ballot: two block barriers
+    //    in all, and a short code path (the phase is latency bound).
+    //  * tiled (batched steps): 64-head tiles staged through shared memory,
+    //    block-wide scans over the units.
+    const bool lean = NH <= (uint32_t)kRouteTile && U <= 32u;
+    if (lean) {
+        // exact fp64 products q_j*k_j and q_j*q_j (f32 x f32 fits in 53 bits)
+        // of every head, computed by all warps off the chains and staged in
+        // smem rows of odd stride (D+1 doubles; conflict-free chain reads) with
+        // a lane-rotated element order (conflict-free stores).  Warp w takes
+        // heads w, w+5, ...; lane l holds elements kV*l .. kV*l+kV-1.
+        double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1]
         double* sk = sq + kRouteTile * SC::kDP;
-        double* s_chain = sk + kRouteTile * SC::kDP;  // [2][kRouteTile]
-        for (uint32_t h_base = 0; h_base < NH; h_base += kRouteTile) {
-            const uint32_t nh = min((uint32_t)kRouteTile, NH - h_base);
-            // warp w loads heads w, w+5, ...; lane l loads kV = D/32 consecutive
-            // floats of the row with one vector load.  The products go to smem
-            // rows of odd stride (D+1 doubles, conflict-free for the chains)
-            // with a lane-rotated element order, so the stores are conflict-free
-            // as well.
+        {
             constexpr int kW = kThreads / 32;
             constexpr int kHPW = (kRouteTile + kW - 1) / kW;
             constexpr int kV = D / 32;
-            float qv[kHPW][kV], kv[kHPW][kV];
             const uint64_t keep = ptx::policy_evict_last();
+            const uint32_t rmagic = 0xFFFFFFFFu / r + 1u;  // i / r == umulhi(i, rmagic) for i < 2^16
+            const float* kbase = t.anchors + size_t(layer) * U * D + kV * lane;
+            float qv[kHPW][kV], kv[kHPW][kV];
 #pragma unroll
             for (int a = 0; a < kHPW; ++a) {
-                const uint32_t hl = warp + a * kW;
-                const bool ok = hl < nh;
-                const uint32_t i = h_base + (ok ? hl : 0);
-                const float* qrow = t.q + size_t(i) * D + kV * lane;
-                const float* krow = t.anchors + (size_t(layer) * U + i / r) * D + kV * lane;
+                const uint32_t h = min(warp + a * kW, NH - 1);
+                const float* qrow = t.q + size_t(h) * D + kV * lane;
+                const float* krow = kbase + size_t(r == 1 ? h : __umulhi(h, rmagic)) * D;
                 if constexpr (kV == 4) {
-                    float4 x = make_float4(0.f, 0.f, 0.f, 0.f), y = x;
-                    if (ok) {
-                        x = ptx::ldg_last4(qrow, keep);
-                        y = ptx::ldg_last4(krow, keep);
-                    }
+                    const float4 x = ptx::ldg_last4(qrow, keep), y = ptx::ldg_last4(krow, keep);
                     qv[a][0] = x.x; qv[a][1] = x.y; qv[a][2] = x.z; qv[a][3] = x.w;
                     kv[a][0] = y.x; kv[a][1] = y.y; kv[a][2] = y.z; kv[a][3] = y.w;
                 } else if constexpr (kV == 2) {
-                    float2 x = make_float2(0.f, 0.f), y = x;
-                    if (ok) {
-                        x = ptx::ldg_last2(qrow, keep);
-                        y = ptx::ldg_last2(krow, keep);
-                    }
+                    const float2 x = ptx::ldg_last2(qrow, keep), y = ptx::ldg_last2(krow, keep);
                     qv[a][0] = x.x; qv[a][1] = x.y;
                     kv[a][0] = y.x; kv[a][1] = y.y;
                 } else {
-                    qv[a][0] = ok ? ptx::ldg_last(qrow, keep) : 0.f;
-                    kv[a][0] = ok ? ptx::ldg_last(krow, keep) : 0.f;
+                    qv[a][0] = ptx::ldg_last(qrow, keep);
+                    kv[a][0] = ptx::ldg_last(krow, keep);
                 }
             }
-            double kn = 1.0;
-            if (tid < nh)
-                kn = (double)ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + (h_base + tid) / r], keep);
-            // exact fp64 products (f32 x f32 fits in 53 bits), off the chain
+            if (tid == 0) STAMP(13);
 #pragma unroll
             for (int a = 0; a < kHPW; ++a) {
-                const uint32_t hl = warp + a * kW;
-                if (hl < nh) {
+                const uint32_t h = warp + a * kW;
+                if (h < NH) {
 #pragma unroll
                     for (int e = 0; e < kV; ++e) {
                         const uint32_t idx = (e + lane) % kV;
@@ -269,145 +263,332 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 kf = kv[a][c];
                             }
                         const double qd = (double)qf;
-                        sq[hl * SC::kDP + kV * lane + idx] = __dmul_rn(qd, (double)kf);
-                        sk[hl * SC::kDP + kV * lane + idx] = __dmul_rn(qd, qd);
+                        sq[h * SC::kDP + kV * lane + idx] = __dmul_rn(qd, (double)kf);
+                        sk[h * SC::kDP + kV * lane + idx] = __dmul_rn(qd, qd);
                     }
                 }
             }
-            if (h_base == 0) STAMP(12);
-            __syncthreads();
-            STAMP(2);
-            if (tid < 2 * kRouteTile && (tid % kRouteTile) < nh) {
-                const uint32_t hl = tid % kRouteTile;
-                // thread h: the dot chain; thread 64+h: the |q|^2 chain, each a
-                // sequential sum in index order (router.cpp:40-43)
-                const double* a = (tid < (uint32_t)kRouteTile ? sq : sk) + hl * SC::kDP;
-                double acc = 0.0;
+        }
+        STAMP(15);
+        __syncthreads();
+        STAMP(16);
+        if (tid < NH) {
+            // the dot and |q|^2 chains of head tid, interleaved: each a
+            // sequential fp64 sum in index order (router.cpp:40-43)
+            const uint32_t u = tid / r;
+            const float kn = ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + u], ptx::policy_evict_last());
+            const double* pa = sq + tid * SC::kDP;
+            const double* pb = sk + tid * SC::kDP;
+            double dot = 0.0, qq = 0.0;
 #pragma unroll 16
-                for (uint32_t j = 0; j < D; ++j) acc = __dadd_rn(acc, a[j]);
-                s_chain[tid] = acc;
+            for (uint32_t j = 0; j < (uint32_t)D; ++j) {
+                dot = __dadd_rn(dot, pa[j]);
+                qq = __dadd_rn(qq, pb[j]);
             }
-            __syncthreads();
-            if (tid < nh) {
-                const double dot = s_chain[tid], qsq = s_chain[kRouteTile + tid];
-                const double qn = __dsqrt_rn(qsq);
-                double sc = 0.0;
-                uint8_t dg = 0;
-                if (qn < 1e-12) {
-                    dg = 1;
-                } else {
-                    sc = __ddiv_rn(dot, __dmul_rn(qn, kn));
-                    sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
+            if (tid == 0) STAMP(14);
+            const double qn = __dsqrt_rn(qq);
+            double sc = 0.0;
+            uint8_t dg = 0;
+            if (qn < 1e-12) {
+                dg = 1;
+            } else {
+                sc = __ddiv_rn(dot, __dmul_rn(qn, (double)kn));
+                sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
+            }
+            s_score[tid] = sc;
+            s_degen[tid] = dg;
+            if (lead) t.head_scores[tid] = sc;
+        }
+        STAMP(12);
+        __syncthreads();  // scores, tau and len visible
+        STAMP(2);
+        if (warp == 0) {
+            const uint32_t u = lane;
+            bool active = false;
+            uint32_t L = 0;
+            if (u < U) {
+                const uint32_t seq = u / t.Hkv;
+                double sum = 0.0;
+                uint32_t degen = 0;
+                for (uint32_t i = 0; i < r; ++i) {
+                    sum = __dadd_rn(sum, s_score[u * r + i]);
+                    degen |= s_degen[u * r + i];
                 }
-                s_score[h_base + tid] = sc;
-                s_degen[h_base + tid] = dg;
-            }
-            __syncthreads();
-            STAMP(3);
-        }
-    }
-
-    // group_score + route (router.cpp:50-57,67-75,113-120) on contiguous unit
-    // runs per thread, then an order-preserving scan builds the Active list.
-    const uint32_t per = (U + kThreads - 1) / kThreads;
-    const uint32_t u0 = min(U, tid * per), u1 = min(U, u0 + per);
-    uint32_t my_active = 0;
-    unsigned long long my_tok = 0;
-    uint64_t my_bits = 0;  // active bits of this thread's run (per <= 64 guaranteed)
-    for (uint32_t u = u0; u < u1; ++u) {
-        const uint32_t seq = u / t.Hkv;
-        double sum = 0.0;
-        uint32_t degen = 0;
-        for (uint32_t i = 0; i < r; ++i) {
-            sum = __dadd_rn(sum, s_score[u * r + i]);
-            degen |= s_degen[u * r + i];
-        }
-        // sum / r (router.cpp:56); for power-of-two r the product with 1/r is
-        // the same correctly rounded value and avoids the division sequence
-        const double S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
-        const double tau = s_tau[seq];
-        const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
-        bool sink = over && !(flags & kLayerExcluded);
-        if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
-        const bool active = (flags & kObserveOnly) || !sink;
-        if (active) {
-            ++my_active;
-            my_tok += s_len[seq];
-            my_bits |= 1ull << (u - u0);
-        }
-        if (lead) {
-            t.group_scores[u] = S;
-            t.unit_flags[u] =
-                (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
-            if (!active) {
-                t.tokens[u] = 0ull;
-                if (t.mode == 1) {  // rank partial of a skipped group: empty
-                    float* P = t.out + size_t(u) * r * (D + 2);
-                    for (uint32_t h = 0; h < r; ++h) {
-                        P[h] = -INFINITY;
-                        P[r + h] = 0.f;
+                // sum / r (router.cpp:56); for power-of-two r the product with
+                // 1/r is the same correctly rounded value
+                const double S =
+                    (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
+                const double tau = s_tau[seq];
+                const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
+                bool sink = over && !(flags & kLayerExcluded);
+                if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
+                active = (flags & kObserveOnly) || !sink;
+                L = s_len[seq];
+                if (lead) {
+                    t.group_scores[u] = S;
+                    t.unit_flags[u] =
+                        (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
+                    if (!active) {
+                        t.tokens[u] = 0ull;
+                        if (t.mode == 1) {  // rank partial of a skipped group: empty
+                            float* P = t.out + size_t(u) * r * (D + 2);
+                            for (uint32_t h = 0; h < r; ++h) {
+                                P[h] = -INFINITY;
+                                P[r + h] = 0.f;
+                            }
+                            for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+                        }
                     }
-                    for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+                }
+            }
+            const uint32_t mask = __ballot_sync(0xffffffffu, active);
+            const uint32_t nact = __popc(mask);
+            const uint32_t pos = __popc(mask & ((1u << lane) - 1u));
+            if (active) {
+                act_unit[pos] = (uint16_t)u;
+                act_len[pos] = L;
+            }
+            unsigned long long T = active ? (unsigned long long)L : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
+            const uint32_t gdiv = G * kChunksPerCta;
+            unsigned long long cc = T < (1ull << 32)
+                                        ? (unsigned long long)(((uint32_t)T + gdiv - 1) / gdiv)
+                                        : (T + gdiv - 1) / gdiv;
+            cc = ((cc + kStageTok - 1) / kStageTok) * kStageTok;
+            if (cc < kMinChunkTok) cc = kMinChunkTok;
+            const bool flat = nact > G;
+            if (flat) {  // chunk prefix over the Active list (lane order == list order)
+                ChunkPlan cp;
+                cp.C = (uint32_t)cc;
+                cp.c = kTailChunkTok;
+                cp.tail = ((G + nact - 1) / max(nact, 1u) + 1) * 2 * kTailChunkTok;
+                const uint32_t mine = active ? plan_nch(L, cp) : 0u;
+                uint32_t incl = mine;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (uint32_t)o) incl += y;
+                }
+                if (active) act_prefix[pos] = incl - mine;
+                if (lane == 31) act_prefix[nact] = incl;
+            }
+            if (lane == 0) {
+                misc[kMiscNact] = nact;
+                misc[kMiscChunk] = (uint32_t)cc;
+                misc[kMiscFlat] = flat ? 1u : 0u;
+            }
+        }
+        STAMP(3);
+    } else {
+        // tiled: head i belongs to unit i / r.  The exact fp64 products of
+        // 64-head tiles are staged in smem; then thread h runs the dot chain and
+        // thread 64+h the |q|^2 chain, each a sequential fp64 sum in index order.
+        {
+            double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1] f64
+            double* sk = sq + kRouteTile * SC::kDP;
+            double* s_chain = sk + kRouteTile * SC::kDP;  // [2][kRouteTile]
+            for (uint32_t h_base = 0; h_base < NH; h_base += kRouteTile) {
+                const uint32_t nh = min((uint32_t)kRouteTile, NH - h_base);
+                // warp w loads heads w, w+5, ...; lane l loads kV = D/32 consecutive
+                // floats of the row with one vector load.  The products go to smem
+                // rows of odd stride (D+1 doubles, conflict-free for the chains)
+                // with a lane-rotated element order, so the stores are conflict-free
+                // as well.
+                constexpr int kW = kThreads / 32;
+                constexpr int kHPW = (kRouteTile + kW - 1) / kW;
+                constexpr int kV = D / 32;
+                float qv[kHPW][kV], kv[kHPW][kV];
+                const uint64_t keep = ptx::policy_evict_last();
+#pragma unroll
+                for (int a = 0; a < kHPW; ++a) {
+                    const uint32_t hl = warp + a * kW;
+                    const bool ok = hl < nh;
+                    const uint32_t i = h_base + (ok ? hl : 0);
+                    const float* qrow = t.q + size_t(i) * D + kV * lane;
+                    const float* krow = t.anchors + (size_t(layer) * U + i / r) * D + kV * lane;
+                    if constexpr (kV == 4) {
+                        float4 x = make_float4(0.f, 0.f, 0.f, 0.f), y = x;
+                        if (ok) {
+                            x = ptx::ldg_last4(qrow, keep);
+                            y = ptx::ldg_last4(krow, keep);
+                        }
+                        qv[a][0] = x.x; qv[a][1] = x.y; qv[a][2] = x.z; qv[a][3] = x.w;
+                        kv[a][0] = y.x; kv[a][1] = y.y; kv[a][2] = y.z; kv[a][3] = y.w;
+                    } else if constexpr (kV == 2) {
+                        float2 x = make_float2(0.f, 0.f), y = x;
+                        if (ok) {
+                            x = ptx::ldg_last2(qrow, keep);
+                            y = ptx::ldg_last2(krow, keep);
+                        }
+                        qv[a][0] = x.x; qv[a][1] = x.y;
+                        kv[a][0] = y.x; kv[a][1] = y.y;
+                    } else {
+                        qv[a][0] = ok ? ptx::ldg_last(qrow, keep) : 0.f;
+                        kv[a][0] = ok ? ptx::ldg_last(krow, keep) : 0.f;
+                    }
+                }
+                double kn = 1.0;
+                if (tid < nh)
+                    kn = (double)ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + (h_base + tid) / r], keep);
+                // exact fp64 products (f32 x f32 fits in 53 bits), off the chain
+#pragma unroll
+                for (int a = 0; a < kHPW; ++a) {
+                    const uint32_t hl = warp + a * kW;
+                    if (hl < nh) {
+#pragma unroll
+                        for (int e = 0; e < kV; ++e) {
+                            const uint32_t idx = (e + lane) % kV;
+                            float qf = qv[a][0], kf = kv[a][0];
+#pragma unroll
+                            for (int c = 1; c < kV; ++c)
+                                if (idx == (uint32_t)c) {
+                                    qf = qv[a][c];
+                                    kf = kv[a][c];
+                                }
+                            const double qd = (double)qf;
+                            sq[hl * SC::kDP + kV * lane + idx] = __dmul_rn(qd, (double)kf);
+                            sk[hl * SC::kDP + kV * lane + idx] = __dmul_rn(qd, qd);
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid < 2 * kRouteTile && (tid % kRouteTile) < nh) {
+                    const uint32_t hl = tid % kRouteTile;
+                    // thread h: the dot chain; thread 64+h: the |q|^2 chain, each a
+                    // sequential sum in index order (router.cpp:40-43)
+                    const double* a = (tid < (uint32_t)kRouteTile ? sq : sk) + hl * SC::kDP;
+                    double acc = 0.0;
+#pragma unroll 16
+                    for (uint32_t j = 0; j < D; ++j) acc = __dadd_rn(acc, a[j]);
+                    s_chain[tid] = acc;
+                }
+                __syncthreads();
+                if (tid < nh) {
+                    const double dot = s_chain[tid], qsq = s_chain[kRouteTile + tid];
+                    const double qn = __dsqrt_rn(qsq);
+                    double sc = 0.0;
+                    uint8_t dg = 0;
+                    if (qn < 1e-12) {
+                        dg = 1;
+                    } else {
+                        sc = __ddiv_rn(dot, __dmul_rn(qn, kn));
+                        sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
+                    }
+                    s_score[h_base + tid] = sc;
+                    s_degen[h_base + tid] = dg;
+                }
+                __syncthreads();
+            }
+        }
+
+        // group_score + route (router.cpp:50-57,67-75,113-120) on contiguous unit
+        // runs per thread, then an order-preserving scan builds the Active list.
+        const uint32_t per = (U + kThreads - 1) / kThreads;
+        const uint32_t u0 = min(U, tid * per), u1 = min(U, u0 + per);
+        uint32_t my_active = 0;
+        unsigned long long my_tok = 0;
+        uint64_t my_bits = 0;  // active bits of this thread's run (per <= 64 guaranteed)
+        for (uint32_t u = u0; u < u1; ++u) {
+            const uint32_t seq = u / t.Hkv;
+            double sum = 0.0;
+            uint32_t degen = 0;
+            for (uint32_t i = 0; i < r; ++i) {
+                sum = __dadd_rn(sum, s_score[u * r + i]);
+                degen |= s_degen[u * r + i];
+            }
+            // sum / r (router.cpp:56); for power-of-two r the product with 1/r is
+            // the same correctly rounded value and avoids the division sequence
+            const double S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
+            const double tau = s_tau[seq];
+            const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
+            bool sink = over && !(flags & kLayerExcluded);
+            if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
+            const bool active = (flags & kObserveOnly) || !sink;
+            if (active) {
+                ++my_active;
+                my_tok += s_len[seq];
+                my_bits |= 1ull << (u - u0);
+            }
+            if (lead) {
+                t.group_scores[u] = S;
+                t.unit_flags[u] =
+                    (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
+                if (!active) {
+                    t.tokens[u] = 0ull;
+                    if (t.mode == 1) {  // rank partial of a skipped group: empty
+                        float* P = t.out + size_t(u) * r * (D + 2);
+                        for (uint32_t h = 0; h < r; ++h) {
+                            P[h] = -INFINITY;
+                            P[r + h] = 0.f;
+                        }
+                        for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+                    }
                 }
             }
         }
+        const unsigned long long tok_all = Reduce(tmp.reduce).Sum(my_tok);
+        if (tid == 0) s_tok_total = tok_all;
+        __syncthreads();
+        uint32_t a_off, nact;
+        Scan(tmp.scan).ExclusiveSum(my_active, a_off, nact);
+        // chunk size: ~kChunksPerCta chunks per CTA, >= kMinChunkTok, stage multiple
+        const unsigned long long T = s_tok_total;
+        const uint32_t gdiv = G * kChunksPerCta;
+        unsigned long long cc = T < (1ull << 32)
+                                    ? (unsigned long long)(((uint32_t)T + gdiv - 1) / gdiv)
+                                    : (T + gdiv - 1) / gdiv;
+        cc = ((cc + kStageTok - 1) / kStageTok) * kStageTok;
+        if (cc < kMinChunkTok) cc = kMinChunkTok;
+        const uint32_t Ck = (uint32_t)cc;
+        const bool flat = nact > G;
+        ChunkPlan cp;
+        cp.C = Ck;
+        cp.c = kTailChunkTok;
+        cp.tail = ((G + nact - 1) / max(nact, 1u) + 1) * 2 * kTailChunkTok;
+        uint32_t my_chunks = 0;
+        {
+            uint32_t a = a_off;
+            for (uint32_t u = u0; u < u1; ++u) {
+                if (!((my_bits >> (u - u0)) & 1ull)) continue;
+                const uint32_t L = s_len[u / t.Hkv];
+                act_len[a] = L;
+                act_unit[a++] = (uint16_t)u;
+                if (flat) my_chunks += plan_nch(L, cp);
+            }
+        }
+        if (flat) {
+            __syncthreads();
+            uint32_t c_off, c_tot;
+            Scan(tmp.scan).ExclusiveSum(my_chunks, c_off, c_tot);
+            uint32_t a = a_off;
+            for (uint32_t u = u0; u < u1; ++u) {
+                if (!((my_bits >> (u - u0)) & 1ull)) continue;
+                act_prefix[a] = c_off;
+                c_off += plan_nch(act_len[a++], cp);
+            }
+            if (tid == 0) act_prefix[nact] = c_tot;
+        }
+        if (tid == 0) {
+            misc[kMiscNact] = nact;
+            misc[kMiscChunk] = Ck;
+            misc[kMiscFlat] = flat ? 1u : 0u;
+        }
+        if (lead)
+            for (uint32_t i = tid; i < NH; i += kThreads) t.head_scores[i] = s_score[i];
     }
-    const unsigned long long tok_all = Reduce(tmp.reduce).Sum(my_tok);
-    STAMP(4);
-    if (tid == 0) s_tok_total = tok_all;
-    __syncthreads();
-    STAMP(5);
-    uint32_t a_off, nact;
-    Scan(tmp.scan).ExclusiveSum(my_active, a_off, nact);
-    STAMP(6);
-    // chunk size: ~kChunksPerCta chunks per CTA, >= kMinChunkTok, stage multiple
-    const unsigned long long T = s_tok_total;
-    const uint32_t gdiv = G * kChunksPerCta;
-    unsigned long long cc = T < (1ull << 32)
-                                ? (unsigned long long)(((uint32_t)T + gdiv - 1) / gdiv)
-                                : (T + gdiv - 1) / gdiv;
-    cc = ((cc + kStageTok - 1) / kStageTok) * kStageTok;
-    if (cc < kMinChunkTok) cc = kMinChunkTok;
-    const uint32_t Ck = (uint32_t)cc;
-    const bool flat = nact > G;
+    __syncthreads();  // Active list, chunk plan and misc visible to all threads
+    STAMP(7);
+    const uint32_t nact = misc[kMiscNact];
+    const uint32_t Ck = misc[kMiscChunk];
+    const bool flat = misc[kMiscFlat] != 0;
     ChunkPlan cp;
     cp.C = Ck;
     cp.c = kTailChunkTok;
     cp.tail = ((G + nact - 1) / max(nact, 1u) + 1) * 2 * kTailChunkTok;
-    uint32_t my_chunks = 0;
-    {
-        uint32_t a = a_off;
-        for (uint32_t u = u0; u < u1; ++u) {
-            if (!((my_bits >> (u - u0)) & 1ull)) continue;
-            const uint32_t L = s_len[u / t.Hkv];
-            act_len[a] = L;
-            act_unit[a++] = (uint16_t)u;
-            if (flat) my_chunks += plan_nch(L, cp);
-        }
-    }
-    if (flat) {
-        __syncthreads();
-        uint32_t c_off, c_tot;
-        Scan(tmp.scan).ExclusiveSum(my_chunks, c_off, c_tot);
-        uint32_t a = a_off;
-        for (uint32_t u = u0; u < u1; ++u) {
-            if (!((my_bits >> (u - u0)) & 1ull)) continue;
-            act_prefix[a] = c_off;
-            c_off += plan_nch(act_len[a++], cp);
-        }
-        if (tid == 0) act_prefix[nact] = c_tot;
-    }
-    if (tid == 0) {
-        misc[kMiscNact] = nact;
-        misc[kMiscChunk] = Ck;
-        // few, long Active groups: merge tasks spread over all CTAs at the end;
-        // many groups: the CTA that streams a group's last rows merges it.
-        misc[kMiscQueue] = (4 * nact <= G) ? 1u : 0u;
-        misc[kMiscFlat] = flat ? 1u : 0u;
-    }
-    if (lead)
-        for (uint32_t i = tid; i < NH; i += kThreads) t.head_scores[i] = s_score[i];
-    STAMP(7);
+    // few, long Active groups: merge tasks spread over all CTAs at the end;
+    // many groups: the CTA that streams a group's last rows merges it.
+    const bool queue_mode = 4 * nact <= G;
     // zero surrogate rows of Sink groups (router.cpp:97): sink unit u is
     // written by CTA u mod G (binary search of the sorted Active list)
     if (t.mode == 0 && nact < U) {
@@ -425,7 +606,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
     if (t.trace && tid == 0) t.trace[bid * 8 + 0] = globaltimer();
-    const bool queue_mode = misc[kMiscQueue] != 0;
     if (lead && tid == 0) clk[1] = globaltimer();
 
     // ======================= phase S: stream + attend ==========================
