@@ -133,7 +133,8 @@ struct sinkr_engine {
     // step result block: out | head_scores | group_scores | tokens | flags
     size_t off_hs = 0, off_gs = 0, off_tok = 0, off_fl = 0, off_status = 0, res_bytes = 0;
     uint8_t* d_res = nullptr;
-    uint8_t* h_res = nullptr;
+    uint8_t* h_res = nullptr;      // pinned + mapped
+    uint8_t* h_res_dev = nullptr;  // device address of h_res (zero-copy results)
 
     dev::WorkState* d_ws = nullptr;
     uint32_t* d_active = nullptr;
@@ -207,7 +208,9 @@ struct sinkr_engine {
         t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
         return t;
     }
-    dev::StepTables step_tables(const float* q, float* out, int mode) const {
+    dev::StepTables step_tables(const float* q, float* out, int mode,
+                                uint8_t* res = nullptr) const {
+        if (!res) res = d_res;
         dev::StepTables t{};
         t.tmk = d_tmap;
         t.tmv = d_tmap + 1;
@@ -216,11 +219,11 @@ struct sinkr_engine {
         t.anchor_norm = d_anchor_norm;
         t.tau_g = reinterpret_cast<const double*>(d_in + off_tau);
         t.len_g = reinterpret_cast<const uint32_t*>(d_in + off_len);
-        t.head_scores = reinterpret_cast<double*>(d_res + off_hs);
-        t.group_scores = reinterpret_cast<double*>(d_res + off_gs);
-        t.unit_flags = reinterpret_cast<uint32_t*>(d_res + off_fl);
-        t.tokens = reinterpret_cast<unsigned long long*>(d_res + off_tok);
-        t.status = reinterpret_cast<uint32_t*>(d_res + off_status);
+        t.head_scores = reinterpret_cast<double*>(res + off_hs);
+        t.group_scores = reinterpret_cast<double*>(res + off_gs);
+        t.unit_flags = reinterpret_cast<uint32_t*>(res + off_fl);
+        t.tokens = reinterpret_cast<unsigned long long*>(res + off_tok);
+        t.status = reinterpret_cast<uint32_t*>(res + off_status);
         t.ss = d_ss;
         t.cursor = d_cursor;
         t.slot_count = d_slot_count;
@@ -325,9 +328,10 @@ void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     CK(cudaLaunchKernelEx(&cfg, dev::step_kernel<D>, st, e->pp));
 }
 
-void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
+void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode,
+                  uint8_t* res = nullptr) {
     if (e->fused) {
-        const dev::StepTables st = e->step_tables(d_q, d_out, mode);
+        const dev::StepTables st = e->step_tables(d_q, d_out, mode, res);
         if (e->timing) CK(cudaEventRecord(e->ev[0], e->stream));
         switch (e->D) {
             case 32: launch_step<32>(e, st); break;
@@ -428,6 +432,75 @@ void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
     if (e->step_events) CK(cudaEventRecord(e->ev[0], e->stream));
     CK(cudaGraphLaunch(ge.exec, e->stream));
     if (e->step_events) CK(cudaEventRecord(e->ev[3], e->stream));
+}
+
+// The host-buffer step (sinkr_routed_decode_batch) as ONE graph: the H2D copy
+// of the staged input block (params + queries) and the fused step kernel,
+// which writes outputs and the routing record straight into the mapped pinned
+// result block (zero-copy, no D2H copy node).  One submission per step and no
+// host round trip between the copy and the kernel.
+static int io_mode() {
+    static int m = [] {
+        const char* v = std::getenv("SINKR_IO");
+        return v ? std::atoi(v) : 1;
+    }();
+    return m;
+}
+
+void run_io_graph(sinkr_engine* e) {
+    e->last_launches = 1;
+    e->last_mode = 0;
+    const auto key = std::make_tuple((const void*)e->h_in, (void*)e->h_res, 2);
+    auto it = e->graphs.find(key);
+    const float* d_q = reinterpret_cast<const float*>(e->d_in + e->off_q);
+    const bool zc = io_mode() == 1;
+    uint8_t* res = zc ? e->h_res_dev : e->d_res;
+    float* out = reinterpret_cast<float*>(res);
+    if (it == e->graphs.end()) {
+        sinkr_engine::GraphEntry ge;
+        CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
+            const bool timing = e->timing;
+            e->timing = false;
+            enqueue_step(e, d_q, out, 0, res);
+            e->timing = timing;
+            if (!zc)
+                CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+        } catch (...) {
+            cudaStreamEndCapture(e->stream, &ge.graph);
+            if (ge.graph) cudaGraphDestroy(ge.graph);
+            throw;
+        }
+        CK(cudaStreamEndCapture(e->stream, &ge.graph));
+        CK(cudaGraphInstantiate(&ge.exec, ge.graph, 0));
+        size_t n = 0;
+        CK(cudaGraphGetNodes(ge.graph, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        CK(cudaGraphGetNodes(ge.graph, nodes.data(), &n));
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeKernel) continue;
+            CK(cudaGraphKernelNodeGetParams(nd, &ge.probe_kp));
+            ge.probe = nd;
+        }
+        if (!ge.probe) fail(SINKR_CUDA_ERROR, "step node not found in the captured graph");
+        ge.step_t = e->step_tables(d_q, out, 0, res);
+        ge.fused = true;
+        ge.pp = e->pp;
+        it = e->graphs.emplace(key, ge).first;
+    }
+    auto& ge = it->second;
+    if (std::memcmp(&ge.pp, &e->pp, sizeof(e->pp)) != 0) {
+        ge.pp = e->pp;
+        void* args[2] = {&ge.step_t, &ge.pp};
+        cudaKernelNodeParams kp = ge.probe_kp;
+        kp.kernelParams = args;
+        kp.extra = nullptr;
+        CK(cudaGraphExecKernelNodeSetParams(ge.exec, ge.probe, &kp));
+    }
+    CK(cudaGraphLaunch(ge.exec, e->stream));
 }
 
 size_t token_count(const sinkr_engine* e, size_t seq) {
@@ -650,7 +723,9 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->off_status = align_up(e->off_fl + e->U * 4, 128);  // status[4] + clocks
             e->res_bytes = align_up(e->off_status + 64 + 256, 128);
             CK(cudaMalloc(&e->d_res, e->res_bytes));
-            CK(cudaMallocHost(&e->h_res, e->res_bytes));
+            CK(cudaHostAlloc(&e->h_res, e->res_bytes, cudaHostAllocMapped));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_res_dev), e->h_res, 0));
+            std::memset(e->h_res, 0, e->res_bytes);
             CK(cudaMemsetAsync(e->d_res, 0, e->res_bytes, e->stream));
 
             CK(cudaMalloc(&e->d_head_degen, e->B * Hq * 4));
@@ -1000,11 +1075,15 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
         // params were written into h_in by stage_params; append the queries
         // and upload the whole input block in one H2D copy.
         std::memcpy(e->h_in + e->off_q, queries, qbytes);
-        CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
-        CK(cudaEventRecord(e->ev_in, e->stream));
-        float* d_out = reinterpret_cast<float*>(e->d_res);
-        run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, 0);
-        CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+        if (e->fused && !e->timing && io_mode() != 0) {
+            run_io_graph(e);  // H2D + step kernel, results land in mapped h_res
+        } else {
+            CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
+            CK(cudaEventRecord(e->ev_in, e->stream));
+            float* d_out = reinterpret_cast<float*>(e->d_res);
+            run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, 0);
+            CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+        }
         CK(cudaStreamSynchronize(e->stream));
         if (!e->fused) {
             dev::WorkState ws;

@@ -232,18 +232,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int a = 0; a < kHPW; ++a) {
                 const uint32_t h = min(warp + a * kW, NH - 1);
+                // q through L2 (coherent: a zero-copy step stages it in this
+                // kernel); the anchors are read-only
                 const float* qrow = t.q + size_t(h) * D + kV * lane;
                 const float* krow = kbase + size_t(r == 1 ? h : __umulhi(h, rmagic)) * D;
                 if constexpr (kV == 4) {
-                    const float4 x = ptx::ldg_last4(qrow, keep), y = ptx::ldg_last4(krow, keep);
+                    const float4 x = ptx::ldg_last4(qrow, keep);
+                    const float4 y = ptx::ldg_last4(krow, keep);
                     qv[a][0] = x.x; qv[a][1] = x.y; qv[a][2] = x.z; qv[a][3] = x.w;
                     kv[a][0] = y.x; kv[a][1] = y.y; kv[a][2] = y.z; kv[a][3] = y.w;
                 } else if constexpr (kV == 2) {
-                    const float2 x = ptx::ldg_last2(qrow, keep), y = ptx::ldg_last2(krow, keep);
+                    const float2 x = ptx::ldg_last2(qrow, keep);
+                    const float2 y = ptx::ldg_last2(krow, keep);
                     qv[a][0] = x.x; qv[a][1] = x.y;
                     kv[a][0] = y.x; kv[a][1] = y.y;
                 } else {
-                    qv[a][0] = ptx::ldg_last(qrow, keep);
+                    qv[a][0] = __ldcg(qrow);
                     kv[a][0] = ptx::ldg_last(krow, keep);
                 }
             }
@@ -614,7 +618,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol = ptx::policy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
+            uint32_t n_emit = 0, tok_emit = 0;  // trace only
             auto emit = [&](uint32_t u, uint32_t L, uint32_t t0, uint32_t t1) {
+                ++n_emit;
+                tok_emit += t1 > t0 ? t1 - t0 : 0u;
                 const int32_t row0 = (int32_t)((size_t(layer) * U + u) * t.cap);
                 for (uint32_t tk = t0; tk < t1; tk += kStageTok) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1u);
@@ -665,7 +672,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         u = act_unit[a];
                         L = act_len[a];
                         first = ((G - a + nact - 1) / nact) * Ck;
-                        const uint32_t sz = guided(first);
+                        // size the hand-off claim from the unit's live cursor:
+                        // a CTA joining a nearly finished unit must not take a
+                        // full-size chunk off its tail
+                        const uint32_t sz = guided(first + ld_volatile(&t.cursor[a]));
                         t0 = first + atomicAdd(&t.cursor[a], sz);
                         t1 = min(t0 + sz, L);
                         continue;
@@ -697,6 +707,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     emit(u, L, t0, t1);
                     chunk = next;
                 }
+            }
+            if (t.trace) {
+                t.trace[bid * 8 + 6] = ((unsigned long long)n_emit << 32) | tok_emit;
+                t.trace[bid * 8 + 7] = globaltimer();
             }
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
             meta[stage].unit = kEnd;

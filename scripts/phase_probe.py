@@ -59,6 +59,14 @@ for L in Ls:
         se = rel(a[:, 1])
         print(f"  stream end min/med/max {se.min():.2f}/{np.median(se):.2f}/{se.max():.2f}; "
               f"merge end max {rel(a[:, 2]).max():.2f}; reset {rel(a[:, 5][a[:, 5] > 0]).max():.2f}")
+        ne = (a[:, 6].astype(np.uint64) >> np.uint64(32)).astype(np.int64)
+        te = (a[:, 6].astype(np.uint64) & np.uint64(0xffffffff)).astype(np.int64)
+        pe = rel(a[:, 7])
+        late = np.argsort(se)[-6:]
+        print("  latest CTAs (id: stream_end, producer_end, claims, tokens):",
+              [(int(c), round(se[c], 2), round(pe[c], 2), int(ne[c]), int(te[c])) for c in late])
+        print(f"  tokens/CTA min/med/max {te.min()}/{int(np.median(te))}/{te.max()}; "
+              f"producer end min/med/max {pe.min():.2f}/{np.median(pe):.2f}/{pe.max():.2f}")
         if s[0]:
             prev = s[0]
             line = []
