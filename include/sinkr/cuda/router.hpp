@@ -15,6 +15,9 @@
 //   auto_num_splits
 //   split_ranges                    attention.hpp:82-85   same
 //   routed_decode_step              router.hpp:84-86      same signature
+//   KvCache::save/load_snapshot     kv_cache.hpp:72-80    same (SNKT + manifest.json)
+//   calibration / analysis APIs     calibration.hpp, analysis.hpp -> sinkr/cuda/calibration.hpp,
+//                                                         sinkr/cuda/analysis.hpp
 //
 // Status codes are rethrown as the reference's exception classes
 // (std::invalid_argument / out_of_range / runtime_error / logic_error), so a
@@ -24,6 +27,7 @@
 
 #include <array>
 #include <cstddef>
+#include <filesystem>
 #include <cstdint>
 #include <span>
 #include <stdexcept>
@@ -63,6 +67,12 @@ struct GroupAnchor {
     float k0_norm = 0.0f;
 };
 
+struct CalibrationPoint {  // calibration.hpp:14-18
+    std::size_t length = 0;
+    double tau = 0.0;
+    double skip = 0.0;
+};
+
 struct ThresholdProfile {
     std::array<double, 4> coeffs{0.0, 0.0, 0.0, 0.0};
     double length_normalizer = 1.0;
@@ -71,6 +81,7 @@ struct ThresholdProfile {
     double target_skip = 0.60;
     double gamma = 0.65;
     std::vector<std::size_t> excluded_layers{0, 1};
+    std::vector<CalibrationPoint> points;
 
     static ThresholdProfile constant(double tau) {  // calibration.cpp:29-35
         ThresholdProfile p;
@@ -171,6 +182,17 @@ public:
     ~KvCache() { sinkr_engine_destroy(e_); }
     KvCache(const KvCache&) = delete;
     KvCache& operator=(const KvCache&) = delete;
+    KvCache(KvCache&& o) noexcept : config_(o.config_), e_(o.e_) { o.e_ = nullptr; }
+
+    // kv_cache.hpp:72-80 — SNKT files + manifest.json, one sequence per snapshot
+    void save_snapshot(const std::filesystem::path& dir, std::size_t seq = 0) const {
+        check(sinkr_save_snapshot(e_, seq, dir.string().c_str()));
+    }
+    static KvCache load_snapshot(const std::filesystem::path& dir, int device = 0) {
+        sinkr_engine* e = nullptr;
+        check(sinkr_load_snapshot(dir.string().c_str(), device, &e));
+        return KvCache(e);
+    }
 
     const CacheConfig& config() const { return config_; }
     sinkr_engine* handle() const { return e_; }
@@ -209,6 +231,12 @@ public:
     }
 
 private:
+    explicit KvCache(sinkr_engine* e) : e_(e) {
+        sinkr_cache_config c{};
+        check(sinkr_engine_config(e, &c));
+        config_ = CacheConfig{c.num_layers, c.num_q_heads, c.num_kv_heads,
+                              c.head_dim,   c.capacity,    c.num_seqs};
+    }
     CacheConfig config_;
     sinkr_engine* e_ = nullptr;
 };

@@ -7,14 +7,16 @@
  * torch or C++ types cross the boundary.  A C++ shim with the reference's own
  * signatures and exception types sits on top: include/sinkr/cuda/router.hpp.
  *
- * Hot path per call (one CUDA stream, captured once in a CUDA graph):
- *   probe kernel   — cosine proxy vs. the cached token-0 key, group mean,
- *                    tau(L) compare  -> route bitmap + compacted active list
- *   decode kernel  — persistent Split-K flash-decode; only Active groups'
- *                    K/V pages are streamed (TMA -> smem ring -> mma.sync
- *                    hi/lo-split bf16, fp32 online softmax)
- *   combine kernel — log-sum-exp merge of the Split-K partials; Sink groups get
- *                    bitwise-zero rows.
+ * Hot path per call: ONE persistent cooperative sm_100a kernel (step.cuh),
+ * replayed from a CUDA graph on the engine stream, in three phases:
+ *   routing — cosine proxy vs. the cached token-0 key (exact fp64, sequential
+ *             sums), group mean, tau(L) compare -> route bitmap + Active list
+ *   stream  — Split-K flash-decode over the Active groups only (TMA -> smem
+ *             ring -> mma.sync hi/lo-split bf16, fp32 online softmax)
+ *   merge   — log-sum-exp merge of the Split-K partials; Sink groups get
+ *             bitwise-zero rows.
+ * The three-kernel form (probe -> decode -> combine) is kept for A/B
+ * profiling (SINKR_FUSED=0), score collection and the multi-rank merge.
  *
  * Threading: an engine is bound to one device and one stream; like the
  * reference's ThreadPool (parallel.hpp:15-18) it must not be driven by two host
@@ -123,6 +125,8 @@ const char* sinkr_version(void);
 sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
                                  sinkr_engine** out);
 sinkr_status sinkr_engine_destroy(sinkr_engine* engine);
+/* The engine's configuration (num_seqs filled in). */
+sinkr_status sinkr_engine_config(sinkr_engine* e, sinkr_cache_config* out);
 /* The engine's CUDA stream (cudaStream_t) — all work is ordered on it. */
 void* sinkr_engine_stream(sinkr_engine* engine);
 
@@ -179,8 +183,9 @@ sinkr_status sinkr_split_ranges(size_t len, size_t num_splits, size_t* from_to);
  *   queries  [B][H_q][D] f32 (read)      outputs [B][H_q][D] f32 (written)
  *   groups   [B][H_kv]                   head_scores [B][H_q] f64
  *   counters summed over the batch (may be NULL).
- * The call copies the queries to the device, runs probe -> decode -> combine
- * and copies the result back (blocking). */
+ * One graph per call: an H2D copy of the queries + step parameters, then the
+ * fused step kernel, which writes outputs and the routing record straight into
+ * mapped pinned host memory (blocking until they are there). */
 sinkr_status sinkr_routed_decode_step(sinkr_engine* e, const float* queries, size_t layer,
                                       const sinkr_routing_config* config,
                                       const sinkr_engine_options* options, float* outputs,
@@ -228,6 +233,105 @@ sinkr_status sinkr_step_io_bytes(sinkr_engine* e, size_t* h2d, size_t* d2h);
 sinkr_status sinkr_set_timing(sinkr_engine* e, int enabled);
 /* Number of SMs / persistent CTAs used by the decode kernel. */
 int sinkr_decode_grid(sinkr_engine* e);
+
+/* ---- calibration (calibration.hpp:14-90, calibration.cpp) --
+ * Host control logic of the reference restated in C++ (bit-identical: same
+ * expression order, no FMA contraction).  Score populations come from the GPU:
+ * sinkr_collect_scores runs the routing phase alone (no KV streaming), so a
+ * calibration sample costs one probe launch instead of a decode step. */
+#define SINKR_MAX_EXCLUDED_LAYERS 32
+#define SINKR_MAX_CALIBRATION_POINTS 64
+typedef struct sinkr_calibration_point { /* CalibrationPoint (calibration.hpp:14-18) */
+    size_t length;
+    double tau;
+    double skip;
+} sinkr_calibration_point;
+typedef struct sinkr_profile { /* ThresholdProfile (calibration.hpp:21-34) */
+    sinkr_threshold_profile threshold; /* coeffs, length_normalizer, clamp */
+    double target_skip;                /* default 0.60 */
+    double gamma;                      /* default 0.65 */
+    size_t excluded_layers[SINKR_MAX_EXCLUDED_LAYERS];
+    size_t num_excluded_layers;        /* default {0, 1} */
+    sinkr_calibration_point points[SINKR_MAX_CALIBRATION_POINTS];
+    size_t num_points;
+} sinkr_profile;
+/* ThresholdProfile{} defaults / ThresholdProfile::constant (calibration.cpp:29-35). */
+void sinkr_profile_default(sinkr_profile* out);
+void sinkr_profile_constant(double tau, sinkr_profile* out);
+/* sweep / skip_ratio_at / solve_threshold (calibration.hpp:52-61). */
+sinkr_status sinkr_sweep(const double* scores, size_t n, const double* thresholds, size_t m,
+                         double* skip_ratios);
+sinkr_status sinkr_skip_ratio_at(const double* scores, size_t n, double threshold, double* out);
+sinkr_status sinkr_solve_threshold(const double* scores, size_t n, double target_skip,
+                                   double* out);
+/* fit_cubic (calibration.hpp:68-70): coeffs a,b,c,d + sum of squared residuals. */
+sinkr_status sinkr_fit_cubic(const double* x, const double* y, size_t n, double* coeffs,
+                             double* residual);
+/* calibrate (calibration.hpp:79-83) over populations the caller collected, one
+ * per entry of `lengths`: population i is samples offsets[i] .. offsets[i+1]-1
+ * of (scores, sample_layers).  As in the reference, each distinct length is
+ * used once (its first population), in ascending order. */
+sinkr_status sinkr_calibrate(const size_t* lengths, size_t n_lengths, const double* scores,
+                             const size_t* sample_layers, const size_t* offsets,
+                             double target_skip, double gamma, const size_t* excluded_layers,
+                             size_t num_excluded_layers, sinkr_profile* out);
+/* save_profile / load_profile (calibration.hpp:85-86): the reference's JSON
+ * schema; files interoperate with the reference's nlohmann-based reader. */
+sinkr_status sinkr_save_profile(const char* path, const sinkr_profile* profile);
+sinkr_status sinkr_load_profile(const char* path, sinkr_profile* out);
+/* Routing-phase-only step (the score-collection mode of SPEC.md:396): proxy
+ * scores of every head and group of all B sequences for `layer`, with routing
+ * decisions under `config` (NULL: none recorded).  Host buffers; blocking.
+ *   head_scores [B][H_q], group_scores [B][H_kv], sink [B][H_kv] (may be NULL). */
+sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t layer,
+                                  const sinkr_routing_config* config, double* head_scores,
+                                  double* group_scores, int32_t* sink);
+
+/* ---- snapshots (kv_cache.hpp:72-80, tensor.hpp:86-96) -----
+ * SNKT tensor files and the snapshot directory layout of the reference
+ * (manifest.json + k_l{layer}_h{head}.snkt / v_...).  K/V are f32 in the
+ * files; the engine stores bf16 (RNE) and captures anchors from the stored
+ * rows.  A snapshot holds one sequence. */
+sinkr_status sinkr_write_tensor(const char* path, const uint64_t* dims, size_t ndim,
+                                const float* data);
+/* Reads the header (dims, ndim <= 64) and, when data != NULL, the payload
+ * (capacity in elements). */
+sinkr_status sinkr_read_tensor(const char* path, uint64_t* dims, size_t* ndim, float* data,
+                               size_t capacity);
+uint64_t sinkr_snkt_file_size(const uint64_t* dims, size_t ndim);
+sinkr_status sinkr_save_snapshot(sinkr_engine* e, size_t seq, const char* dir);
+/* Creates a single-sequence engine on `device` sized by the manifest. */
+sinkr_status sinkr_load_snapshot(const char* dir, int device, sinkr_engine** out);
+/* Replays a snapshot into sequence `seq` of an existing (empty) engine. */
+sinkr_status sinkr_load_snapshot_into(sinkr_engine* e, size_t seq, const char* dir);
+/* Device prefill: f32 rows already on the device, converted to bf16 on the
+ * device; anchor capture as in sinkr_kv_append. */
+sinkr_status sinkr_kv_append_device_f32(sinkr_engine* e, size_t seq, size_t layer,
+                                        size_t kv_head, const float* d_k, const float* d_v,
+                                        size_t rows);
+
+/* ---- analysis (attention.cpp:75-99, analysis.hpp:12-39) ---
+ * Full-attention BOS mass on the GPU for oracle sink labels: for every query
+ * head, alpha0 = softmax(scale * q.K^T)[0] over the whole cached context of
+ * `layer` (one K-only streaming pass).  alpha0: [B][H_q] f64. */
+sinkr_status sinkr_attention_bos_mass(sinkr_engine* e, const float* queries, size_t layer,
+                                      double* alpha0);
+/* attention_weights (attention.cpp:75-99) for one (seq, kv_head) group on the
+ * GPU: weights [r][len] f32 over the slot's cached rows. */
+sinkr_status sinkr_attention_weights(sinkr_engine* e, const float* queries, size_t seq,
+                                     size_t layer, size_t kv_head, float* weights);
+/* oracle labels (analysis.hpp:12-22) from BOS masses: mode 0 = per head
+ * (alpha0 > gamma, strict), mode 1 = group mean over `group` consecutive
+ * heads.  n_heads % group == 0.  Outputs have n_heads (mode 0) or
+ * n_heads / group (mode 1) entries. */
+sinkr_status sinkr_oracle_labels(const double* alpha0, size_t n_heads, size_t group,
+                                 double gamma, int mode, double* label_alpha0,
+                                 uint8_t* is_sink);
+/* pr_curve (analysis.hpp:24-39): operating points at every distinct score
+ * (positive iff score >= threshold), descending; AUPRC by average-precision
+ * step summation.  points: up to n entries of {threshold, precision, recall, f1}. */
+sinkr_status sinkr_pr_curve(const double* scores, const uint8_t* labels, size_t n,
+                            double* points, size_t* num_points, double* auprc);
 
 #ifdef __cplusplus
 } /* extern "C" */

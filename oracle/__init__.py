@@ -222,6 +222,107 @@ class RefLib(_Lib):
                                                    _p(k), C.c_size_t(k.shape[0]), _p(out)))
         return out
 
+    # -- calibration (calibration.hpp:36-90) -----------------------------------
+    def sweep(self, scores, thresholds):
+        s, t = _f64(scores), _f64(thresholds)
+        out = np.zeros(t.size)
+        self._check(self.lib.ref_sweep(_p(s), C.c_size_t(s.size), _p(t), C.c_size_t(t.size), _p(out)))
+        return out
+
+    def skip_ratio_at(self, scores, thr):
+        s = _f64(scores)
+        out = C.c_double()
+        self._check(self.lib.ref_skip_ratio_at(_p(s), C.c_size_t(s.size), C.c_double(thr), C.byref(out)))
+        return out.value
+
+    def solve_threshold(self, scores, target):
+        s = _f64(scores)
+        out = C.c_double()
+        self._check(self.lib.ref_solve_threshold(_p(s), C.c_size_t(s.size), C.c_double(target),
+                                                 C.byref(out)))
+        return out.value
+
+    def fit_cubic(self, x, y):
+        x, y = _f64(x), _f64(y)
+        co = np.zeros(4)
+        res = C.c_double()
+        self._check(self.lib.ref_fit_cubic(_p(x), _p(y), C.c_size_t(x.size), _p(co), C.byref(res)))
+        return co, res.value
+
+    @staticmethod
+    def _profile_dict(f8, ex, nex, pts, npts):
+        return {"coeffs": f8[:4].copy(), "normalizer": f8[4], "lo": f8[5], "hi": f8[6],
+                "target_skip": f8[7], "gamma": f8[8], "excluded": [int(x) for x in ex[:nex]],
+                "points": [(int(pts[3 * i]), pts[3 * i + 1], pts[3 * i + 2]) for i in range(npts)]}
+
+    def calibrate(self, lengths, populations, target, gamma, excluded=(0, 1)):
+        """populations[i] = (scores, layers) for lengths[i]."""
+        ln = np.ascontiguousarray(lengths, dtype=np.uint64)
+        sc = _f64(np.concatenate([np.asarray(p[0], dtype=np.float64) for p in populations]))
+        ly = np.ascontiguousarray(np.concatenate([np.asarray(p[1]) for p in populations]),
+                                  dtype=np.uint64)
+        off = np.ascontiguousarray(np.cumsum([0] + [len(p[0]) for p in populations]), dtype=np.uint64)
+        ex = np.ascontiguousarray(list(excluded) or [0], dtype=np.uint64)
+        f8 = np.zeros(9)
+        exo = np.zeros(64, dtype=np.uint64)
+        pts = np.zeros(3 * 256)
+        nex, npts, calls = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        self._check(self.lib.ref_calibrate(_p(ln), C.c_size_t(ln.size), _p(sc), _p(ly), _p(off),
+                                           C.c_double(target), C.c_double(gamma), _p(ex),
+                                           C.c_size_t(len(excluded)), _p(f8), _p(exo), C.byref(nex),
+                                           _p(pts), C.byref(npts), C.byref(calls)))
+        d = self._profile_dict(f8, exo, nex.value, pts, npts.value)
+        d["collector_calls"] = calls.value
+        return d
+
+    def save_profile(self, path, d):
+        f8 = np.array(list(d["coeffs"]) + [d["normalizer"], d["lo"], d["hi"], d["target_skip"],
+                                           d["gamma"]], dtype=np.float64)
+        ex = np.ascontiguousarray(d["excluded"] or [0], dtype=np.uint64)
+        pts = _f64([x for p in d["points"] for x in p] or [0.0])
+        self._check(self.lib.ref_save_profile(str(path).encode(), _p(f8), _p(ex),
+                                              C.c_size_t(len(d["excluded"])), _p(pts),
+                                              C.c_size_t(len(d["points"]))))
+
+    def load_profile(self, path):
+        f8 = np.zeros(9)
+        exo = np.zeros(64, dtype=np.uint64)
+        pts = np.zeros(3 * 256)
+        nex, npts = C.c_size_t(), C.c_size_t()
+        self._check(self.lib.ref_load_profile(str(path).encode(), _p(f8), _p(exo), C.byref(nex),
+                                              _p(pts), C.byref(npts)))
+        return self._profile_dict(f8, exo, nex.value, pts, npts.value)
+
+    # -- SNKT (tensor.hpp:86-96) ----------------------------------------------------
+    def write_tensor(self, path, arr):
+        a = _f32(arr)
+        dims = np.ascontiguousarray(a.shape, dtype=np.uint64)
+        self._check(self.lib.ref_write_tensor(str(path).encode(), _p(dims), C.c_size_t(dims.size),
+                                              _p(a)))
+
+    def read_tensor(self, path):
+        dims = np.zeros(64, dtype=np.uint64)
+        nd = C.c_size_t()
+        self._check(self.lib.ref_read_tensor(str(path).encode(), _p(dims), C.byref(nd), None,
+                                             C.c_size_t(0)))
+        shape = tuple(int(x) for x in dims[:nd.value])
+        out = np.zeros(shape, dtype=np.float32)
+        self._check(self.lib.ref_read_tensor(str(path).encode(), _p(dims), C.byref(nd), _p(out),
+                                             C.c_size_t(out.size)))
+        return out
+
+    def snkt_file_size(self, dims):
+        d = np.ascontiguousarray(dims, dtype=np.uint64)
+        self.lib.ref_snkt_file_size.restype = C.c_uint64
+        return int(self.lib.ref_snkt_file_size(_p(d), C.c_size_t(d.size)))
+
+    def load_snapshot(self, path, layers, hq, hkv, dim):
+        h = C.c_void_p()
+        self._check(self.lib.ref_cache_load_snapshot(str(path).encode(), C.byref(h)))
+        c = RefCache.__new__(RefCache)
+        c.ref, c.hq, c.hkv, c.dim, c.h = self, hq, hkv, dim, h
+        return c
+
 
 class RefCache:
     """sinkr::KvCache (kv_cache.hpp:42-80) owned by the compiled reference."""
@@ -246,6 +347,21 @@ class RefCache:
         self.ref._check(self.ref.lib.ref_cache_append_rows(
             self.h, C.c_size_t(layer), C.c_size_t(head), _p(k), _p(v),
             C.c_size_t(k.shape[0])))
+
+    def save_snapshot(self, path):
+        self.ref._check(self.ref.lib.ref_cache_save_snapshot(self.h, str(path).encode()))
+
+    def token_count(self):
+        n = C.c_size_t()
+        self.ref._check(self.ref.lib.ref_cache_token_count(self.h, C.byref(n)))
+        return n.value
+
+    def historical(self, layer, head, frm, to):
+        k = np.zeros((to - frm, self.dim), dtype=np.float32)
+        v = np.zeros((to - frm, self.dim), dtype=np.float32)
+        self.ref._check(self.ref.lib.ref_cache_historical(self.h, C.c_size_t(layer), C.c_size_t(head),
+                                                          C.c_size_t(frm), C.c_size_t(to), _p(k), _p(v)))
+        return k, v
 
     def anchor(self, layer, head):
         k0 = np.zeros(self.dim, dtype=np.float32)

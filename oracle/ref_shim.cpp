@@ -23,6 +23,7 @@
 #include "sinkr/kv_cache.hpp"
 #include "sinkr/parallel.hpp"
 #include "sinkr/router.hpp"
+#include "sinkr/tensor.hpp"
 
 namespace {
 
@@ -298,6 +299,152 @@ int ref_routed_decode_step(void* c, const float* queries, std::size_t layer,
         seconds[0] = r.counters.routing_seconds;
         seconds[1] = r.counters.attention_seconds;
         seconds[2] = r.counters.merge_seconds;
+    });
+}
+
+// ---- calibration (calibration.hpp:36-90) -------------------------------------
+namespace {
+sinkr::ScorePopulation pop_of(const double* s, const std::size_t* layers, std::size_t n,
+                              std::size_t length) {
+    sinkr::ScorePopulation p;
+    for (std::size_t i = 0; i < n; ++i) p.add(s[i], layers ? layers[i] : 0, length);
+    return p;
+}
+// profile <-> flat arrays: coeffs[4], norm, lo, hi, target, gamma | excluded | points (len,tau,skip)
+void profile_out(const sinkr::ThresholdProfile& p, double* f8, std::size_t* excluded,
+                 std::size_t* n_excl, double* points, std::size_t* n_points) {
+    for (int i = 0; i < 4; ++i) f8[i] = p.coeffs[i];
+    f8[4] = p.length_normalizer;
+    f8[5] = p.clamp_lo;
+    f8[6] = p.clamp_hi;
+    f8[7] = p.target_skip;
+    f8[8] = p.gamma;
+    *n_excl = p.excluded_layers.size();
+    for (std::size_t i = 0; i < p.excluded_layers.size(); ++i) excluded[i] = p.excluded_layers[i];
+    *n_points = p.points.size();
+    for (std::size_t i = 0; i < p.points.size(); ++i) {
+        points[3 * i] = (double)p.points[i].length;
+        points[3 * i + 1] = p.points[i].tau;
+        points[3 * i + 2] = p.points[i].skip;
+    }
+}
+}  // namespace
+
+int ref_sweep(const double* s, std::size_t n, const double* t, std::size_t m, double* out) {
+    return guard([&] {
+        const auto r = sinkr::sweep(pop_of(s, nullptr, n, 0), std::span<const double>(t, m));
+        for (std::size_t i = 0; i < r.size(); ++i) out[i] = r[i].second;
+    });
+}
+
+int ref_skip_ratio_at(const double* s, std::size_t n, double t, double* out) {
+    return guard([&] { *out = sinkr::skip_ratio_at(pop_of(s, nullptr, n, 0), t); });
+}
+
+int ref_solve_threshold(const double* s, std::size_t n, double target, double* out) {
+    return guard([&] { *out = sinkr::solve_threshold(pop_of(s, nullptr, n, 0), target); });
+}
+
+int ref_fit_cubic(const double* x, const double* y, std::size_t n, double* coeffs,
+                  double* residual) {
+    return guard([&] {
+        std::vector<std::pair<double, double>> pts;
+        for (std::size_t i = 0; i < n; ++i) pts.emplace_back(x[i], y[i]);
+        const auto f = sinkr::fit_cubic(pts);
+        for (int i = 0; i < 4; ++i) coeffs[i] = f.coeffs[i];
+        *residual = f.residual;
+    });
+}
+
+// calibrate with a collector replaying caller-given populations (one per length)
+int ref_calibrate(const std::size_t* lengths, std::size_t n_lengths, const double* scores,
+                  const std::size_t* layers, const std::size_t* offsets, double target,
+                  double gamma, const std::size_t* excluded, std::size_t n_excl, double* f8,
+                  std::size_t* excl_out, std::size_t* n_excl_out, double* points,
+                  std::size_t* n_points, std::size_t* calls) {
+    return guard([&] {
+        *calls = 0;
+        sinkr::ScoreCollector collect = [&](std::size_t len) {
+            ++*calls;
+            for (std::size_t i = 0; i < n_lengths; ++i)
+                if (lengths[i] == len)
+                    return pop_of(scores + offsets[i], layers + offsets[i],
+                                  offsets[i + 1] - offsets[i], len);
+            return sinkr::ScorePopulation{};
+        };
+        const auto p = sinkr::calibrate(collect, std::span<const std::size_t>(lengths, n_lengths),
+                                        target, gamma,
+                                        std::vector<std::size_t>(excluded, excluded + n_excl));
+        profile_out(p, f8, excl_out, n_excl_out, points, n_points);
+    });
+}
+
+int ref_save_profile(const char* path, const double* f8, const std::size_t* excluded,
+                     std::size_t n_excl, const double* points, std::size_t n_points) {
+    return guard([&] {
+        sinkr::ThresholdProfile p;
+        for (int i = 0; i < 4; ++i) p.coeffs[i] = f8[i];
+        p.length_normalizer = f8[4];
+        p.clamp_lo = f8[5];
+        p.clamp_hi = f8[6];
+        p.target_skip = f8[7];
+        p.gamma = f8[8];
+        p.excluded_layers.assign(excluded, excluded + n_excl);
+        for (std::size_t i = 0; i < n_points; ++i)
+            p.points.push_back({(std::size_t)points[3 * i], points[3 * i + 1], points[3 * i + 2]});
+        sinkr::save_profile(path, p);
+    });
+}
+
+int ref_load_profile(const char* path, double* f8, std::size_t* excluded, std::size_t* n_excl,
+                     double* points, std::size_t* n_points) {
+    return guard([&] { profile_out(sinkr::load_profile(path), f8, excluded, n_excl, points, n_points); });
+}
+
+// ---- SNKT + snapshots (tensor.hpp:86-96, kv_cache.hpp:72-80) -----------------
+int ref_write_tensor(const char* path, const std::uint64_t* dims, std::size_t ndim,
+                     const float* data) {
+    return guard([&] {
+        sinkr::Tensor t;
+        t.dims.assign(dims, dims + ndim);
+        t.data.assign(data, data + sinkr::element_count(t.dims));
+        sinkr::write_tensor(path, t);
+    });
+}
+
+int ref_read_tensor(const char* path, std::uint64_t* dims, std::size_t* ndim, float* data,
+                    std::size_t capacity) {
+    return guard([&] {
+        const auto t = sinkr::read_tensor(path);
+        *ndim = t.dims.size();
+        for (std::size_t i = 0; i < t.dims.size(); ++i) dims[i] = t.dims[i];
+        if (data) {
+            if (t.data.size() > capacity) throw std::invalid_argument("buffer too small");
+            std::memcpy(data, t.data.data(), t.data.size() * sizeof(float));
+        }
+    });
+}
+
+std::uint64_t ref_snkt_file_size(const std::uint64_t* dims, std::size_t ndim) {
+    return sinkr::snkt_file_size(std::span<const std::uint64_t>(dims, ndim));
+}
+
+int ref_cache_save_snapshot(void* c, const char* dir) {
+    return guard([&] { static_cast<sinkr::KvCache*>(c)->save_snapshot(dir); });
+}
+
+int ref_cache_load_snapshot(const char* dir, void** out) {
+    return guard([&] { *out = new sinkr::KvCache(sinkr::KvCache::load_snapshot(dir)); });
+}
+
+int ref_cache_historical(void* c, std::size_t layer, std::size_t head, std::size_t from,
+                         std::size_t to, float* k, float* v) {
+    return guard([&] {
+        auto* cache = static_cast<sinkr::KvCache*>(c);
+        sinkr::LoadCounters ctr;
+        const auto h = cache->historical(layer, head, from, to, ctr);
+        std::memcpy(k, h.k.data(), h.k.size() * sizeof(float));
+        std::memcpy(v, h.v.data(), h.v.size() * sizeof(float));
     });
 }
 

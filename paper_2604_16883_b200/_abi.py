@@ -50,6 +50,22 @@ class GroupInfoC(C.Structure):
                 ("kv_floats_loaded", C.c_uint64), ("tokens_loaded", C.c_uint64)]
 
 
+class CalibrationPointC(C.Structure):
+    _fields_ = [("length", c_size_t), ("tau", C.c_double), ("skip", C.c_double)]
+
+
+MAX_EXCLUDED_LAYERS = 32
+MAX_CALIBRATION_POINTS = 64
+
+
+class ProfileC(C.Structure):
+    _fields_ = [("threshold", ThresholdProfileC), ("target_skip", C.c_double),
+                ("gamma", C.c_double), ("excluded_layers", c_size_t * MAX_EXCLUDED_LAYERS),
+                ("num_excluded_layers", c_size_t),
+                ("points", CalibrationPointC * MAX_CALIBRATION_POINTS),
+                ("num_points", c_size_t)]
+
+
 # sinkr_status -> the Python analogue of the reference's exception classes
 SINKR_OK = 0
 _EXC = {
@@ -82,7 +98,17 @@ EXPORTS = (
     "sinkr_routed_decode_batch", "sinkr_routed_decode_async", "sinkr_fetch_step_info",
     "sinkr_rank_partial_floats", "sinkr_decode_rank_partial_async",
     "sinkr_merge_rank_partials_async", "sinkr_last_step_stats", "sinkr_set_timing",
-    "sinkr_decode_grid", "sinkr_step_io_bytes",
+    "sinkr_decode_grid", "sinkr_step_io_bytes", "sinkr_engine_config",
+    # calibration (f1)
+    "sinkr_profile_default", "sinkr_profile_constant", "sinkr_sweep", "sinkr_skip_ratio_at",
+    "sinkr_solve_threshold", "sinkr_fit_cubic", "sinkr_calibrate", "sinkr_save_profile",
+    "sinkr_load_profile", "sinkr_collect_scores",
+    # snapshots / device prefill (f2)
+    "sinkr_write_tensor", "sinkr_read_tensor", "sinkr_snkt_file_size", "sinkr_save_snapshot",
+    "sinkr_load_snapshot", "sinkr_load_snapshot_into", "sinkr_kv_append_device_f32",
+    # analysis (f4)
+    "sinkr_attention_bos_mass", "sinkr_attention_weights", "sinkr_oracle_labels",
+    "sinkr_pr_curve",
 )
 
 _lib = None
@@ -108,6 +134,38 @@ def lib():
         L.sinkr_decode_grid.restype = C.c_int
         L.sinkr_decode_grid.argtypes = [C.c_void_p]
         L.sinkr_engine_destroy.argtypes = [C.c_void_p]
+        L.sinkr_snkt_file_size.restype = C.c_uint64
+        L.sinkr_snkt_file_size.argtypes = [C.c_void_p, c_size_t]
+        L.sinkr_profile_default.restype = None
+        L.sinkr_profile_constant.restype = None
+        L.sinkr_profile_constant.argtypes = [C.c_double, C.c_void_p]
+        for name in ("sinkr_skip_ratio_at", "sinkr_solve_threshold"):
+            getattr(L, name).argtypes = [C.c_void_p, c_size_t, C.c_double, C.c_void_p]
+        L.sinkr_calibrate.argtypes = [C.c_void_p, c_size_t, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_double, C.c_double, C.c_void_p, c_size_t, C.c_void_p]
+        L.sinkr_oracle_labels.argtypes = [C.c_void_p, c_size_t, c_size_t, C.c_double, C.c_int,
+                                          C.c_void_p, C.c_void_p]
+        vp, sz = C.c_void_p, c_size_t
+        for name, at in {
+            "sinkr_sweep": [vp, sz, vp, sz, vp],
+            "sinkr_fit_cubic": [vp, vp, sz, vp, vp],
+            "sinkr_save_profile": [C.c_char_p, vp],
+            "sinkr_load_profile": [C.c_char_p, vp],
+            "sinkr_profile_default": [vp],
+            "sinkr_collect_scores": [vp, vp, sz, vp, vp, vp, vp],
+            "sinkr_write_tensor": [C.c_char_p, vp, sz, vp],
+            "sinkr_read_tensor": [C.c_char_p, vp, vp, vp, sz],
+            "sinkr_save_snapshot": [vp, sz, C.c_char_p],
+            "sinkr_load_snapshot": [C.c_char_p, C.c_int, vp],
+            "sinkr_load_snapshot_into": [vp, sz, C.c_char_p],
+            "sinkr_kv_append_device_f32": [vp, sz, sz, sz, vp, vp, sz],
+            "sinkr_engine_config": [vp, vp],
+            "sinkr_attention_bos_mass": [vp, vp, sz, vp],
+            "sinkr_attention_weights": [vp, vp, sz, sz, sz, vp],
+            "sinkr_pr_curve": [vp, vp, sz, vp, vp, vp],
+        }.items():
+            getattr(L, name).argtypes = at
+            getattr(L, name).restype = C.c_int if name != "sinkr_profile_default" else None
         _lib = L
     return _lib
 

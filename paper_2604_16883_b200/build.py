@@ -28,7 +28,13 @@ def nvcc() -> str:
 
 def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
-                  if f.endswith((".cu", ".cuh", ".h")))
+                  if f.endswith((".cu", ".cuh", ".h", ".hpp", ".cpp")))
+
+
+def translation_units():
+    """engine.cu (device kernels + the engine) and the host-only C++ units
+    (calibration, snapshots, analysis) — all linked into one library."""
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
 def up_to_date() -> bool:
@@ -48,7 +54,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
            "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
            "-Xptxas", "-v" if verbose else "-O3",
            "-shared", "-I", os.path.join(ROOT, "include"),
-           os.path.join(CSRC, "engine.cu"), "-o", LIB + ".tmp"]
+           *translation_units(), "-o", LIB + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

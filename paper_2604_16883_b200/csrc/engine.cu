@@ -19,20 +19,17 @@
 #include <vector>
 
 #include "../../include/sinkr_cuda.h"
+#include "host_util.hpp"
 #include "step.cuh"
+#include "analysis.cuh"
 
 namespace {
 
 using namespace sinkr;
-
-thread_local std::string g_err;
-
-struct Error {
-    sinkr_status code;
-    std::string msg;
-};
-
-[[noreturn]] void fail(sinkr_status code, const std::string& msg) { throw Error{code, msg}; }
+using sinkr::host::Error;
+using sinkr::host::fail;
+using sinkr::host::g_err;
+using sinkr::host::guard;
 
 #define CK(x)                                                                          \
     do {                                                                               \
@@ -40,23 +37,6 @@ struct Error {
         if (e_ != cudaSuccess)                                                         \
             fail(SINKR_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_));    \
     } while (0)
-
-template <class F>
-sinkr_status guard(F&& f) {
-    try {
-        f();
-        return SINKR_OK;
-    } catch (const Error& e) {
-        g_err = e.msg;
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return SINKR_RUNTIME_ERROR;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return SINKR_RUNTIME_ERROR;
-    }
-}
 
 // f32 -> bf16 round-to-nearest-even (bit-identical to __float2bfloat16_rn for
 // finite inputs and to oracle/sinkr_oracle.c:orc_round_bf16).
@@ -919,6 +899,40 @@ sinkr_status sinkr_kv_append_device_bf16(sinkr_engine* e, size_t seq, size_t lay
     });
 }
 
+sinkr_status sinkr_kv_append_device_f32(sinkr_engine* e, size_t seq, size_t layer,
+                                        size_t kv_head, const float* d_k, const float* d_v,
+                                        size_t rows) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        check_slot(e, seq, layer, kv_head);
+        if (rows == 0) return;
+        if (!d_k || !d_v) fail(SINKR_INVALID_ARGUMENT, "k/v row size does not match head_dim");
+        const size_t idx = e->slot_index(layer, seq, kv_head), D = e->D;
+        if (e->len[idx] + rows > e->cap)
+            fail(SINKR_RUNTIME_ERROR,
+                 "kv cache overflow: slot at capacity " + std::to_string(e->cap));
+        if ((reinterpret_cast<uintptr_t>(d_k) | reinterpret_cast<uintptr_t>(d_v)) & 15)
+            fail(SINKR_INVALID_ARGUMENT, "device rows must be 16-byte aligned");
+        const size_t off = (e->row_base(layer, seq, kv_head) + e->len[idx]) * D;
+        const size_t n = rows * D;
+        const int grid = (int)std::min<size_t>((n / 4 + 255) / 256 + 1, (size_t)e->num_sms * 8);
+        dev::f32_to_bf16_kernel<<<grid, 256, 0, e->stream>>>(d_k, e->d_k + off, n);
+        dev::f32_to_bf16_kernel<<<grid, 256, 0, e->stream>>>(d_v, e->d_v + off, n);
+        CK(cudaGetLastError());
+        if (e->len[idx] == 0) capture_anchor_device(e, idx);
+        CK(cudaStreamSynchronize(e->stream));
+        e->len[idx] += rows;
+    });
+}
+
+sinkr_status sinkr_engine_config(sinkr_engine* e, sinkr_cache_config* out) {
+    return guard([&] {
+        if (!e || !out) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        *out = e->cfg;
+        out->num_seqs = e->B;
+    });
+}
+
 sinkr_status sinkr_kv_append_synthetic(sinkr_engine* e, size_t seq, size_t layer,
                                        size_t kv_head, uint64_t key_k, uint64_t key_v,
                                        float k_scale, float v_scale, size_t global_row0,
@@ -1131,6 +1145,152 @@ sinkr_status sinkr_fetch_step_info(sinkr_engine* e, sinkr_group_info* groups,
             check_error_flag(e);
         const auto* hdr = reinterpret_cast<const dev::StepHdr*>(e->h_in);
         fill_info(e, hdr->layer, nullptr, groups, head_scores, counters, nullptr);
+    });
+}
+
+// Score-collection mode (calibration.hpp:74-76): the routing
+// phase alone — the probe kernel scores every head and group and records the
+// decisions, no K/V row is streamed.  Calibration populations therefore cost
+// one small launch per sample instead of a full decode step.
+sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t layer,
+                                  const sinkr_routing_config* config, double* head_scores,
+                                  double* group_scores, int32_t* sink) {
+    return guard([&] {
+        if (!e || !queries) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        sinkr_routing_config none{};
+        none.profile.coeffs[3] = 2.0;  // ThresholdProfile::constant(2.0): nothing sinks
+        none.profile.length_normalizer = 1.0;
+        none.profile.clamp_lo = 0.0;
+        none.profile.clamp_hi = 2.0;
+        stage_params(e, layer, config ? config : &none, nullptr, true);
+        const size_t NH = e->B * e->cfg.num_q_heads;
+        std::memcpy(e->h_in + e->off_q, queries, NH * e->D * 4);
+        CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaEventRecord(e->ev_in, e->stream));
+        const dev::DevTables t = e->tables(reinterpret_cast<const float*>(e->d_in + e->off_q));
+        switch (e->D) {
+            case 32: dev::probe_kernel<32><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+            case 64: dev::probe_kernel<64><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+            default: dev::probe_kernel<128><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+        }
+        CK(cudaGetLastError());
+        // head scores, group scores and flags are contiguous in the result block
+        CK(cudaMemcpyAsync(e->h_res + e->off_hs, e->d_res + e->off_hs, e->off_status - e->off_hs,
+                           cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        const auto* hs = reinterpret_cast<const double*>(e->h_res + e->off_hs);
+        const auto* gs = reinterpret_cast<const double*>(e->h_res + e->off_gs);
+        const auto* fl = reinterpret_cast<const uint32_t*>(e->h_res + e->off_fl);
+        if (head_scores) std::memcpy(head_scores, hs, NH * sizeof(double));
+        if (group_scores) std::memcpy(group_scores, gs, e->U * sizeof(double));
+        if (sink)
+            for (size_t u = 0; u < e->U; ++u) sink[u] = (config && (fl[u] & dev::kSink)) ? 1 : 0;
+    });
+}
+
+// Full-attention BOS mass (analysis.cuh).  Queries are staged in the input
+// block's query area; the scratch is allocated per call (analysis path).
+static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size_t q_offset,
+                    size_t layer, uint32_t u_first, uint32_t n_units, double* alpha0,
+                    float* weights) {
+    if (layer >= e->layers) fail(SINKR_OUT_OF_RANGE, "layer index out of range");
+    const size_t U = e->U, r = e->r, D = e->D;
+    std::vector<uint32_t> lens(U);
+    uint32_t max_len = 0;
+    for (size_t u = u_first; u < u_first + n_units; ++u) {
+        const size_t L = e->len[layer * U + u];
+        if (L == 0) fail(SINKR_RUNTIME_ERROR, "attention over an empty cache slot");
+        lens[u] = (uint32_t)L;
+        max_len = std::max<uint32_t>(max_len, (uint32_t)L);
+    }
+    uint32_t chunks = (uint32_t)std::max<size_t>(1, (4 * (size_t)e->num_sms + n_units - 1) / n_units);
+    chunks = std::min<uint32_t>(chunks, std::max<uint32_t>(1, (max_len + 255) / 256));
+    // scratch: len[U] | part[U][chunks][r][2] | z0[U*r] | stats[U*r][2] | alpha0[U*r] f64 | weights
+    const size_t off_part = align_up(U * 4, 256);
+    const size_t off_z0 = align_up(off_part + U * chunks * r * 2 * 4, 256);
+    const size_t off_st = align_up(off_z0 + U * r * 4, 256);
+    const size_t off_a0 = align_up(off_st + U * r * 2 * 4, 256);
+    const size_t off_w = align_up(off_a0 + U * r * 8, 256);
+    const size_t wbytes = weights ? r * (size_t)max_len * 4 : 0;
+    uint8_t* scratch = nullptr;
+    CK(cudaMalloc(&scratch, off_w + wbytes));
+    try {
+        CK(cudaEventSynchronize(e->ev_in));  // the input block is free
+        std::memcpy(e->h_in + e->off_q + q_offset * 4, queries, q_floats * 4);
+        CK(cudaMemcpyAsync(e->d_in + e->off_q + q_offset * 4, e->h_in + e->off_q + q_offset * 4,
+                           q_floats * 4, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(scratch, lens.data(), U * 4, cudaMemcpyHostToDevice, e->stream));
+        dev::BosArgs a{};
+        a.k = e->d_k;
+        a.q = reinterpret_cast<const float*>(e->d_in + e->off_q);
+        a.len = reinterpret_cast<const uint32_t*>(scratch);
+        a.part = reinterpret_cast<float*>(scratch + off_part);
+        a.z0 = reinterpret_cast<float*>(scratch + off_z0);
+        a.stats = reinterpret_cast<float*>(scratch + off_st);
+        a.alpha0 = reinterpret_cast<double*>(scratch + off_a0);
+        a.weights = reinterpret_cast<float*>(scratch + off_w);
+        a.U = (uint32_t)U;
+        a.r = (uint32_t)r;
+        a.Hkv = (uint32_t)e->cfg.num_kv_heads;
+        a.cap = (uint32_t)e->cap;
+        a.chunks = chunks;
+        a.slot0 = (uint32_t)(layer * U);
+        a.u_first = u_first;
+        a.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
+        for (uint32_t h0 = 0; h0 < r; h0 += dev::kBosHeads) {
+            const dim3 g(chunks, n_units);
+            switch (D) {
+                case 32: dev::bos_partial_kernel<32><<<g, dev::kBosThreads, 0, e->stream>>>(a, h0); break;
+                case 64: dev::bos_partial_kernel<64><<<g, dev::kBosThreads, 0, e->stream>>>(a, h0); break;
+                default: dev::bos_partial_kernel<128><<<g, dev::kBosThreads, 0, e->stream>>>(a, h0); break;
+            }
+        }
+        const uint32_t nh = n_units * (uint32_t)r;
+        dev::bos_finish_kernel<<<(nh + 127) / 128, 128, 0, e->stream>>>(a, n_units);
+        if (weights) {
+            const dim3 g(std::min<uint32_t>((max_len + dev::kBosThreads - 1) / dev::kBosThreads,
+                                            8u * (uint32_t)e->num_sms),
+                         (uint32_t)((r + dev::kBosHeads - 1) / dev::kBosHeads));
+            switch (D) {
+                case 32: dev::weights_kernel<32><<<g, dev::kBosThreads, 0, e->stream>>>(a); break;
+                case 64: dev::weights_kernel<64><<<g, dev::kBosThreads, 0, e->stream>>>(a); break;
+                default: dev::weights_kernel<128><<<g, dev::kBosThreads, 0, e->stream>>>(a); break;
+            }
+        }
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(alpha0, scratch + off_a0 + (size_t)u_first * r * 8, (size_t)nh * 8,
+                           cudaMemcpyDeviceToHost, e->stream));
+        if (weights)
+            CK(cudaMemcpyAsync(weights, scratch + off_w, wbytes, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+    } catch (...) {
+        cudaStreamSynchronize(e->stream);
+        cudaFree(scratch);
+        throw;
+    }
+    CK(cudaFree(scratch));
+}
+
+sinkr_status sinkr_attention_bos_mass(sinkr_engine* e, const float* queries, size_t layer,
+                                      double* alpha0) {
+    return guard([&] {
+        if (!e || !queries || !alpha0) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        const size_t nq = e->B * e->cfg.num_q_heads * e->D;
+        run_bos(e, queries, nq, 0, layer, 0, (uint32_t)e->U, alpha0, nullptr);
+    });
+}
+
+sinkr_status sinkr_attention_weights(sinkr_engine* e, const float* queries, size_t seq,
+                                     size_t layer, size_t kv_head, float* weights) {
+    return guard([&] {
+        if (!e || !queries || !weights) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        check_slot(e, seq, layer, kv_head);
+        CK(cudaSetDevice(e->device));
+        const uint32_t u = (uint32_t)(seq * e->cfg.num_kv_heads + kv_head);
+        std::vector<double> a0(e->r);
+        run_bos(e, queries, e->r * e->D, (size_t)u * e->r * e->D, layer, u, 1, a0.data(), weights);
     });
 }
 

@@ -724,6 +724,24 @@ __global__ void anchor_capture_kernel(const __nv_bfloat16* __restrict__ row, uin
     *k0_norm = (float)n;
 }
 
+// device prefill: f32 rows -> bf16 (RNE) slot rows, 4 elements per thread
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                   size_t n) {
+    const size_t n4 = n / 4;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const float4 x = reinterpret_cast<const float4*>(src)[i];
+        __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&a);
+        pk.y = *reinterpret_cast<uint32_t*>(&b);
+        reinterpret_cast<uint2*>(dst)[i] = pk;
+    }
+    for (size_t i = n4 * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
 // synthetic rows: value = bf16(scale * gauss12(key, row*D + j)), the exact
 // restatement of oracle/sinkr_oracle.c:orc_fill_rows (counter-based access to
 // the reference's SplitMix64 stream, tensor.hpp:15-25).

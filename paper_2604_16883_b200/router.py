@@ -301,6 +301,40 @@ class KvCache:
                                         C.c_size_t(kv_head), k0.ctypes.data_as(C.c_void_p),
                                         C.c_float(k0_norm)))
 
+    def append_device_f32(self, layer: int, kv_head: int, k_ptr: int, v_ptr: int, rows: int,
+                          seq: int = 0) -> None:
+        """Device prefill: f32 rows already in device memory, converted to bf16
+        on the device (16-byte aligned pointers)."""
+        check(lib().sinkr_kv_append_device_f32(self._h, C.c_size_t(seq), C.c_size_t(layer),
+                                               C.c_size_t(kv_head), C.c_void_p(k_ptr),
+                                               C.c_void_p(v_ptr), C.c_size_t(rows)))
+
+    # -- snapshots (kv_cache.hpp:72-80; SNKT files + manifest.json)
+    def save_snapshot(self, directory, seq: int = 0) -> None:
+        """KvCache::save_snapshot for sequence `seq` (kv_cache.cpp:123-153)."""
+        check(lib().sinkr_save_snapshot(self._h, C.c_size_t(seq), str(directory).encode()))
+
+    def load_snapshot_into(self, directory, seq: int = 0) -> None:
+        """Replays a snapshot into sequence `seq` of this (empty) cache."""
+        check(lib().sinkr_load_snapshot_into(self._h, C.c_size_t(seq), str(directory).encode()))
+
+    @staticmethod
+    def load_snapshot(directory, device: int = 0) -> "KvCache":
+        """KvCache::load_snapshot (kv_cache.cpp:155-191): a single-sequence
+        cache sized by the manifest, rows replayed on the device."""
+        h = C.c_void_p()
+        check(lib().sinkr_load_snapshot(str(directory).encode(), C.c_int(device), C.byref(h)))
+        cc = _abi.CacheConfigC()
+        check(lib().sinkr_engine_config(h, C.byref(cc)))
+        self = KvCache.__new__(KvCache)
+        self._h = h
+        self._config = CacheConfig(cc.num_layers, cc.num_q_heads, cc.num_kv_heads, cc.head_dim,
+                                   cc.capacity, cc.num_seqs)
+        self.device = device
+        self.B = cc.num_seqs
+        self._keep = []
+        return self
+
     def historical(self, layer: int, kv_head: int, frm: int, to: int, seq: int = 0):
         """Rows [frm, to) of K and V as f32 (exact upcast of the stored bf16)."""
         d = self._config.head_dim

@@ -6,6 +6,8 @@
 #include <stdexcept>
 #include <vector>
 
+#include "sinkr/cuda/analysis.hpp"
+#include "sinkr/cuda/calibration.hpp"
 #include "sinkr/cuda/router.hpp"
 
 namespace sc = sinkr::cuda;
@@ -80,6 +82,57 @@ int main() {
     REQUIRE(sr[1].first == 4 && sr[1].second == 7);
     REQUIRE(sc::threshold_for_length(5, sc::ThresholdProfile{{1, 0, 0, 0}, 10.0, 0.0, 1.0}) ==
             0.125);
+
+    // calibration.hpp: a collector over the GPU's routing-phase-only scores
+    std::fprintf(stderr, "calibrate\n");
+    const std::vector<std::size_t> lens{100, 200, 400, 600, 777};
+    std::vector<std::size_t> seen;
+    auto collect = [&](std::size_t len) {
+        seen.push_back(len);
+        sc::ScorePopulation pop;
+        std::normal_distribution<float> shift(0.02f * (float)len / 100.0f, 1.0f);
+        for (int sample = 0; sample < 8; ++sample) {
+            std::vector<float> qs(hq * D);
+            for (auto& x : qs) x = shift(rng);
+            for (double g : sc::collect_group_scores(cache, qs, 1)) pop.add(g, 1, len);
+        }
+        return pop;
+    };
+    auto prof = sc::calibrate(collect, lens, 0.6, 0.65, {0});
+    REQUIRE(seen == lens && prof.points.size() == lens.size());
+    REQUIRE(prof.length_normalizer == 777.0);
+    const auto path = std::filesystem::temp_directory_path() / "sinkr_shim_profile.json";
+    sc::save_profile(path, prof);
+    const auto back = sc::load_profile(path);
+    REQUIRE(back.coeffs == prof.coeffs && back.points.size() == prof.points.size());
+    REQUIRE(throws<std::invalid_argument>([&] {
+        sc::calibrate(collect, std::vector<std::size_t>{1, 2, 3}, 0.6, 0.65);
+    }));
+
+    // analysis.hpp: GPU BOS mass, oracle labels, PR curve
+    const auto a0 = sc::attention_bos_mass(cache, q, 1);
+    for (double a : a0) REQUIRE(a > 0.0 && a < 1.0);
+    const auto w = sc::attention_weights(cache, std::span<const float>(q.data(), 4 * D), 1, 0);
+    REQUIRE(w.size() == 4 * L && std::fabs(w[0] - a0[0]) < 1e-6);
+    const auto labs = sc::oracle_labels(w, 4, L, 0.65, sc::OracleMode::GroupMean);
+    REQUIRE(labs.size() == 1 && !labs[0].is_sink);
+    const std::vector<double> sco{0.9, 0.8, 0.3, 0.1};
+    const std::vector<std::uint8_t> lab{1, 1, 0, 0};
+    REQUIRE(sc::pr_curve(sco, lab).auprc == 1.0);
+
+    // kv_cache.hpp:72-80: snapshot round trip
+    std::fprintf(stderr, "snapshot\n");
+    const auto dir = std::filesystem::temp_directory_path() / "sinkr_shim_snapshot";
+    cache.save_snapshot(dir);
+    auto loaded = sc::KvCache::load_snapshot(dir);
+    REQUIRE(loaded.token_count() == L && loaded.config().num_layers == 2);
+    REQUIRE(loaded.historical(1, 5, 0, L).first == cache.historical(1, 5, 0, L).first);
+    auto r2 = sc::routed_decode_step(q, 1, loaded, cfg);
+    float md = 0.0f;  // Split-K partials merge in claim order: equal within tolerance
+    for (std::size_t i = 0; i < r.outputs.size(); ++i) md = std::fmax(md, std::fabs(r2.outputs[i] - r.outputs[i]));
+    REQUIRE(md <= 1e-5f);
+    std::filesystem::remove_all(dir);
+    std::filesystem::remove(path);
     std::printf("shim OK (%.1f us attention)\n", r.counters.attention_seconds * 1e6);
     return 0;
 }
