@@ -128,6 +128,7 @@ struct sinkr_engine {
     dev::StepState* d_ss = nullptr;
     uint32_t* d_cursor = nullptr;
     uint32_t* d_tokens_done = nullptr;
+    uint32_t* d_route_flags = nullptr;  // distributed routing decisions [U]
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
 
     CUtensorMap tmk{}, tmv{};
@@ -208,6 +209,7 @@ struct sinkr_engine {
         t.cursor = d_cursor;
         t.slot_count = d_slot_count;
         t.tokens_done = d_tokens_done;
+        t.route_flags = d_route_flags;
         t.partials = d_partials;
         t.out = out;
         t.B = (uint32_t)B;
@@ -715,6 +717,7 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMalloc(&e->d_cursor, e->U * 4));
             CK(cudaMemsetAsync(e->d_cursor, 0, e->U * 4, e->stream));
             CK(cudaMalloc(&e->d_tokens_done, e->U * 4));
+            CK(cudaMalloc(&e->d_route_flags, e->U * 4));
             CK(cudaMemsetAsync(e->d_tokens_done, 0, e->U * 4, e->stream));
             if (const char* tr = std::getenv("SINKR_TRACE"); tr && tr[0] == '1') {
                 CK(cudaMalloc(&e->d_trace, e->grid * 8 * 8));
@@ -806,6 +809,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_tmap);
     cudaFree(e->d_cursor);
     cudaFree(e->d_tokens_done);
+    cudaFree(e->d_route_flags);
     cudaFree(e->d_head_degen);
     cudaFree(e->d_active);
     cudaFree(e->d_prefix);

@@ -9,8 +9,8 @@
 //            memory.  No inter-CTA traffic; CTA 0 publishes the routing record.
 //   phase S  Split-K flash-decode (attend_chunk, attention.cpp:101-142) over the
 //            Active groups only: TMA producer warp + 4 mma.sync consumer warps
-//            per CTA, unit-affine dynamic chunk claims (or one flat cursor when
-//            there are more Active groups than SMs).
+//            per CTA, unit-affine dynamic chunk claims (or guided claims over
+//            one global token space when there are more Active groups than SMs).
 //   phase M  LSE merge (merge_partials, attention.cpp:159-183): with few Active
 //            groups the (group, head, 32-dim) merge tasks are spread over all
 //            CTAs once a group's last row has been streamed; with many groups
@@ -29,13 +29,15 @@ constexpr int kMaxUnits = 1280;      // B * H_kv per step (LLaVA-13B B=32 x 40)
 constexpr int kMaxStepHeads = 4096;  // B * H_q per step
 constexpr int kRouteTile = 64;       // heads per routing tile
 constexpr int kRouteSub = 32;        // heads per load batch
+constexpr uint32_t kFlatMinTok = 512;  // smallest claim of the global token-space scheduler
 
 struct StepState {
     unsigned int flat_counter;
     unsigned int merge_next;
     unsigned int exit_count;
     unsigned int error;
-    unsigned int pad[4];
+    unsigned int route_done;  // CTAs that published their units' decisions (distributed routing)
+    unsigned int pad[3];
 };
 
 struct StepTables {
@@ -52,6 +54,7 @@ struct StepTables {
     double* head_scores;           // result [B*Hq]
     double* group_scores;          // result [U]
     uint32_t* unit_flags;          // result [U]
+    uint32_t* route_flags;         // [U] device scratch: decisions for the distributed routing
     unsigned long long* tokens;    // result [U] rows streamed (the skipped-block record)
     uint32_t* status;              // result: nonzero = partial-slot overflow
     StepState* ss;
@@ -92,31 +95,6 @@ struct StepCfg {
 // misc smem words
 enum : int { kMiscNact = 0, kMiscChunk, kMiscQueue, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat };
 
-// Split-K chunk plan of one unit of L rows: big chunks of C rows, then a tail
-// of `tail` (or more) rows cut into small chunks of c rows so the last claims
-// are short and every SM finishes within ~one small chunk of the others.
-struct ChunkPlan {
-    uint32_t C, c, tail;
-};
-__device__ __forceinline__ uint32_t plan_nb(uint32_t L, const ChunkPlan& cp) {
-    return L > cp.tail ? (L - cp.tail) / cp.C : 0u;
-}
-__device__ __forceinline__ uint32_t plan_nch(uint32_t L, const ChunkPlan& cp) {
-    const uint32_t nb = plan_nb(L, cp);
-    return nb + (L - nb * cp.C + cp.c - 1) / cp.c;
-}
-__device__ __forceinline__ void plan_range(uint32_t L, uint32_t k, const ChunkPlan& cp,
-                                           uint32_t& t0, uint32_t& t1) {
-    const uint32_t nb = plan_nb(L, cp);
-    if (k < nb) {
-        t0 = k * cp.C;
-        t1 = t0 + cp.C;
-    } else {
-        t0 = nb * cp.C + (k - nb) * cp.c;
-        t1 = min(t0 + cp.c, L);
-    }
-}
-constexpr uint32_t kTailChunkTok = 64;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long v;
@@ -210,8 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     //    each, the floor of this phase) and scores it.  Warp 0 routes one unit
     //    per lane and builds the Active list with a ballot: two block barriers
     //    in all, and a short code path (the phase is latency bound).
-    //  * tiled (batched steps): 64-head tiles staged through shared memory,
-    //    block-wide scans over the units.
+    //  * distributed (batched steps): each CTA scores its share of the units,
+    //    one grid barrier, then every CTA scans the published decisions.
     const bool lean = NH <= (uint32_t)kRouteTile && U <= 32u;
     if (lean) {
         // exact fp64 products q_j*k_j and q_j*q_j (f32 x f32 fits in 53 bits)
@@ -362,12 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             cc = ((cc + kStageTok - 1) / kStageTok) * kStageTok;
             if (cc < kMinChunkTok) cc = kMinChunkTok;
             const bool flat = nact > G;
-            if (flat) {  // chunk prefix over the Active list (lane order == list order)
-                ChunkPlan cp;
-                cp.C = (uint32_t)cc;
-                cp.c = kTailChunkTok;
-                cp.tail = ((G + nact - 1) / max(nact, 1u) + 1) * 2 * kTailChunkTok;
-                const uint32_t mine = active ? plan_nch(L, cp) : 0u;
+            if (flat) {  // token prefix over the Active list (lane order == list order)
+                const uint32_t mine = active ? L : 0u;
                 uint32_t incl = mine;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -385,15 +359,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         STAMP(3);
     } else {
-        // tiled: head i belongs to unit i / r.  The exact fp64 products of
-        // 64-head tiles are staged in smem; then thread h runs the dot chain and
-        // thread 64+h the |q|^2 chain, each a sequential fp64 sum in index order.
+        // distributed (batched steps): CTA c scores units [u_lo, u_hi) -- all r
+        // heads of each, so it also takes their group means and decisions --
+        // publishes them, and after one grid barrier every CTA builds the Active
+        // list from the published decisions.  Head i belongs to unit i / r.  The
+        // exact fp64 products of 64-head tiles are staged in smem; then thread h
+        // runs the dot chain and thread 64+h the |q|^2 chain, each a sequential
+        // fp64 sum in index order.
+        const uint32_t up = (U + G - 1) / G;
+        const uint32_t u_lo = min(U, bid * up), u_hi = min(U, u_lo + up);
+        const uint32_t h_lo = u_lo * r, h_hi = u_hi * r;
         {
             double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1] f64
             double* sk = sq + kRouteTile * SC::kDP;
             double* s_chain = sk + kRouteTile * SC::kDP;  // [2][kRouteTile]
-            for (uint32_t h_base = 0; h_base < NH; h_base += kRouteTile) {
-                const uint32_t nh = min((uint32_t)kRouteTile, NH - h_base);
+            for (uint32_t h_base = h_lo; h_base < h_hi; h_base += kRouteTile) {
+                const uint32_t nh = min((uint32_t)kRouteTile, h_hi - h_base);
                 // warp w loads heads w, w+5, ...; lane l loads kV = D/32 consecutive
                 // floats of the row with one vector load.  The products go to smem
                 // rows of odd stride (D+1 doubles, conflict-free for the chains)
@@ -479,27 +460,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                         sc = __ddiv_rn(dot, __dmul_rn(qn, kn));
                         sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
                     }
-                    s_score[h_base + tid] = sc;
-                    s_degen[h_base + tid] = dg;
+                    s_score[h_base - h_lo + tid] = sc;
+                    s_degen[h_base - h_lo + tid] = dg;
                 }
                 __syncthreads();
             }
         }
 
-        // group_score + route (router.cpp:50-57,67-75,113-120) on contiguous unit
-        // runs per thread, then an order-preserving scan builds the Active list.
-        const uint32_t per = (U + kThreads - 1) / kThreads;
-        const uint32_t u0 = min(U, tid * per), u1 = min(U, u0 + per);
-        uint32_t my_active = 0;
-        unsigned long long my_tok = 0;
-        uint64_t my_bits = 0;  // active bits of this thread's run (per <= 64 guaranteed)
-        for (uint32_t u = u0; u < u1; ++u) {
+        // group_score + route (router.cpp:50-57,67-75,113-120) of this CTA's units
+        for (uint32_t u = u_lo + tid; u < u_hi; u += kThreads) {
             const uint32_t seq = u / t.Hkv;
+            const uint32_t hb = (u - u_lo) * r;
             double sum = 0.0;
             uint32_t degen = 0;
             for (uint32_t i = 0; i < r; ++i) {
-                sum = __dadd_rn(sum, s_score[u * r + i]);
-                degen |= s_degen[u * r + i];
+                sum = __dadd_rn(sum, s_score[hb + i]);
+                degen |= s_degen[hb + i];
             }
             // sum / r (router.cpp:56); for power-of-two r the product with 1/r is
             // the same correctly rounded value and avoids the division sequence
@@ -509,26 +485,52 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool sink = over && !(flags & kLayerExcluded);
             if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
             const bool active = (flags & kObserveOnly) || !sink;
-            if (active) {
-                ++my_active;
-                my_tok += s_len[seq];
-                my_bits |= 1ull << (u - u0);
-            }
-            if (lead) {
-                t.group_scores[u] = S;
-                t.unit_flags[u] =
-                    (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
-                if (!active) {
-                    t.tokens[u] = 0ull;
-                    if (t.mode == 1) {  // rank partial of a skipped group: empty
-                        float* P = t.out + size_t(u) * r * (D + 2);
-                        for (uint32_t h = 0; h < r; ++h) {
-                            P[h] = -INFINITY;
-                            P[r + h] = 0.f;
-                        }
-                        for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+            const uint32_t fl = (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
+            t.route_flags[u] = fl;
+            t.group_scores[u] = S;
+            t.unit_flags[u] = fl;
+            if (!active) {
+                t.tokens[u] = 0ull;
+                if (t.mode == 1) {  // rank partial of a skipped group: empty
+                    float* P = t.out + size_t(u) * r * (D + 2);
+                    for (uint32_t h = 0; h < r; ++h) {
+                        P[h] = -INFINITY;
+                        P[r + h] = 0.f;
                     }
+                    for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
                 }
+            }
+        }
+        for (uint32_t h = h_lo + tid; h < h_hi; h += kThreads) t.head_scores[h] = s_score[h - h_lo];
+        // grid barrier: every unit's decision is published (cooperative launch,
+        // all CTAs resident; a 2 s watchdog turns a bug into an error, not a hang)
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(&t.ss->route_done, 1u);
+            const unsigned long long t_spin = globaltimer();
+            while (ld_volatile(&t.ss->route_done) < G) {
+                if (globaltimer() - t_spin > 2000000000ull) {
+                    atomicExch(&t.ss->error, 3u);
+                    break;
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+
+        // the Active list from the published decisions: contiguous unit runs
+        // per thread, then an order-preserving scan.
+        const uint32_t per = (U + kThreads - 1) / kThreads;
+        const uint32_t u0 = min(U, tid * per), u1 = min(U, u0 + per);
+        uint32_t my_active = 0;
+        unsigned long long my_tok = 0;
+        uint64_t my_bits = 0;  // active bits of this thread's run (per <= 64 guaranteed)
+        for (uint32_t u = u0; u < u1; ++u) {
+            if (__ldcg(&t.route_flags[u]) & kActive) {
+                ++my_active;
+                my_tok += s_len[u / t.Hkv];
+                my_bits |= 1ull << (u - u0);
             }
         }
         const unsigned long long tok_all = Reduce(tmp.reduce).Sum(my_tok);
@@ -546,11 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cc < kMinChunkTok) cc = kMinChunkTok;
         const uint32_t Ck = (uint32_t)cc;
         const bool flat = nact > G;
-        ChunkPlan cp;
-        cp.C = Ck;
-        cp.c = kTailChunkTok;
-        cp.tail = ((G + nact - 1) / max(nact, 1u) + 1) * 2 * kTailChunkTok;
-        uint32_t my_chunks = 0;
+        uint32_t my_chunks = 0;  // flat mode: this thread's Active tokens (token prefix)
         {
             uint32_t a = a_off;
             for (uint32_t u = u0; u < u1; ++u) {
@@ -558,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t L = s_len[u / t.Hkv];
                 act_len[a] = L;
                 act_unit[a++] = (uint16_t)u;
-                if (flat) my_chunks += plan_nch(L, cp);
+                if (flat) my_chunks += L;
             }
         }
         if (flat) {
@@ -569,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (uint32_t u = u0; u < u1; ++u) {
                 if (!((my_bits >> (u - u0)) & 1ull)) continue;
                 act_prefix[a] = c_off;
-                c_off += plan_nch(act_len[a++], cp);
+                c_off += act_len[a++];
             }
             if (tid == 0) act_prefix[nact] = c_tot;
         }
@@ -578,18 +576,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             misc[kMiscChunk] = Ck;
             misc[kMiscFlat] = flat ? 1u : 0u;
         }
-        if (lead)
-            for (uint32_t i = tid; i < NH; i += kThreads) t.head_scores[i] = s_score[i];
     }
     __syncthreads();  // Active list, chunk plan and misc visible to all threads
     STAMP(7);
     const uint32_t nact = misc[kMiscNact];
     const uint32_t Ck = misc[kMiscChunk];
     const bool flat = misc[kMiscFlat] != 0;
-    ChunkPlan cp;
-    cp.C = Ck;
-    cp.c = kTailChunkTok;
-    cp.tail = ((G + nact - 1) / max(nact, 1u) + 1) * 2 * kTailChunkTok;
     // few, long Active groups: merge tasks spread over all CTAs at the end;
     // many groups: the CTA that streams a group's last rows merges it.
     const bool queue_mode = 4 * nact <= G;
@@ -688,24 +680,53 @@ __global__ void __launch_bounds__(kThreads, 1)
                     t1 = min(n0 + sz, L);
                 }
             } else if (nact > 0) {
-                // many Active groups: one flat chunk cursor over the active list
-                const uint32_t total = act_prefix[nact];
-                uint32_t chunk = bid, a = 0;
-                while (chunk < total) {
-                    const uint32_t next = G + atomicAdd(&t.ss->flat_counter, 1u);
-                    // act_prefix is sorted: advance (chunk ids of one CTA increase)
-                    uint32_t lo = a, hi = nact;
-                    while (hi - lo > 1) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (act_prefix[mid] <= chunk) lo = mid; else hi = mid;
+                // many Active groups (batched steps): guided self-scheduling over
+                // ONE global token space, the Active units laid end to end
+                // (act_prefix = token prefix).  A static first claim of T/(3G)
+                // tokens per CTA, then claims from one cursor whose size shrinks
+                // with the remaining tokens (T - pos)/(2G), down to one stage.
+                // Early claims cover about a unit, so a CTA flushes a partial
+                // every few units rather than every chunk; a claim that crosses
+                // a unit boundary is emitted piecewise.
+                const uint32_t T = act_prefix[nact];
+                uint32_t S0 = T / (3 * G);
+                S0 = max((uint32_t)kStageTok, S0 / kStageTok * kStageTok);
+                const uint32_t base = min(G * S0, T);  // dynamic region start
+                // claims never shrink below kFlatMinTok: consecutive claims of
+                // one CTA land in different units, so each costs a partial flush
+                // (~3 L2 round trips); a 512-token floor bounds the tail at
+                // ~256 KB per SM instead of paying a flush per 64 tokens
+                const uint32_t floor_tok = min(S0, kFlatMinTok);
+                auto guided = [&](uint32_t pos) {
+                    const uint32_t rem = T > pos ? T - pos : 0u;
+                    uint32_t sz = rem / (2 * G) / kStageTok * kStageTok;
+                    return sz < floor_tok ? floor_tok : (sz > S0 ? S0 : sz);
+                };
+                uint32_t g0 = min(bid * S0, base), g1 = min(g0 + S0, base);
+                uint32_t a = 0;
+                for (;;) {
+                    // prefetch the next claim, sized from the LIVE cursor: our own
+                    // position lags it by about one claim per CTA, which would
+                    // keep late claims large and leave a long tail
+                    const uint32_t sz = guided(base + ld_volatile(&t.ss->flat_counter));
+                    const uint32_t n0 = base + atomicAdd(&t.ss->flat_counter, sz);
+                    while (g0 < g1) {
+                        // act_prefix is sorted and claims of one CTA increase
+                        if (act_prefix[a + 1] <= g0) {
+                            uint32_t lo = a + 1, hi = nact;
+                            while (hi - lo > 1) {
+                                const uint32_t mid = (lo + hi) >> 1;
+                                if (act_prefix[mid] <= g0) lo = mid; else hi = mid;
+                            }
+                            a = lo;
+                        }
+                        const uint32_t pa = act_prefix[a], pe = min(act_prefix[a + 1], g1);
+                        emit(act_unit[a], act_len[a], g0 - pa, pe - pa);
+                        g0 = pe;
                     }
-                    a = lo;
-                    const uint32_t u = act_unit[a], L = act_len[a];
-                    const uint32_t k = chunk - act_prefix[a];
-                    uint32_t t0, t1;
-                    plan_range(L, k, cp, t0, t1);
-                    emit(u, L, t0, t1);
-                    chunk = next;
+                    if (n0 >= T) break;
+                    g0 = n0;
+                    g1 = min(n0 + sz, T);
                 }
             }
             if (t.trace) {
@@ -1043,6 +1064,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             t.ss->flat_counter = 0;
             t.ss->merge_next = 0;
             t.ss->exit_count = 0;
+            t.ss->route_done = 0;
         }
     }
 }

@@ -20,11 +20,14 @@ NAMES = {0: "start", 1: "mbar-init", 13: "loads-issued", 15: "products", 16: "sy
 ORDER = [0, 1, 13, 15, 16, 14, 12, 2, 3, 7, 8, 9, 10, 11]
 
 Ls = [int(x) for x in sys.argv[1:]] or [32768, 524288]
+HQ, HKV, B = (int(os.environ.get(k, d)) for k, d in (("HQ", 32), ("HKV", 8), ("B", 1)))
+IMG = int(os.environ.get("IMG", 0))
 for L in Ls:
-    spec = WorkloadSpec(length=L, sink_fraction=0.625)
-    cache = P.KvCache(P.CacheConfig(1, 32, 8, 128, L))
+    spec = WorkloadSpec(num_q_heads=HQ, num_kv_heads=HKV, num_seqs=B, length=L, sink_fraction=0.625,
+                        image_tokens=IMG)
+    cache = P.KvCache(P.CacheConfig(1, HQ, HKV, 128, L, B))
     spec.fill(cache)
-    q = torch.from_numpy(spec.queries()[0]).cuda()
+    q = torch.from_numpy(spec.queries().reshape(B * HQ, 128)).cuda()
     out = torch.zeros_like(q)
     P.set_timing(cache, False)
     G = cache.decode_grid()
@@ -76,7 +79,7 @@ for L in Ls:
             print("  lead cycles:", " ".join(line))
     import time
     runner = P.StepRunner(cache, P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=()))
-    qh = spec.queries()[0]
+    qh = spec.queries() if B > 1 else spec.queries()[0]
     for _ in range(10):
         runner(qh)
     t = time.perf_counter()

@@ -56,6 +56,9 @@ def check_seq(orc, res_out, groups, spec, seq, q, k, v, kv_floats=None):
     ("C3-yi9b-200K-B2", dict(num_q_heads=32, num_kv_heads=4, length=204800, num_seqs=2)),
     ("C5-llava13b-8K-B8-image", dict(num_q_heads=40, num_kv_heads=40, length=8192, num_seqs=8,
                                       image_tokens=576)),
+    # the BASELINE batch: 480 Active groups > 148 SMs -> the global token-space scheduler
+    ("C5-llava13b-8K-B32-image", dict(num_q_heads=40, num_kv_heads=40, length=8192, num_seqs=32,
+                                       image_tokens=576)),
 ])
 def test_config_parity(oracle_libs, name, kw):
     _, orc = oracle_libs
