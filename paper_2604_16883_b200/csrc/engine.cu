@@ -129,6 +129,7 @@ struct sinkr_engine {
     uint32_t* d_cursor = nullptr;
     uint32_t* d_tokens_done = nullptr;
     uint32_t* d_route_flags = nullptr;  // distributed routing decisions [U]
+    uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [U]
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
 
     CUtensorMap tmk{}, tmv{};
@@ -210,6 +211,7 @@ struct sinkr_engine {
         t.slot_count = d_slot_count;
         t.tokens_done = d_tokens_done;
         t.route_flags = d_route_flags;
+        t.ovf = d_ovf;
         t.partials = d_partials;
         t.out = out;
         t.B = (uint32_t)B;
@@ -718,6 +720,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMemsetAsync(e->d_cursor, 0, e->U * 4, e->stream));
             CK(cudaMalloc(&e->d_tokens_done, e->U * 4));
             CK(cudaMalloc(&e->d_route_flags, e->U * 4));
+            CK(cudaMalloc(&e->d_ovf, e->U * 4));
+            CK(cudaMemsetAsync(e->d_ovf, 0, e->U * 4, e->stream));
             CK(cudaMemsetAsync(e->d_tokens_done, 0, e->U * 4, e->stream));
             if (const char* tr = std::getenv("SINKR_TRACE"); tr && tr[0] == '1') {
                 CK(cudaMalloc(&e->d_trace, e->grid * 8 * 8));
@@ -734,8 +738,13 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMalloc(&e->d_prefix, (e->U + 1) * 4));  // unit_next cursors
             CK(cudaMalloc(&e->d_slot_count, e->U * 4));
             CK(cudaMemsetAsync(e->d_slot_count, 0, e->U * 4, e->stream));
-            // one flush per (CTA, unit) at most: S = min(grid, stages per slot)
-            e->S = std::min<size_t>(e->grid, (e->cap + dev::kStageTok - 1) / dev::kStageTok);
+            // partial slots per unit: one per (CTA, unit) visit up to S-1; any
+            // further partial of a unit is LSE-combined into slot S-1 under a
+            // per-unit lock (step.cuh flush), so S only sizes the fast path.
+            // SINKR_DEBUG_SLOTS forces a small S to exercise the spill path.
+            e->S = std::min<size_t>(e->grid, (e->cap + dev::kStageTok - 1) / dev::kStageTok) + 32;
+            if (const char* ds = std::getenv("SINKR_DEBUG_SLOTS"); ds && std::atoi(ds) >= 2)
+                e->S = (size_t)std::atoi(ds);
             e->PS = e->r * (e->D + 2);
             CK(cudaMalloc(&e->d_partials, e->U * e->S * e->PS * 4));
             // combine reads candidate slots speculatively: keep them finite
@@ -810,6 +819,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_cursor);
     cudaFree(e->d_tokens_done);
     cudaFree(e->d_route_flags);
+    cudaFree(e->d_ovf);
     cudaFree(e->d_head_degen);
     cudaFree(e->d_active);
     cudaFree(e->d_prefix);

@@ -61,6 +61,7 @@ struct StepTables {
     uint32_t* cursor;              // [U] chunk cursor per active-list entry
     uint32_t* slot_count;          // [U]
     uint32_t* tokens_done;         // [U]
+    uint32_t* ovf;                 // [U] spill-slot lock (bit0) + valid (bit1)
     float* partials;               // [U][S][r*(D+2)]: m[r], l[r], acc[r][D]
     float* out;                    // mode 0: [B][Hq][D]; mode 1: [U][r][D+2]
     uint32_t B, Hq, Hkv, r, cap, S, mode;
@@ -76,7 +77,7 @@ struct StepCfg {
     static constexpr int kOffMeta = kOffBars + 2 * C::kStages * 8;
     static constexpr int kOffO = kOffMeta + C::kStages * 16;
     static constexpr int kOffML = kOffO + kCWarps * kMaxR * C::kOStride * 4;
-    static constexpr int kOffMisc = kOffML + kCWarps * kMaxR * 2 * 4;
+    static constexpr int kOffMisc = kOffML + (kCWarps + 1) * kMaxR * 2 * 4;  // + spill staging
     static constexpr int kOffAct = kOffMisc + 64;
     static constexpr int kOffPrefix = kOffAct + kMaxUnits * 2;
     static constexpr int kOffLen = kOffPrefix + (kMaxUnits + 1) * 4;
@@ -104,6 +105,66 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
     return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// One warp LSE-merges the n Split-K partials of (unit, head h) for the 32
+// dims d0 .. d0+31 (merge_partials, attention.cpp:159-183): partials come in
+// groups of 96 -- lane j holds (m, l) of partials j, j+32, j+64, every lane
+// holds its dim of all 96 acc rows, all loads of a group in flight at once --
+// and the weights 2^(m_j - max) reach the lanes by shuffle.  One L2 round trip
+// per 96 partials.  Writes the normalised row (mode 0) or an un-normalised
+// rank partial (mode 1).
+template <int D>
+__device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
+                                           uint32_t lane) {
+    const uint32_t r = t.r, PS = r * (D + 2);
+    const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
+    const float* base = t.partials + size_t(u) * t.S * PS;
+    const uint32_t d = d0 + lane;
+    float mx = -INFINITY, lsum = 0.f, acc = 0.f;
+    for (uint32_t j0 = 0; j0 < n; j0 += 96) {
+        float mv[3], lv[3], av[96];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const uint32_t j = j0 + 32 * c + lane;
+            mv[c] = j < n ? __ldcg(base + size_t(j) * PS + h) : -INFINITY;
+            lv[c] = j < n ? __ldcg(base + size_t(j) * PS + r + h) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 96; ++k)
+            av[k] = (j0 + k < n) ? __ldcg(base + size_t(j0 + k) * PS + 2 * r + h * D + d) : 0.f;
+        float cm = fmaxf(fmaxf(mv[0], mv[1]), mv[2]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+        const float nm = fmaxf(mx, cm);
+        if (nm != mx) {  // rescale the running sums to the new max
+            const float sc = mx == -INFINITY ? 0.f : ptx::ex2(mx - nm);
+            acc *= sc;
+            lsum *= sc;
+            mx = nm;
+        }
+        float w[3], lw = 0.f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            w[c] = mv[c] == -INFINITY ? 0.f : ptx::ex2(mv[c] - mx);
+            lw += lv[c] * w[c];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
+        lsum += lw;
+#pragma unroll
+        for (int k = 0; k < 96; ++k) acc += av[k] * __shfl_sync(0xffffffffu, w[k / 32], k % 32);
+    }
+    if (t.mode == 0) {
+        t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
+    } else {
+        float* P = t.out + size_t(u) * PS;
+        if (d == 0) {
+            P[h] = mx;
+            P[r + h] = lsum;
+        }
+        P[2 * r + h * D + d] = acc;
+    }
 }
 
 template <int D>
@@ -644,9 +705,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // the statically covered prefix base(a)*Ck; their size shrinks
                 // with the unit's remaining rows (guided), down to one 64-token
                 // stage, so all SMs finish within about one stage of each other.
-                // An exhausted unit hands the CTA on to the next entry.
+                // An exhausted unit hands the CTA on to the unit with the most
+                // unclaimed rows (all cursors read in parallel, 16 loads in
+                // flight), so the tail is spent streaming, not probing.
                 const uint32_t cpu = (G + nact - 1) / nact;  // CTAs per unit
-                uint32_t a = bid % nact, visited = 1;
+                uint32_t a = bid % nact;
                 uint32_t u = act_unit[a], L = act_len[a];
                 uint32_t first = ((G - a + nact - 1) / nact) * Ck;
                 uint32_t t0 = (bid / nact) * Ck, t1 = min(t0 + Ck, L);
@@ -658,16 +721,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                 };
                 for (;;) {
                     if (t0 >= L) {
-                        if (visited == nact) break;
-                        ++visited;
-                        a = (a + 1 == nact) ? 0 : a + 1;
+                        uint32_t best = 0, best_rem = 0;
+                        for (uint32_t b0 = 0; b0 < nact; b0 += 16) {
+                            uint32_t cur[16];
+#pragma unroll
+                            for (int k = 0; k < 16; ++k)
+                                cur[k] = (b0 + k < nact) ? ld_volatile(&t.cursor[b0 + k]) : 0u;
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const uint32_t b = b0 + k;
+                                if (b < nact) {
+                                    const uint32_t pos = ((G - b + nact - 1) / nact) * Ck + cur[k];
+                                    const uint32_t rem = act_len[b] > pos ? act_len[b] - pos : 0u;
+                                    if (rem > best_rem) {
+                                        best_rem = rem;
+                                        best = b;
+                                    }
+                                }
+                            }
+                        }
+                        if (best_rem == 0) break;
+                        a = best;
                         u = act_unit[a];
                         L = act_len[a];
                         first = ((G - a + nact - 1) / nact) * Ck;
-                        // size the hand-off claim from the unit's live cursor:
-                        // a CTA joining a nearly finished unit must not take a
-                        // full-size chunk off its tail
-                        const uint32_t sz = guided(first + ld_volatile(&t.cursor[a]));
+                        // a hand-off claim is sized from the unit's live remainder
+                        const uint32_t sz = guided(L - best_rem);
                         t0 = first + atomicAdd(&t.cursor[a], sz);
                         t1 = min(t0 + sz, L);
                         continue;
@@ -696,11 +775,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // one CTA land in different units, so each costs a partial flush
                 // (~3 L2 round trips); a 512-token floor bounds the tail at
                 // ~256 KB per SM instead of paying a flush per 64 tokens
-                const uint32_t floor_tok = min(S0, kFlatMinTok);
+                const uint32_t cap_tok = max(S0, kFlatMinTok);
                 auto guided = [&](uint32_t pos) {
                     const uint32_t rem = T > pos ? T - pos : 0u;
                     uint32_t sz = rem / (2 * G) / kStageTok * kStageTok;
-                    return sz < floor_tok ? floor_tok : (sz > S0 ? S0 : sz);
+                    return sz < kFlatMinTok ? kFlatMinTok : (sz > cap_tok ? cap_tok : sz);
                 };
                 uint32_t g0 = min(bid * S0, base), g1 = min(g0 + S0, base);
                 uint32_t a = 0;
@@ -753,6 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float o[2 * C::kNK][4];
         float m_used = -INFINITY, l_acc = 0.f;
         uint32_t cur = kEnd, cur_len = 0, run_tokens = 0;
+        uint32_t my_slot = 0;  // ctid 0: partial slot of the current visit, claimed at its start
 
         auto reset_state = [&]() {
 #pragma unroll
@@ -780,30 +860,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         // merge every partial of unit u (consumers only; few partials)
         auto merge_unit = [&](uint32_t u, uint32_t L) {
-            const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
-            const float* base = t.partials + size_t(u) * t.S * PS;
-            for (uint32_t idx = ctid; idx < r * D; idx += kCWarps * 32) {
-                const uint32_t h = idx / D, d = idx % D;
-                float mx = -INFINITY;
-                for (uint32_t j = 0; j < n; ++j) mx = fmaxf(mx, __ldcg(base + j * PS + h));
-                float acc = 0.f, lsum = 0.f;
-                for (uint32_t j = 0; j < n; ++j) {
-                    const float m = __ldcg(base + j * PS + h);
-                    const float w = m == -INFINITY ? 0.f : ptx::ex2(m - mx);
-                    acc += __ldcg(base + j * PS + 2 * r + h * D + d) * w;
-                    lsum += __ldcg(base + j * PS + r + h) * w;
-                }
-                if (t.mode == 0) {
-                    t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
-                } else {
-                    float* P = t.out + size_t(u) * PS;
-                    if (d == 0) {
-                        P[h] = mx;
-                        P[r + h] = lsum;
-                    }
-                    P[2 * r + h * D + d] = acc;
-                }
-            }
+            for (uint32_t task = cw; task < r * (D / 32); task += kCWarps)
+                warp_merge<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane);
             if (ctid == 0) t.tokens[u] = L;
         };
         auto flush = [&](uint32_t u, uint32_t L) {
@@ -821,43 +879,80 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sm_ml[(cw * kMaxR + grp) * 2 + 1] = l_tot;
                 }
             }
-            if (ctid == 0) misc[kMiscSlot] = atomicAdd(&t.slot_count[u], 1u);
+            if (ctid == 0) misc[kMiscSlot] = my_slot;
             ptx::named_bar_sync(1, kCWarps * 32);
             const uint32_t slot = misc[kMiscSlot];
-            if (slot < t.S) {
-                float* P = t.partials + (size_t(u) * t.S + slot) * PS;
-                for (uint32_t idx = ctid; idx < r * D; idx += kCWarps * 32) {
-                    const uint32_t h = idx / D, d = idx % D;
-                    float mx = -INFINITY;
-#pragma unroll
-                    for (int w = 0; w < kCWarps; ++w) mx = fmaxf(mx, sm_ml[(w * kMaxR + h) * 2]);
-                    float acc = 0.f, lsum = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kCWarps; ++w) {
-                        const float sc = ptx::ex2(sm_ml[(w * kMaxR + h) * 2] - mx);
-                        acc += sm_o[(w * kMaxR + h) * C::kOStride + d] * sc;
-                        lsum += sm_ml[(w * kMaxR + h) * 2 + 1] * sc;
+            // slots [0, S-1) take one partial each; every later partial of the
+            // unit (only a long, many-handed tail gets there) is LSE-combined
+            // into slot S-1 under a per-unit lock (ovf: bit0 lock, bit1 valid)
+            const bool spill = slot >= t.S - 1;
+            if (spill) {
+                if (ctid == 0) {
+                    uint32_t old_v;
+                    const unsigned long long t_spin = globaltimer();
+                    while ((old_v = atomicOr(&t.ovf[u], 1u)) & 1u) {
+                        if (globaltimer() - t_spin > 2000000000ull) {
+                            atomicExch(&t.ss->error, 1u);
+                            break;
+                        }
                     }
-                    P[2 * r + h * D + d] = acc;
-                    if (d == 0) {
-                        P[h] = mx;
-                        P[r + h] = lsum;
-                    }
+                    __threadfence();
+                    misc[kMiscTask] = old_v & 2u;  // slot S-1 already holds a partial
                 }
-            } else if (ctid == 0) {
-                atomicExch(&t.ss->error, 1u);
+                ptx::named_bar_sync(1, kCWarps * 32);
             }
-            __threadfence();  // partial visible before this run's rows are counted
+            const bool combine = spill && misc[kMiscTask] != 0;
+            float* P = t.partials + (size_t(u) * t.S + (spill ? t.S - 1 : slot)) * PS;
+            float* old_ml = sm_ml + kCWarps * kMaxR * 2;  // [kMaxR][2] staged (m, l) of slot S-1
+            if (combine) {
+                if (ctid < r) {
+                    old_ml[2 * ctid] = __ldcg(P + ctid);
+                    old_ml[2 * ctid + 1] = __ldcg(P + r + ctid);
+                }
+                ptx::named_bar_sync(1, kCWarps * 32);
+            }
+            for (uint32_t idx = ctid; idx < r * D; idx += kCWarps * 32) {
+                const uint32_t h = idx / D, d = idx % D;
+                float mx = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kCWarps; ++w) mx = fmaxf(mx, sm_ml[(w * kMaxR + h) * 2]);
+                float acc = 0.f, lsum = 0.f;
+#pragma unroll
+                for (int w = 0; w < kCWarps; ++w) {
+                    const float sc = ptx::ex2(sm_ml[(w * kMaxR + h) * 2] - mx);
+                    acc += sm_o[(w * kMaxR + h) * C::kOStride + d] * sc;
+                    lsum += sm_ml[(w * kMaxR + h) * 2 + 1] * sc;
+                }
+                if (combine) {
+                    const float mo = old_ml[2 * h], mn = fmaxf(mo, mx);
+                    const float so = mo == -INFINITY ? 0.f : ptx::ex2(mo - mn);
+                    const float sn = mx == -INFINITY ? 0.f : ptx::ex2(mx - mn);
+                    acc = __ldcg(P + 2 * r + h * D + d) * so + acc * sn;
+                    lsum = old_ml[2 * h + 1] * so + lsum * sn;
+                    mx = mn;
+                }
+                P[2 * r + h * D + d] = acc;
+                if (d == 0) {
+                    P[h] = mx;
+                    P[r + h] = lsum;
+                }
+            }
+            if (spill) {
+                __threadfence();
+                ptx::named_bar_sync(1, kCWarps * 32);
+                if (ctid == 0) atomicExch(&t.ovf[u], 2u);  // release; slot S-1 now valid
+            }
+            // the partial is visible before this run's rows are counted: the
+            // barrier orders the CTA's writes before ctid 0's gpu-scope release
             ptx::named_bar_sync(1, kCWarps * 32);
             if (ctid == 0) {
-                const uint32_t done = atomicAdd(&t.tokens_done[u], run_tokens) + run_tokens;
+                const uint32_t done = (queue_mode ? ptx::atom_add_release(&t.tokens_done[u], run_tokens)
+                                                  : ptx::atom_add_acq_rel(&t.tokens_done[u], run_tokens)) +
+                                      run_tokens;
                 misc[kMiscLast] = (done == L) ? 1u : 0u;
             }
             ptx::named_bar_sync(1, kCWarps * 32);
-            if (misc[kMiscLast] && !queue_mode) {
-                __threadfence();
-                merge_unit(u, L);
-            }
+            if (misc[kMiscLast] && !queue_mode) merge_unit(u, L);
             ptx::named_bar_sync(1, kCWarps * 32);
         };
 
@@ -870,6 +965,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (cur != kEnd) flush(cur, cur_len);  // the only flush site
                 if (unit == kEnd) break;
                 cur = unit;
+                if (ctid == 0) my_slot = atomicAdd(&t.slot_count[unit], 1u);  // hidden by the stream
                 cur_len = meta[stage].pad;
                 run_tokens = 0;
                 load_q(unit);
@@ -950,90 +1046,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ======================= phase M: distributed merge ========================
+    // Tasks (active entry, head, 32-dim slice) are claimed by WARPS: a warp
+    // waits until its unit's last rows are counted, then merges the slice with
+    // warp_merge (one L2 round trip per 96 partials, no block barrier).
     if (queue_mode && nact > 0) {
-        constexpr int kW = kThreads / 32;     // 5 warps share one task's partials
-        constexpr int kPW = 16;               // partials per warp held in registers
-        const uint32_t nd = D / 32;
+        constexpr uint32_t nd = D / 32;
         const uint32_t ntasks = nact * r * nd;
-        const uint32_t PS = r * (D + 2);
-        float* red = sm_o;                    // [kW][32] acc, [kW] l, [kW] max
         for (;;) {
-            if (tid == 0) misc[kMiscTask] = atomicAdd(&t.ss->merge_next, 1u);
-            __syncthreads();
-            const uint32_t task = misc[kMiscTask];
+            uint32_t task = 0;
+            if (lane == 0) task = atomicAdd(&t.ss->merge_next, 1u);
+            task = __shfl_sync(0xffffffffu, task, 0);
             if (task >= ntasks) break;
             const uint32_t a = task / (r * nd), rem = task % (r * nd);
             const uint32_t h = rem / nd, d = (rem % nd) * 32 + lane;
             const uint32_t u = act_unit[a];
             const uint32_t L = act_len[a];
-            if (tid == 0) {
+            if (lane == 0) {
                 // watchdog: a unit that never completes (a bug) must not hang
                 // the GPU; after 2 s report an error and give up the task
                 const unsigned long long t_spin = globaltimer();
-                while (ld_volatile(&t.tokens_done[u]) < L) {
+                while (ptx::ld_acquire(&t.tokens_done[u]) < L) {
                     if (globaltimer() - t_spin > 2000000000ull) {
                         atomicExch(&t.ss->error, 2u);
                         break;
                     }
                 }
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
-                __threadfence();
             }
-            __syncthreads();
-            const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
-            const float* base = t.partials + size_t(u) * t.S * PS;
-            float mv[kPW], av[kPW], lv[kPW];
-            float mx = -INFINITY;
-#pragma unroll
-            for (int k = 0; k < kPW; ++k) {
-                const uint32_t j = warp + k * kW;
-                mv[k] = j < n ? __ldcg(base + j * PS + h) : -INFINITY;
-                lv[k] = j < n ? __ldcg(base + j * PS + r + h) : 0.f;
-                av[k] = j < n ? __ldcg(base + j * PS + 2 * r + h * D + d) : 0.f;
-            }
-#pragma unroll
-            for (int k = 0; k < kPW; ++k) mx = fmaxf(mx, mv[k]);
-            for (uint32_t j = warp + kPW * kW; j < n; j += kW) mx = fmaxf(mx, __ldcg(base + j * PS + h));
-            if (lane == 0) red[kW * 33 + warp] = mx;
-            __syncthreads();
-            mx = red[kW * 33];
-#pragma unroll
-            for (int w = 1; w < kW; ++w) mx = fmaxf(mx, red[kW * 33 + w]);
-            float acc = 0.f, lsum = 0.f;
-#pragma unroll
-            for (int k = 0; k < kPW; ++k) {
-                const float w = mv[k] == -INFINITY ? 0.f : ptx::ex2(mv[k] - mx);
-                acc += av[k] * w;
-                lsum += lv[k] * w;
-            }
-            for (uint32_t j = warp + kPW * kW; j < n; j += kW) {
-                const float m = __ldcg(base + j * PS + h);
-                const float w = m == -INFINITY ? 0.f : ptx::ex2(m - mx);
-                acc += __ldcg(base + j * PS + 2 * r + h * D + d) * w;
-                lsum += __ldcg(base + j * PS + r + h) * w;
-            }
-            red[warp * 33 + lane] = acc;
-            if (lane == 0) red[warp * 33 + 32] = lsum;
-            __syncthreads();
-            if (warp == 0) {
-#pragma unroll
-                for (int w = 1; w < kW; ++w) {
-                    acc += red[w * 33 + lane];
-                    lsum += red[w * 33 + 32];
-                }
-                if (t.mode == 0) {
-                    t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
-                } else {
-                    float* P = t.out + size_t(u) * PS;
-                    if (d == 0) {
-                        P[h] = mx;
-                        P[r + h] = lsum;
-                    }
-                    P[2 * r + h * D + d] = acc;
-                }
-                if (h == 0 && d == 0) t.tokens[u] = L;
-            }
-            __syncthreads();
+            __syncwarp();
+            warp_merge<D>(t, u, h, d - lane, lane);
+            if (h == 0 && d == 0) t.tokens[u] = L;
         }
     }
 
@@ -1054,6 +1096,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             t.cursor[a] = 0;
             t.slot_count[u] = 0;
             t.tokens_done[u] = 0;
+            t.ovf[u] = 0;
         }
         if (tid == 0 && t.trace) t.trace[bid * 8 + 5] = globaltimer();
         if (tid == 0) {

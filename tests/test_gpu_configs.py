@@ -54,6 +54,9 @@ def check_seq(orc, res_out, groups, spec, seq, q, k, v, kv_floats=None):
 @pytest.mark.parametrize("name,kw", [
     ("C1-llama8b-32K", dict(num_q_heads=32, num_kv_heads=8, length=32768)),
     ("C3-yi9b-200K-B2", dict(num_q_heads=32, num_kv_heads=4, length=204800, num_seqs=2)),
+    # the BASELINE batch: 32 Active groups -> distributed routing, global
+    # token-space scheduler, warp-claimed queue merge over many partials
+    ("C3-yi9b-200K-B16", dict(num_q_heads=32, num_kv_heads=4, length=204800, num_seqs=16)),
     ("C5-llava13b-8K-B8-image", dict(num_q_heads=40, num_kv_heads=40, length=8192, num_seqs=8,
                                       image_tokens=576)),
     # the BASELINE batch: 480 Active groups > 148 SMs -> the global token-space scheduler

@@ -315,3 +315,30 @@ def test_golden_fixture_engine(name):
     assert res.counters.kv_floats_loaded == cnt[0]
     assert res.counters.anchor_floats_loaded == cnt[1]
     assert res.counters.groups_active == cnt[2] and res.counters.groups_skipped == cnt[3]
+
+
+@pytest.mark.parametrize("slots", [2, 5])
+def test_partial_spill_slot(oracle_libs, monkeypatch, slots):
+    """Force a tiny partial-slot budget (SINKR_DEBUG_SLOTS) so most Split-K
+    partials of a unit spill into the locked, LSE-combined last slot; the step
+    must still match the oracle (routing bit-exact, outputs within tolerance)."""
+    import oracle
+
+    _, orc = oracle_libs
+    monkeypatch.setenv("SINKR_DEBUG_SLOTS", str(slots))
+    spec = WorkloadSpec(length=65536, sink_fraction=0.625, seed=slots)
+    q = spec.queries()[0]
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as cache:
+        spec.fill(cache)
+        res = P.routed_decode_step(q, 0, cache, cfg)
+        res2 = P.routed_decode_step(q, 0, cache, cfg)  # counters/locks reset between steps
+    k, v = spec.host_cache(0)
+    k0n = [orc.anchor_norm(k[g, 0]) for g in range(8)]
+    ref = orc.routed_decode_step(k, v, k[:, 0].copy(), k0n, q, 0, oracle.Profile.constant(0.5),
+                                 excluded=(), threads=8)
+    for r_ in (res, res2):
+        assert np.array_equal(r_.route_bitmap, ref.sink.astype(bool))
+        assert [g.kv_floats_loaded for g in r_.groups] == list(ref.group_kv_floats)
+        assert np.abs(r_.outputs - ref.outputs).max() <= 2e-3
+        assert np.linalg.norm(r_.outputs - ref.outputs) <= 1e-3 * np.linalg.norm(ref.outputs)
