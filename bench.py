@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the sequence-sharded N>1 path even at N=1 (validation)")
     return ap.parse_args()
 
 
@@ -383,7 +385,7 @@ def run_ours(args, world, rank, local_rank):
     dev = local_rank
     torch.cuda.set_device(dev)
     dist = None
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
@@ -394,11 +396,12 @@ def run_ours(args, world, rank, local_rank):
     dense_cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(2.0), excluded_layers=())
     peak, peak_src = peak_hbm()
 
-    if world > 1:
+    if world > 1 or args.force_sharded:
         from paper_2604_16883_b200 import sharding
 
         result = sharding.bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg,
-                                                 args, rank, world, dev)
+                                                 args, rank, world, dev, peak_gbs=peak,
+                                                 peak_src=peak_src, clock_sampler=ClockSampler)
         if rank == 0:
             print(json.dumps(result), flush=True)
         dist.barrier()

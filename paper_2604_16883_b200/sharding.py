@@ -88,20 +88,32 @@ def sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, 
     P.merge_rank_partials_async(cache, gathered.data_ptr(), world, dout.data_ptr())
 
 
-def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev):
-    """bench.py's N>1 path: strong scaling of the headline workload."""
+def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev,
+                           peak_gbs=None, peak_src="", clock_sampler=None):
+    """bench.py's N>1 path (and --force-sharded at N=1): strong scaling of the
+    headline workload, every number the max over ranks."""
     import json
+    import time
 
     cache, (lo, hi) = build_sequence_shard(P, spec, rank, world, dev)
     P.set_timing(cache, False)
     opts = P.EngineOptions(global_context_len=spec.length)
-    dq = torch.from_numpy(spec.queries()[0]).cuda()
+    q_host = torch.from_numpy(spec.queries()[0]).pin_memory()
+    dq = q_host.cuda()
     dout = torch.empty_like(dq)
-    nf = cache.rank_partial_floats()
+    out_host = torch.empty_like(q_host).pin_memory()
+    nf = P.rank_partial_floats(cache)
     partial = torch.empty(nf, dtype=torch.float32, device="cuda")
     gathered = torch.empty(world * nf, dtype=torch.float32, device="cuda")
     stream = torch.cuda.ExternalStream(cache.stream)
+
+    def maxed(x: float) -> float:
+        t = torch.tensor([x], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     res = {}
+    clocks = None
     for name, cfg in (("routed", routed_cfg), ("dense", dense_cfg)):
         for _ in range(max(3, args.warmup)):
             sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world)
@@ -110,20 +122,51 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        sampler = clock_sampler(dev) if (clock_sampler and name == "routed") else None
+        if sampler:
+            sampler.__enter__()
         e0.record(stream)
         for _ in range(args.steps):
             sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world)
         e1.record(stream)
         torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__(None, None, None)
+            clocks = sampler.summary()
         dist.barrier()
-        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        res[name] = float(t.item())
-    info = P.fetch_step_info(cache)
-    n_act = info.counters.groups_active
-    kv = n_act * 2 * spec.length * spec.head_dim * 2
-    return {
-        "metric": ("decode-attn µs/step & KV GB/s (% HBM peak) at 512K; "
+        res[name] = maxed(e0.elapsed_time(e1) / args.steps)
+        if name == "routed":
+            n_act = P.fetch_step_info(cache).counters.groups_active
+
+    # e2e: host queries in (pinned H2D), sharded step, host outputs out, per step
+    for _ in range(2):
+        with torch.cuda.stream(stream):
+            dq.copy_(q_host, non_blocking=True)
+        sharded_step(P, torch, dist, cache, routed_cfg, opts, dq, partial, gathered, dout, world)
+        with torch.cuda.stream(stream):
+            out_host.copy_(dout, non_blocking=True)
+        stream.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            dq.copy_(q_host, non_blocking=True)
+        sharded_step(P, torch, dist, cache, routed_cfg, opts, dq, partial, gathered, dout, world)
+        with torch.cuda.stream(stream):
+            out_host.copy_(dout, non_blocking=True)
+        stream.synchronize()
+    e2e_us = maxed((time.perf_counter() - t0) / args.steps * 1e6)
+    h2d_bytes, d2h_bytes = int(q_host.numel() * 4), int(out_host.numel() * 4)
+    # pinned host blocks record an event on the engine stream when freed: free
+    # them while the engine (and its stream) is alive
+    stream.synchronize()
+    del q_host, out_host
+
+    kv_total = n_act * 2 * spec.length * spec.head_dim * 2          # all ranks
+    kv_rank = n_act * 2 * (hi - lo) * spec.head_dim * 2             # this rank
+    per_gpu_gbs = kv_rank / (res["routed"] * 1e-3) / 1e9  # the step time is already max-over-ranks
+    line = {
+        "metric": ("decode-attn \u00b5s/step & KV GB/s (% HBM peak) at 512K; "
                    "speedup vs own dense path"),
         "value": round(res["routed"] * 1e3, 2), "unit": "us/step", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["routed"], 5),
@@ -132,10 +175,23 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         "config": {"workload": f"llama3.1-8b-attn L={spec.length} B=1 "
                                f"routed={spec.sink_fraction} sequence-sharded",
                    "parallelism": f"sequence-shard x{world} + NCCL all-gather LSE merge",
-                   "context": spec.length, "tokens_per_rank": hi - lo},
+                   "context": spec.length, "tokens_per_rank": hi - lo,
+                   "l2": "per-rank KV larger than L2 at N <= 8"},
         "dense_us_per_step": round(res["dense"] * 1e3, 2),
         "speedup_vs_dense": round(res["dense"] / res["routed"], 3),
-        "kv_gbs_routed_step": round(kv / (res["routed"] * 1e-3) / 1e9, 1),
-        "gpu_launches": 4 * args.steps,
+        "kv_gbs_routed_step": round(kv_total / (res["routed"] * 1e-3) / 1e9, 1),
+        "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1),
+                     "peak": peak_gbs, "unit": "GB/s",
+                     "frac": round(per_gpu_gbs / peak_gbs, 4) if peak_gbs else None,
+                     "traffic": None,
+                     "kernel": "step_kernel<128> rank partial (per GPU) + combine_kernel",
+                     "peak_source": peak_src},
+        "e2e": {"value": round(e2e_us, 2), "unit": "us/step",
+                "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes},
+        "gpu_launches": 2 * args.steps,  # rank-partial step kernel + LSE combine (NCCL's own not counted)
+        "clocks": clocks,
         "note": json.dumps({"partial_bytes_per_rank": nf * 4}),
     }
+    cache.close()
+    return line
