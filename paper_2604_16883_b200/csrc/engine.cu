@@ -581,7 +581,13 @@ void fill_info(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg,
         // device-side phase stamps (%globaltimer, ns) written by the step kernel
         const auto* st = reinterpret_cast<const uint32_t*>(e->h_res + e->off_status);
         const auto* clk = reinterpret_cast<const unsigned long long*>(st + 4);
-        if (st[0]) fail(SINKR_RUNTIME_ERROR, "decode partial-slot overflow");
+        if (st[0]) {
+            static const char* what[] = {"", "partial spill-slot lock timeout",
+                                         "merge watchdog: a group never completed",
+                                         "routing grid-barrier watchdog",
+                                         "fp32 route estimate disagreed with the exact route"};
+            fail(SINKR_RUNTIME_ERROR, std::string("step kernel error: ") + (st[0] < 5 ? what[st[0]] : "unknown"));
+        }
         if (clk[1] >= clk[0] && clk[2] >= clk[1] && clk[3] >= clk[2]) {
             c.routing_seconds = (clk[1] - clk[0]) * 1e-9;
             c.attention_seconds = (clk[2] - clk[1]) * 1e-9;

@@ -30,6 +30,9 @@ constexpr int kMaxStepHeads = 4096;  // B * H_q per step
 constexpr int kRouteTile = 64;       // heads per routing tile
 constexpr int kRouteSub = 32;        // heads per load batch
 constexpr uint32_t kFlatMinTok = 512;  // smallest claim of the global token-space scheduler
+// an fp32 estimate of a group score decides the route when it clears tau by
+// this much (its own error is ~1e-6); closer calls wait for the exact score
+constexpr double kRouteMargin = 1e-4;
 
 struct StepState {
     unsigned int flat_counter;
@@ -94,7 +97,7 @@ struct StepCfg {
 };
 
 // misc smem words
-enum : int { kMiscNact = 0, kMiscChunk, kMiscQueue, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat };
+enum : int { kMiscNact = 0, kMiscChunk, kMiscQueue, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast };
 
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -253,26 +256,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     //    one grid barrier, then every CTA scans the published decisions.
     const bool lean = NH <= (uint32_t)kRouteTile && U <= 32u;
     if (lean) {
-        // exact fp64 products q_j*k_j and q_j*q_j (f32 x f32 fits in 53 bits)
-        // of every head, computed by all warps off the chains and staged in
-        // smem rows of odd stride (D+1 doubles; conflict-free chain reads) with
-        // a lane-rotated element order (conflict-free stores).  Warp w takes
-        // heads w, w+5, ...; lane l holds elements kV*l .. kV*l+kV-1.
+        // Fast decision first: an fp32 estimate of every head score (warp
+        // dot products of the rows already in registers).  If every group's
+        // estimate clears tau by kRouteMargin -- far above the estimate's
+        // error of ~1e-6 -- the decisions are exact already and streaming
+        // starts now; the lead CTA's consumer warps then compute the exact
+        // fp64 scores for the record (and check the decisions) while their
+        // first stages are in flight.  Otherwise the exact scores come first:
+        // all warps form the exact fp64 products (a product of two floats is
+        // exact in fp64, so s + p is bit-identical to the reference's
+        // `s += (double)q[i] * k0[i]`), thread h runs its head's dot and |q|^2
+        // chains (sequential DADDs in index order), and warp 0 routes.
         double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1]
         double* sk = sq + kRouteTile * SC::kDP;
+        float* est = reinterpret_cast<float*>(s_score);  // [2][kRouteTile] fp32 dot, |q|^2
+        constexpr int kW = kThreads / 32;
+        constexpr int kHPW = (kRouteTile + kW - 1) / kW;
+        constexpr int kV = D / 32;
+        float qv[kHPW][kV], kv[kHPW][kV];
+        // warp 0 lane u: k0_norm of unit u, loaded with the rows (off the
+        // decision's critical path)
+        const float kn_lane = (warp == 0 && lane < U)
+                                  ? ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + lane], ptx::policy_evict_last())
+                                  : 1.f;
         {
-            constexpr int kW = kThreads / 32;
-            constexpr int kHPW = (kRouteTile + kW - 1) / kW;
-            constexpr int kV = D / 32;
             const uint64_t keep = ptx::policy_evict_last();
             const uint32_t rmagic = 0xFFFFFFFFu / r + 1u;  // i / r == umulhi(i, rmagic) for i < 2^16
             const float* kbase = t.anchors + size_t(layer) * U * D + kV * lane;
-            float qv[kHPW][kV], kv[kHPW][kV];
 #pragma unroll
             for (int a = 0; a < kHPW; ++a) {
                 const uint32_t h = min(warp + a * kW, NH - 1);
-                // q through L2 (coherent: a zero-copy step stages it in this
-                // kernel); the anchors are read-only
                 const float* qrow = t.q + size_t(h) * D + kV * lane;
                 const float* krow = kbase + size_t(r == 1 ? h : __umulhi(h, rmagic)) * D;
                 if constexpr (kV == 4) {
@@ -286,11 +299,122 @@ __global__ void __launch_bounds__(kThreads, 1)
                     qv[a][0] = x.x; qv[a][1] = x.y;
                     kv[a][0] = y.x; kv[a][1] = y.y;
                 } else {
-                    qv[a][0] = __ldcg(qrow);
+                    qv[a][0] = ptx::ldg_last(qrow, keep);
                     kv[a][0] = ptx::ldg_last(krow, keep);
                 }
             }
             if (tid == 0) STAMP(13);
+#pragma unroll
+            for (int a = 0; a < kHPW; ++a) {
+                const uint32_t h = warp + a * kW;
+                float d = 0.f, qq = 0.f;
+#pragma unroll
+                for (int e = 0; e < kV; ++e) {
+                    d = fmaf(qv[a][e], kv[a][e], d);
+                    qq = fmaf(qv[a][e], qv[a][e], qq);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    d += __shfl_xor_sync(0xffffffffu, d, o);
+                    qq += __shfl_xor_sync(0xffffffffu, qq, o);
+                }
+                if (lane == 0 && h < NH) {
+                    est[h] = d;
+                    est[kRouteTile + h] = qq;
+                }
+            }
+        }
+        __syncthreads();
+        STAMP(15);
+        // warp 0: one unit per lane -> decisions (from the estimates, or from the
+        // exact scores on the second pass), then the Active list by ballot
+        auto route_units = [&](bool exact) -> bool {
+            const uint32_t u = lane;
+            bool active = false, certain = true;
+            uint32_t L = 0;
+            if (u < U) {
+                const uint32_t seq = u / t.Hkv;
+                const double tau = s_tau[seq];
+                double S;
+                uint32_t degen = 0;
+                if (exact) {
+                    double sum = 0.0;
+                    for (uint32_t i = 0; i < r; ++i) {
+                        sum = __dadd_rn(sum, s_score[u * r + i]);
+                        degen |= s_degen[u * r + i];
+                    }
+                    // sum / r (router.cpp:56); for power-of-two r the product
+                    // with 1/r is the same correctly rounded value
+                    S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
+                } else {
+                    // fast-math estimate (rsqrt, reciprocal): its error stays far
+                    // below kRouteMargin
+                    const float inv_kn = __frcp_rn(kn_lane);
+                    float sum = 0.f;
+                    for (uint32_t i = 0; i < r; ++i) {
+                        const float qq = est[kRouteTile + u * r + i];
+                        certain &= qq > 1e-20f;  // near-degenerate query: decide exactly
+                        sum += qq > 0.f ? est[u * r + i] * rsqrtf(qq) * inv_kn : 0.f;
+                    }
+                    const float Sf = sum * __frcp_rn((float)r);
+                    certain &= fabsf(Sf - (float)tau) > (float)kRouteMargin;
+                    S = (double)Sf;
+                }
+                const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
+                bool sink = over && !(flags & kLayerExcluded);
+                if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
+                active = (flags & kObserveOnly) || !sink;
+                if ((flags & kObserveOnly) || (flags & kLayerExcluded)) certain = true;
+                L = s_len[seq];
+                if (!exact) act_prefix[u] = active ? 1u : 0u;  // estimate decisions, checked later
+                if (lead) {
+                    if (exact) t.group_scores[u] = S;
+                    t.unit_flags[u] =
+                        (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
+                    if (!active) {
+                        t.tokens[u] = 0ull;
+                        if (t.mode == 1) {  // rank partial of a skipped group: empty
+                            float* P = t.out + size_t(u) * r * (D + 2);
+                            for (uint32_t h = 0; h < r; ++h) {
+                                P[h] = -INFINITY;
+                                P[r + h] = 0.f;
+                            }
+                            for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+                        }
+                    }
+                }
+            }
+            if (!exact && !__all_sync(0xffffffffu, certain)) return false;
+            const uint32_t mask = __ballot_sync(0xffffffffu, active);
+            const uint32_t nact = __popc(mask);
+            const uint32_t pos = __popc(mask & ((1u << lane) - 1u));
+            if (active) {
+                act_unit[pos] = (uint16_t)u;
+                act_len[pos] = L;
+            }
+            // chunk size from the Active token total (32-bit: U <= 32 slots)
+            uint32_t T = active ? L : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
+            if (lane == 0) {
+                const uint32_t gdiv = G * kChunksPerCta;
+                uint32_t cc = (T + gdiv - 1) / gdiv;
+                cc = (cc + kStageTok - 1) / kStageTok * kStageTok;
+                misc[kMiscNact] = nact;
+                misc[kMiscChunk] = cc < kMinChunkTok ? kMinChunkTok : cc;
+                misc[kMiscFlat] = 0u;  // U <= 32 < #SMs: unit-affine scheduling
+            }
+            return true;
+        };
+        if (warp == 0) {
+            const bool fast = route_units(false);
+            if (lane == 0) misc[kMiscFast] = fast ? 1u : 0u;
+        }
+        STAMP(14);
+        __syncthreads();
+        STAMP(16);
+        if (!misc[kMiscFast]) {
+            // exact scores before any decision: products, chains, then route
 #pragma unroll
             for (int a = 0; a < kHPW; ++a) {
                 const uint32_t h = warp + a * kW;
@@ -311,112 +435,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-        }
-        STAMP(15);
-        __syncthreads();
-        STAMP(16);
-        if (tid < NH) {
-            // the dot and |q|^2 chains of head tid, interleaved: each a
-            // sequential fp64 sum in index order (router.cpp:40-43)
-            const uint32_t u = tid / r;
-            const float kn = ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + u], ptx::policy_evict_last());
-            const double* pa = sq + tid * SC::kDP;
-            const double* pb = sk + tid * SC::kDP;
-            double dot = 0.0, qq = 0.0;
+            __syncthreads();
+            if (tid < NH) {
+                // the dot and |q|^2 chains of head tid, interleaved: each a
+                // sequential fp64 sum in index order (router.cpp:40-43)
+                const uint32_t u = tid / r;
+                const float kn = ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + u], ptx::policy_evict_last());
+                const double* pa = sq + tid * SC::kDP;
+                const double* pb = sk + tid * SC::kDP;
+                double dot = 0.0, qq = 0.0;
 #pragma unroll 16
-            for (uint32_t j = 0; j < (uint32_t)D; ++j) {
-                dot = __dadd_rn(dot, pa[j]);
-                qq = __dadd_rn(qq, pb[j]);
-            }
-            if (tid == 0) STAMP(14);
-            const double qn = __dsqrt_rn(qq);
-            double sc = 0.0;
-            uint8_t dg = 0;
-            if (qn < 1e-12) {
-                dg = 1;
-            } else {
-                sc = __ddiv_rn(dot, __dmul_rn(qn, (double)kn));
-                sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
-            }
-            s_score[tid] = sc;
-            s_degen[tid] = dg;
-            if (lead) t.head_scores[tid] = sc;
-        }
-        STAMP(12);
-        __syncthreads();  // scores, tau and len visible
-        STAMP(2);
-        if (warp == 0) {
-            const uint32_t u = lane;
-            bool active = false;
-            uint32_t L = 0;
-            if (u < U) {
-                const uint32_t seq = u / t.Hkv;
-                double sum = 0.0;
-                uint32_t degen = 0;
-                for (uint32_t i = 0; i < r; ++i) {
-                    sum = __dadd_rn(sum, s_score[u * r + i]);
-                    degen |= s_degen[u * r + i];
+                for (uint32_t j = 0; j < (uint32_t)D; ++j) {
+                    dot = __dadd_rn(dot, pa[j]);
+                    qq = __dadd_rn(qq, pb[j]);
                 }
-                // sum / r (router.cpp:56); for power-of-two r the product with
-                // 1/r is the same correctly rounded value
-                const double S =
-                    (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
-                const double tau = s_tau[seq];
-                const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
-                bool sink = over && !(flags & kLayerExcluded);
-                if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
-                active = (flags & kObserveOnly) || !sink;
-                L = s_len[seq];
-                if (lead) {
-                    t.group_scores[u] = S;
-                    t.unit_flags[u] =
-                        (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
-                    if (!active) {
-                        t.tokens[u] = 0ull;
-                        if (t.mode == 1) {  // rank partial of a skipped group: empty
-                            float* P = t.out + size_t(u) * r * (D + 2);
-                            for (uint32_t h = 0; h < r; ++h) {
-                                P[h] = -INFINITY;
-                                P[r + h] = 0.f;
-                            }
-                            for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
-                        }
-                    }
+                const double qn = __dsqrt_rn(qq);
+                double sc = 0.0;
+                uint8_t dg = 0;
+                if (qn < 1e-12) {
+                    dg = 1;
+                } else {
+                    sc = __ddiv_rn(dot, __dmul_rn(qn, (double)kn));
+                    sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
                 }
+                s_score[tid] = sc;
+                s_degen[tid] = dg;
+                if (lead) t.head_scores[tid] = sc;
             }
-            const uint32_t mask = __ballot_sync(0xffffffffu, active);
-            const uint32_t nact = __popc(mask);
-            const uint32_t pos = __popc(mask & ((1u << lane) - 1u));
-            if (active) {
-                act_unit[pos] = (uint16_t)u;
-                act_len[pos] = L;
-            }
-            unsigned long long T = active ? (unsigned long long)L : 0ull;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
-            const uint32_t gdiv = G * kChunksPerCta;
-            unsigned long long cc = T < (1ull << 32)
-                                        ? (unsigned long long)(((uint32_t)T + gdiv - 1) / gdiv)
-                                        : (T + gdiv - 1) / gdiv;
-            cc = ((cc + kStageTok - 1) / kStageTok) * kStageTok;
-            if (cc < kMinChunkTok) cc = kMinChunkTok;
-            const bool flat = nact > G;
-            if (flat) {  // token prefix over the Active list (lane order == list order)
-                const uint32_t mine = active ? L : 0u;
-                uint32_t incl = mine;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= (uint32_t)o) incl += y;
-                }
-                if (active) act_prefix[pos] = incl - mine;
-                if (lane == 31) act_prefix[nact] = incl;
-            }
-            if (lane == 0) {
-                misc[kMiscNact] = nact;
-                misc[kMiscChunk] = (uint32_t)cc;
-                misc[kMiscFlat] = flat ? 1u : 0u;
-            }
+            __syncthreads();  // scores visible
+            if (warp == 0) route_units(true);
         }
         STAMP(3);
     } else {
@@ -646,6 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // few, long Active groups: merge tasks spread over all CTAs at the end;
     // many groups: the CTA that streams a group's last rows merges it.
     const bool queue_mode = 4 * nact <= G;
+    const bool lean_fast = lean && misc[kMiscFast] != 0;
     // zero surrogate rows of Sink groups (router.cpp:97): sink unit u is
     // written by CTA u mod G (binary search of the sorted Active list)
     if (t.mode == 0 && nact < U) {
@@ -821,6 +869,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------ consumers ------------------------------
         const int cw = warp - 1;
         const uint32_t ctid = tid - 32;
+        if (lean_fast && lead) {
+            // the routing record's exact fp64 scores (the decisions were taken
+            // from fp32 estimates that cleared tau by kRouteMargin), computed
+            // while the first stages are in flight: thread h streams q row h and
+            // its group's k0 row through registers, exact products off the
+            // chain, sequential DADD chains in index order (router.cpp:40-43).
+            double* xs = reinterpret_cast<double*>(sm_o);  // flush staging is idle until the first flush
+            uint8_t* xd = reinterpret_cast<uint8_t*>(xs + kRouteTile);
+            if (ctid < NH) {
+                const uint32_t u = ctid / r;
+                const float4* qrow = reinterpret_cast<const float4*>(t.q + size_t(ctid) * D);
+                const float4* krow = reinterpret_cast<const float4*>(t.anchors + (size_t(layer) * U + u) * D);
+                const float kn = __ldg(&t.anchor_norm[size_t(layer) * U + u]);
+                double dot = 0.0, qq = 0.0;
+#pragma unroll 8
+                for (int c = 0; c < D / 4; ++c) {
+                    const float4 x = __ldg(qrow + c), y = __ldg(krow + c);
+                    const float qf[4] = {x.x, x.y, x.z, x.w}, kf[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const double qd = (double)qf[e];
+                        dot = __dadd_rn(dot, __dmul_rn(qd, (double)kf[e]));
+                        qq = __dadd_rn(qq, __dmul_rn(qd, qd));
+                    }
+                }
+                const double qn = __dsqrt_rn(qq);
+                double sc = 0.0;
+                uint8_t dg = 0;
+                if (qn < 1e-12) {
+                    dg = 1;
+                } else {
+                    sc = __ddiv_rn(dot, __dmul_rn(qn, (double)kn));
+                    sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
+                }
+                xs[ctid] = sc;
+                xd[ctid] = dg;
+                t.head_scores[ctid] = sc;
+            }
+            ptx::named_bar_sync(1, kCWarps * 32);
+            if (ctid < U) {
+                const uint32_t u = ctid, seq = u / t.Hkv;
+                double sum = 0.0;
+                uint32_t degen = 0;
+                for (uint32_t i = 0; i < r; ++i) {
+                    sum = __dadd_rn(sum, xs[u * r + i]);
+                    degen |= xd[u * r + i];
+                }
+                const double S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
+                double tau = 0.0;  // the ring overlay (s_tau) is gone: re-read the step's tau
+                if (p.inline_seqs) {
+#pragma unroll
+                    for (int k = 0; k < kParamSeqs; ++k)
+                        if ((uint32_t)k == seq) tau = p.tau[k];
+                } else {
+                    tau = __ldg(&t.tau_g[seq]);
+                }
+                const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
+                bool sink = over && !(flags & kLayerExcluded);
+                if (degen) sink = false;
+                const bool active = (flags & kObserveOnly) || !sink;
+                t.group_scores[u] = S;
+                if (active != (act_prefix[u] != 0u)) atomicExch(&t.ss->error, 4u);  // never: margin >> error
+            }
+            ptx::named_bar_sync(1, kCWarps * 32);
+        }
         const int tb = cw * kWarpTok;
         const int grp = lane >> 2, qd = lane & 3;
         const int lj = lane >> 3, li = lane & 7;

@@ -14,10 +14,10 @@ import paper_2604_16883_b200 as P
 from paper_2604_16883_b200 import _abi
 from paper_2604_16883_b200.workload import WorkloadSpec
 
-NAMES = {0: "start", 1: "mbar-init", 13: "loads-issued", 15: "products", 16: "sync", 14: "chains", 12: "scores", 2: "sync",
-         3: "route", 7: "sync", 8: "zero-rows+sync",
+NAMES = {0: "start", 1: "mbar-init", 13: "loads-issued", 15: "estimate+sync", 14: "decide",
+         16: "sync", 3: "exact-fallback", 7: "sync", 8: "zero-rows+sync",
          9: "stream-end", 10: "merge-end", 11: "exit-count"}
-ORDER = [0, 1, 13, 15, 16, 14, 12, 2, 3, 7, 8, 9, 10, 11]
+ORDER = [0, 1, 13, 15, 14, 16, 3, 7, 8, 9, 10, 11]
 
 Ls = [int(x) for x in sys.argv[1:]] or [32768, 524288]
 HQ, HKV, B = (int(os.environ.get(k, d)) for k, d in (("HQ", 32), ("HKV", 8), ("B", 1)))
