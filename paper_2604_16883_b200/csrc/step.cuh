@@ -33,6 +33,7 @@ constexpr uint32_t kFlatMinTok = 512;  // smallest claim of the global token-spa
 // an fp32 estimate of a group score decides the route when it clears tau by
 // this much (its own error is ~1e-6); closer calls wait for the exact score
 constexpr double kRouteMargin = 1e-4;
+constexpr uint32_t kMaxEstHeads = 2048;  // distributed form: per-CTA estimate slots (s_score overlay)
 
 struct StepState {
     unsigned int flat_counter;
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     //  * distributed (batched steps): each CTA scores its share of the units,
     //    one grid barrier, then every CTA scans the published decisions.
     const bool lean = NH <= (uint32_t)kRouteTile && U <= 32u;
+    bool exact_later = false;  // distributed form: exact record after streaming starts
     if (lean) {
         // Fast decision first: an fp32 estimate of every head score (warp
         // dot products of the rows already in registers).  If every group's
@@ -477,7 +479,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t up = (U + G - 1) / G;
         const uint32_t u_lo = min(U, bid * up), u_hi = min(U, u_lo + up);
         const uint32_t h_lo = u_lo * r, h_hi = u_hi * r;
+        // fp32 estimates of this CTA's head scores first (warp dot products);
+        // if all its groups clear tau by kRouteMargin the decisions are
+        // published now and the exact fp64 record is computed by the consumer
+        // warps after streaming starts (as in the lean form)
         {
+            float* est = reinterpret_cast<float*>(s_score);  // [2][kMaxEstHeads]
+            constexpr int kV = D / 32;
+            const uint64_t keep = ptx::policy_evict_last();
+            for (uint32_t h = h_lo + warp; h < h_hi; h += kThreads / 32) {
+                const float* qrow = t.q + size_t(h) * D + kV * lane;
+                const float* krow = t.anchors + (size_t(layer) * U + h / r) * D + kV * lane;
+                float d = 0.f, qq = 0.f;
+#pragma unroll
+                for (int e = 0; e < kV; ++e) {
+                    const float x = ptx::ldg_last(qrow + e, keep), y = ptx::ldg_last(krow + e, keep);
+                    d = fmaf(x, y, d);
+                    qq = fmaf(x, x, qq);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    d += __shfl_xor_sync(0xffffffffu, d, o);
+                    qq += __shfl_xor_sync(0xffffffffu, qq, o);
+                }
+                if (lane == 0) {
+                    est[h - h_lo] = d;
+                    est[kMaxEstHeads + h - h_lo] = qq;
+                }
+            }
+            __syncthreads();
+            bool certain = true;
+            for (uint32_t u = u_lo + tid; u < u_hi; u += kThreads) {
+                const float inv_kn = __frcp_rn(__ldg(&t.anchor_norm[size_t(layer) * U + u]));
+                const uint32_t hb = (u - u_lo) * r;
+                float sum = 0.f;
+                for (uint32_t i = 0; i < r; ++i) {
+                    const float qq = est[kMaxEstHeads + hb + i];
+                    certain &= qq > 1e-20f;
+                    sum += qq > 0.f ? est[hb + i] * rsqrtf(qq) * inv_kn : 0.f;
+                }
+                const float Sf = sum * __frcp_rn((float)r);
+                const double tau = s_tau[u / t.Hkv];
+                certain &= fabsf(Sf - (float)tau) > (float)kRouteMargin ||
+                           (flags & (kObserveOnly | kLayerExcluded)) != 0;
+                s_score[kMaxEstHeads + (u - u_lo)] = (double)Sf;  // estimate, for the decision below
+            }
+            exact_later = __syncthreads_and(certain) != 0 && (h_hi - h_lo) <= (uint32_t)(kThreads - 32);
+        }
+        STAMP(15);
+        if (!exact_later) {
             double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1] f64
             double* sk = sq + kRouteTile * SC::kDP;
             double* s_chain = sk + kRouteTile * SC::kDP;  // [2][kRouteTile]
@@ -573,21 +623,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __syncthreads();
             }
-        }
+        }  // !exact_later
 
         // group_score + route (router.cpp:50-57,67-75,113-120) of this CTA's units
         for (uint32_t u = u_lo + tid; u < u_hi; u += kThreads) {
             const uint32_t seq = u / t.Hkv;
             const uint32_t hb = (u - u_lo) * r;
-            double sum = 0.0;
+            double S;
             uint32_t degen = 0;
-            for (uint32_t i = 0; i < r; ++i) {
-                sum = __dadd_rn(sum, s_score[hb + i]);
-                degen |= s_degen[hb + i];
+            if (exact_later) {
+                S = s_score[kMaxEstHeads + (u - u_lo)];  // the estimate: it cleared the margin
+            } else {
+                double sum = 0.0;
+                for (uint32_t i = 0; i < r; ++i) {
+                    sum = __dadd_rn(sum, s_score[hb + i]);
+                    degen |= s_degen[hb + i];
+                }
+                // sum / r (router.cpp:56); for power-of-two r the product with
+                // 1/r is the same correctly rounded value
+                S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
             }
-            // sum / r (router.cpp:56); for power-of-two r the product with 1/r is
-            // the same correctly rounded value and avoids the division sequence
-            const double S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
             const double tau = s_tau[seq];
             const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
             bool sink = over && !(flags & kLayerExcluded);
@@ -595,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool active = (flags & kObserveOnly) || !sink;
             const uint32_t fl = (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
             t.route_flags[u] = fl;
-            t.group_scores[u] = S;
+            if (!exact_later) t.group_scores[u] = S;
             t.unit_flags[u] = fl;
             if (!active) {
                 t.tokens[u] = 0ull;
@@ -606,10 +661,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         P[r + h] = 0.f;
                     }
                     for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+                } else {  // zero surrogate rows (router.cpp:97), written by the owner
+                    float4* row = reinterpret_cast<float4*>(t.out + size_t(u) * r * D);
+                    for (uint32_t k = 0; k < r * D / 4; ++k) row[k] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
         }
-        for (uint32_t h = h_lo + tid; h < h_hi; h += kThreads) t.head_scores[h] = s_score[h - h_lo];
+        if (!exact_later)
+            for (uint32_t h = h_lo + tid; h < h_hi; h += kThreads) t.head_scores[h] = s_score[h - h_lo];
+        STAMP(14);
         // grid barrier: every unit's decision is published (cooperative launch,
         // all CTAs resident; a 2 s watchdog turns a bug into an error, not a hang)
         __syncthreads();
@@ -626,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __threadfence();
         }
         __syncthreads();
+        STAMP(16);
 
         // the Active list from the published decisions: contiguous unit runs
         // per thread, then an order-preserving scan.
@@ -634,18 +695,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t my_active = 0;
         unsigned long long my_tok = 0;
         uint64_t my_bits = 0;  // active bits of this thread's run (per <= 64 guaranteed)
-        for (uint32_t u = u0; u < u1; ++u) {
-            if (__ldcg(&t.route_flags[u]) & kActive) {
-                ++my_active;
-                my_tok += s_len[u / t.Hkv];
-                my_bits |= 1ull << (u - u0);
+        // all of this thread's flags in flight at once (runs are <= 8 units for
+        // U <= 1280), then the bookkeeping
+        for (uint32_t ub = u0; ub < u1; ub += 8) {
+            uint32_t fl[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) fl[k] = (ub + k < u1) ? __ldcg(&t.route_flags[ub + k]) : 0u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (fl[k] & kActive) {
+                    const uint32_t u = ub + k;
+                    ++my_active;
+                    my_tok += s_len[u / t.Hkv];
+                    my_bits |= 1ull << (u - u0);
+                }
             }
         }
+        STAMP(17);
         const unsigned long long tok_all = Reduce(tmp.reduce).Sum(my_tok);
         if (tid == 0) s_tok_total = tok_all;
         __syncthreads();
+        STAMP(18);
         uint32_t a_off, nact;
         Scan(tmp.scan).ExclusiveSum(my_active, a_off, nact);
+        STAMP(19);
         // chunk size: ~kChunksPerCta chunks per CTA, >= kMinChunkTok, stage multiple
         const unsigned long long T = s_tok_total;
         const uint32_t gdiv = G * kChunksPerCta;
@@ -667,6 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (flat) my_chunks += L;
             }
         }
+        STAMP(20);
         if (flat) {
             __syncthreads();
             uint32_t c_off, c_tot;
@@ -679,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (tid == 0) act_prefix[nact] = c_tot;
         }
+        STAMP(21);
         if (tid == 0) {
             misc[kMiscNact] = nact;
             misc[kMiscChunk] = Ck;
@@ -696,7 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool lean_fast = lean && misc[kMiscFast] != 0;
     // zero surrogate rows of Sink groups (router.cpp:97): sink unit u is
     // written by CTA u mod G (binary search of the sorted Active list)
-    if (t.mode == 0 && nact < U) {
+    if (lean && t.mode == 0 && nact < U) {  // (the distributed form's owners did it)
         for (uint32_t u = bid; u < U; u += G) {
             uint32_t lo = 0, hi = nact;
             while (lo < hi) {
@@ -869,17 +944,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------ consumers ------------------------------
         const int cw = warp - 1;
         const uint32_t ctid = tid - 32;
-        if (lean_fast && lead) {
+        if ((lean_fast && lead) || exact_later) {
             // the routing record's exact fp64 scores (the decisions were taken
             // from fp32 estimates that cleared tau by kRouteMargin), computed
             // while the first stages are in flight: thread h streams q row h and
             // its group's k0 row through registers, exact products off the
             // chain, sequential DADD chains in index order (router.cpp:40-43).
+            // Lean form: the lead CTA, all heads; distributed form: every CTA,
+            // its own units.
+            uint32_t xu_lo = 0, xu_hi = U;
+            if (!lean) {
+                const uint32_t up = (U + G - 1) / G;
+                xu_lo = min(U, bid * up);
+                xu_hi = min(U, xu_lo + up);
+            }
+            const uint32_t xh_lo = xu_lo * r, nxh = (xu_hi - xu_lo) * r;
             double* xs = reinterpret_cast<double*>(sm_o);  // flush staging is idle until the first flush
-            uint8_t* xd = reinterpret_cast<uint8_t*>(xs + kRouteTile);
-            if (ctid < NH) {
-                const uint32_t u = ctid / r;
-                const float4* qrow = reinterpret_cast<const float4*>(t.q + size_t(ctid) * D);
+            uint8_t* xd = reinterpret_cast<uint8_t*>(xs + (kThreads - 32));
+            if (ctid < nxh) {
+                const uint32_t h = xh_lo + ctid, u = h / r;
+                const float4* qrow = reinterpret_cast<const float4*>(t.q + size_t(h) * D);
                 const float4* krow = reinterpret_cast<const float4*>(t.anchors + (size_t(layer) * U + u) * D);
                 const float kn = __ldg(&t.anchor_norm[size_t(layer) * U + u]);
                 double dot = 0.0, qq = 0.0;
@@ -905,16 +989,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 xs[ctid] = sc;
                 xd[ctid] = dg;
-                t.head_scores[ctid] = sc;
+                t.head_scores[h] = sc;
             }
             ptx::named_bar_sync(1, kCWarps * 32);
-            if (ctid < U) {
-                const uint32_t u = ctid, seq = u / t.Hkv;
+            for (uint32_t u = xu_lo + ctid; u < xu_hi; u += kCWarps * 32) {
+                const uint32_t seq = u / t.Hkv, hb = (u - xu_lo) * r;
                 double sum = 0.0;
                 uint32_t degen = 0;
                 for (uint32_t i = 0; i < r; ++i) {
-                    sum = __dadd_rn(sum, xs[u * r + i]);
-                    degen |= xd[u * r + i];
+                    sum = __dadd_rn(sum, xs[hb + i]);
+                    degen |= xd[hb + i];
                 }
                 const double S = (r & (r - 1)) == 0 ? __dmul_rn(sum, 1.0 / (double)r) : __ddiv_rn(sum, (double)r);
                 double tau = 0.0;  // the ring overlay (s_tau) is gone: re-read the step's tau
@@ -930,7 +1014,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (degen) sink = false;
                 const bool active = (flags & kObserveOnly) || !sink;
                 t.group_scores[u] = S;
-                if (active != (act_prefix[u] != 0u)) atomicExch(&t.ss->error, 4u);  // never: margin >> error
+                const bool taken = lean ? act_prefix[u] != 0u : (t.route_flags[u] & kActive) != 0u;
+                if (active != taken) atomicExch(&t.ss->error, 4u);  // never: margin >> error
             }
             ptx::named_bar_sync(1, kCWarps * 32);
         }

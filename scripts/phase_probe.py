@@ -18,6 +18,9 @@ NAMES = {0: "start", 1: "mbar-init", 13: "loads-issued", 15: "estimate+sync", 14
          16: "sync", 3: "exact-fallback", 7: "sync", 8: "zero-rows+sync",
          9: "stream-end", 10: "merge-end", 11: "exit-count"}
 ORDER = [0, 1, 13, 15, 14, 16, 3, 7, 8, 9, 10, 11]
+if os.environ.get("DIST"):
+    NAMES.update({17: "flags", 18: "reduce", 19: "scan", 20: "actlist", 21: "flatscan"})
+    ORDER = [0, 1, 15, 14, 16, 17, 18, 19, 20, 21, 7, 8, 9, 10, 11]
 
 Ls = [int(x) for x in sys.argv[1:]] or [32768, 524288]
 HQ, HKV, B = (int(os.environ.get(k, d)) for k, d in (("HQ", 32), ("HKV", 8), ("B", 1)))
@@ -50,8 +53,8 @@ for L in Ls:
         P.routed_decode_async(q.data_ptr(), 0, cache, cfg, d_outputs=out.data_ptr())
         res = P.fetch_step_info(cache) if hasattr(P, "fetch_step_info") else None
         _abi.lib().sinkr_debug_trace(cache.handle, buf)
-        stamps = (C.c_ulonglong * 20)()
-        _abi.lib().sinkr_debug_stamps(cache.handle, stamps, 20)
+        stamps = (C.c_ulonglong * 24)()
+        _abi.lib().sinkr_debug_stamps(cache.handle, stamps, 24)
         s = np.array(stamps, dtype=np.int64)
         a = np.array(buf, dtype=np.float64).reshape(G, 8)
         t0 = a[:, 4].min()
