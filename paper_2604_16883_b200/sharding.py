@@ -194,4 +194,54 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         "note": json.dumps({"partial_bytes_per_rank": nf * 4}),
     }
     cache.close()
+    line["other_configs"] = [bench_unit_sharded(P, torch, dist, spec_cls=type(spec), args=args,
+                                                rank=rank, world=world, dev=dev,
+                                                routed_cfg=routed_cfg, dense_cfg=dense_cfg)]
     return line
+
+
+def bench_unit_sharded(P, torch, dist, spec_cls, args, rank, world, dev, routed_cfg, dense_cfg):
+    """BASELINE config 3 (Yi-9B-200K shape, 32 q / 4 KV heads, L = 204,800,
+    B = 16) with (seq, kv_head) units sharded across the ranks: rank k owns
+    sequences [k*B/N, (k+1)*B/N) -- all their units -- and steps them with no
+    collective at all.  Back-to-back steps, max over ranks."""
+    B = 16
+    if B % world:
+        return {"config": "C3 yi-9b-200k unit-sharded", "skipped": f"B={B} not divisible by {world}"}
+    nb = B // world
+    spec = spec_cls(num_q_heads=32, num_kv_heads=4, head_dim=128, length=204800, num_seqs=nb,
+                    sink_fraction=args.sink_fraction, seed=args.seed + 1000 + rank)
+    cache = P.KvCache(P.CacheConfig(1, 32, 4, 128, spec.length, nb), device=dev)
+    spec.fill(cache)
+    P.set_timing(cache, False)
+    dq = torch.from_numpy(spec.queries()).cuda()
+    dout = torch.empty_like(dq)
+    stream = torch.cuda.ExternalStream(cache.stream)
+    res = {}
+    for name, cfg in (("routed", routed_cfg), ("dense", dense_cfg)):
+        for _ in range(max(3, args.warmup)):
+            P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        res[name] = float(t.item()) * 1e3
+        if name == "routed":
+            n_act = torch.tensor([P.fetch_step_info(cache).counters.groups_active], device="cuda")
+            dist.all_reduce(n_act)
+    cache.close()
+    kv = int(n_act.item()) * 2 * spec.length * 128 * 2
+    return {"config": f"C3 yi-9b-200k-attn L=204800 B={B}, (seq, kv_head) units sharded x{world}, "
+                      "no collective",
+            "groups_active": int(n_act.item()), "groups_total": B * 4,
+            "routed_us": round(res["routed"], 2), "dense_us": round(res["dense"], 2),
+            "speedup_vs_dense": round(res["dense"] / res["routed"], 3),
+            "kv_gbs_routed": round(kv / (res["routed"] * 1e-6) / 1e9, 1),
+            "sequences_per_s_routed": round(B / (res["routed"] * 1e-6), 1)}
