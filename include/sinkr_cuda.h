@@ -221,6 +221,28 @@ sinkr_status sinkr_decode_rank_partial_async(sinkr_engine* e, const float* d_que
 sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gathered,
                                              size_t num_ranks, float* d_outputs);
 
+/* The same split with the collective fused into the step kernel: every rank's
+ * kernel writes its LSE partials straight into every rank's exchange block
+ * over NVLink (peer memory), signals each rank with a system-scope atomic, and
+ * its last CTA waits for all ranks' partials of the step and merges them into
+ * d_outputs -- one kernel per rank per step, no NCCL call.
+ *   sinkr_peer_setup       allocate this rank's exchange block (world <= 8)
+ *   sinkr_peer_ipc_handle  64-byte cudaIpcMemHandle of the block (all-gather it)
+ *   sinkr_peer_open        map every rank's block from the gathered handles
+ *   sinkr_peer_set_blocks  same, from device pointers (ranks in one process)
+ * All ranks must issue the same number of peer steps (the arrival counters
+ * are step-numbered); a rank that never arrives turns into a step-kernel error
+ * after 2 s, never a hang. */
+sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, size_t* block_bytes);
+sinkr_status sinkr_peer_ipc_handle(sinkr_engine* e, void* handle);
+sinkr_status sinkr_peer_open(sinkr_engine* e, const void* handles);
+sinkr_status sinkr_peer_set_blocks(sinkr_engine* e, void* const* blocks);
+void* sinkr_peer_block(sinkr_engine* e);
+sinkr_status sinkr_routed_decode_peer_async(sinkr_engine* e, const float* d_queries, size_t layer,
+                                            const sinkr_routing_config* config,
+                                            const sinkr_engine_options* options,
+                                            float* d_outputs);
+
 /* ---- instrumentation ------------------------------------------------------- */
 /* Launch count of the last step (kernels of this library) and the device
  * time (ms) of its decode kernel, measured with events on the engine stream. */

@@ -26,6 +26,7 @@ from .router import (  # noqa: F401
     last_step_stats,
     route,
     routed_decode_async,
+    routed_decode_peer_async,
     routed_decode_step,
     set_timing,
     split_ranges,

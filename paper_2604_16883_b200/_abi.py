@@ -109,6 +109,9 @@ EXPORTS = (
     # analysis (f4)
     "sinkr_attention_bos_mass", "sinkr_attention_weights", "sinkr_oracle_labels",
     "sinkr_pr_curve",
+    # fused sequence-sharded peer merge
+    "sinkr_peer_setup", "sinkr_peer_ipc_handle", "sinkr_peer_open", "sinkr_peer_set_blocks",
+    "sinkr_peer_block", "sinkr_routed_decode_peer_async",
 )
 
 _lib = None
@@ -134,6 +137,8 @@ def lib():
         L.sinkr_decode_grid.restype = C.c_int
         L.sinkr_decode_grid.argtypes = [C.c_void_p]
         L.sinkr_engine_destroy.argtypes = [C.c_void_p]
+        L.sinkr_peer_block.restype = C.c_void_p
+        L.sinkr_peer_block.argtypes = [C.c_void_p]
         L.sinkr_snkt_file_size.restype = C.c_uint64
         L.sinkr_snkt_file_size.argtypes = [C.c_void_p, c_size_t]
         L.sinkr_profile_default.restype = None
@@ -163,6 +168,11 @@ def lib():
             "sinkr_attention_bos_mass": [vp, vp, sz, vp],
             "sinkr_attention_weights": [vp, vp, sz, sz, sz, vp],
             "sinkr_pr_curve": [vp, vp, sz, vp, vp, vp],
+            "sinkr_peer_setup": [vp, C.c_uint32, C.c_uint32, vp],
+            "sinkr_peer_ipc_handle": [vp, vp],
+            "sinkr_peer_open": [vp, vp],
+            "sinkr_peer_set_blocks": [vp, vp],
+            "sinkr_routed_decode_peer_async": [vp, vp, sz, vp, vp, vp],
         }.items():
             getattr(L, name).argtypes = at
             getattr(L, name).restype = C.c_int if name != "sinkr_profile_default" else None

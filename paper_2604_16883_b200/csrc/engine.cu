@@ -131,6 +131,14 @@ struct sinkr_engine {
     uint32_t* d_route_flags = nullptr;  // distributed routing decisions [U]
     uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [U]
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
+    // sequence-sharded peer merge (mode 3): this rank's exchange block
+    // [2][world][U][PS] f32 + arrival counter, and every rank's block mapped here
+    uint8_t* d_xchg = nullptr;
+    size_t xchg_floats = 0, xchg_bytes = 0;
+    uint32_t world = 0, rank = 0;
+    float** d_peer_xchg = nullptr;          // device array [world]
+    unsigned int** d_peer_arrive = nullptr;  // device array [world]
+    std::vector<void*> ipc_opened;           // peer blocks opened through CUDA IPC
 
     CUtensorMap tmk{}, tmv{};
     CUtensorMap* d_tmap = nullptr;  // device copies of tmk, tmv (fused kernel)
@@ -223,6 +231,14 @@ struct sinkr_engine {
         t.mode = (uint32_t)mode;
         t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
         t.trace = d_trace;
+        if (mode == 3) {
+            t.peer_xchg = d_peer_xchg;
+            t.peer_arrive = d_peer_arrive;
+            t.xchg_local = reinterpret_cast<const float*>(d_xchg);
+            t.arrive_local = reinterpret_cast<const unsigned int*>(d_xchg + xchg_floats * 4);
+            t.world = world;
+            t.rank = rank;
+        }
         return t;
     }
     uint32_t* clocks() const { return reinterpret_cast<uint32_t*>(d_res + off_status) + 4; }
@@ -585,8 +601,9 @@ void fill_info(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg,
             static const char* what[] = {"", "partial spill-slot lock timeout",
                                          "merge watchdog: a group never completed",
                                          "routing grid-barrier watchdog",
-                                         "fp32 route estimate disagreed with the exact route"};
-            fail(SINKR_RUNTIME_ERROR, std::string("step kernel error: ") + (st[0] < 5 ? what[st[0]] : "unknown"));
+                                         "fp32 route estimate disagreed with the exact route",
+                                         "peer merge watchdog: a rank never delivered its partials"};
+            fail(SINKR_RUNTIME_ERROR, std::string("step kernel error: ") + (st[0] < 6 ? what[st[0]] : "unknown"));
         }
         if (clk[1] >= clk[0] && clk[2] >= clk[1] && clk[3] >= clk[2]) {
             c.routing_seconds = (clk[1] - clk[0]) * 1e-9;
@@ -675,6 +692,10 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->device = device;
             e->num_sms = prop.multiProcessorCount;
             e->grid = e->num_sms;
+            // SINKR_DEBUG_GRID: fewer persistent CTAs (tests run two engines'
+            // cooperative kernels side by side on one GPU)
+            if (const char* dg = std::getenv("SINKR_DEBUG_GRID"); dg && std::atoi(dg) > 0)
+                e->grid = std::min(e->grid, std::atoi(dg));
             const size_t rows = e->layers * e->B * c.num_kv_heads * e->cap;
             if (rows >= (size_t(1) << 31))
                 fail(SINKR_INVALID_ARGUMENT, "cache exceeds 2^31 rows (TMA coordinate range)");
@@ -825,6 +846,10 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_cursor);
     cudaFree(e->d_tokens_done);
     cudaFree(e->d_route_flags);
+    for (void* pb : e->ipc_opened) cudaIpcCloseMemHandle(pb);
+    cudaFree(e->d_xchg);
+    cudaFree(e->d_peer_xchg);
+    cudaFree(e->d_peer_arrive);
     cudaFree(e->d_ovf);
     cudaFree(e->d_head_degen);
     cudaFree(e->d_active);
@@ -1338,6 +1363,94 @@ sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gat
         launch_combine(e, t, d_gathered, e->PS, e->U * e->PS, (uint32_t)num_ranks, d_outputs, 0,
                        num_ranks);
         CK(cudaGetLastError());
+    });
+}
+
+// ---- fused sequence-sharded merge over peer memory (mode 3) ------------------
+static void peer_tables(sinkr_engine* e, const std::vector<uint8_t*>& blocks) {
+    std::vector<float*> px(e->world);
+    std::vector<unsigned int*> pa(e->world);
+    for (uint32_t q = 0; q < e->world; ++q) {
+        px[q] = reinterpret_cast<float*>(blocks[q]);
+        pa[q] = reinterpret_cast<unsigned int*>(blocks[q] + e->xchg_floats * 4);
+    }
+    if (!e->d_peer_xchg) CK(cudaMalloc(&e->d_peer_xchg, 8 * sizeof(float*)));
+    if (!e->d_peer_arrive) CK(cudaMalloc(&e->d_peer_arrive, 8 * sizeof(unsigned int*)));
+    CK(cudaMemcpy(e->d_peer_xchg, px.data(), e->world * sizeof(float*), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(e->d_peer_arrive, pa.data(), e->world * sizeof(unsigned int*), cudaMemcpyHostToDevice));
+}
+
+sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, size_t* block_bytes) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        if (world == 0 || world > 8 || rank >= world)
+            fail(SINKR_INVALID_ARGUMENT, "peer merge needs 1 <= world <= 8 and rank < world");
+        if (!e->fused) fail(SINKR_INVALID_ARGUMENT, "peer merge needs the fused step kernel");
+        CK(cudaSetDevice(e->device));
+        if (e->d_xchg) fail(SINKR_LOGIC_ERROR, "peer merge already set up");
+        e->world = world;
+        e->rank = rank;
+        e->xchg_floats = 2ull * world * e->U * e->PS;
+        e->xchg_bytes = align_up(e->xchg_floats * 4, 256) + 256;
+        CK(cudaMalloc(&e->d_xchg, e->xchg_bytes));
+        CK(cudaMemset(e->d_xchg, 0, e->xchg_bytes));
+        if (block_bytes) *block_bytes = e->xchg_bytes;
+    });
+}
+
+sinkr_status sinkr_peer_ipc_handle(sinkr_engine* e, void* handle) {
+    return guard([&] {
+        if (!e || !handle || !e->d_xchg) fail(SINKR_INVALID_ARGUMENT, "peer merge not set up");
+        CK(cudaSetDevice(e->device));
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, e->d_xchg));
+        std::memcpy(handle, &h, sizeof(h));
+    });
+}
+
+sinkr_status sinkr_peer_open(sinkr_engine* e, const void* handles) {
+    return guard([&] {
+        if (!e || !handles || !e->d_xchg) fail(SINKR_INVALID_ARGUMENT, "peer merge not set up");
+        CK(cudaSetDevice(e->device));
+        std::vector<uint8_t*> blocks(e->world);
+        for (uint32_t q = 0; q < e->world; ++q) {
+            if (q == e->rank) {
+                blocks[q] = e->d_xchg;
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const uint8_t*>(handles) + q * sizeof(h), sizeof(h));
+            void* ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            e->ipc_opened.push_back(ptr);
+            blocks[q] = static_cast<uint8_t*>(ptr);
+        }
+        peer_tables(e, blocks);
+    });
+}
+
+sinkr_status sinkr_peer_set_blocks(sinkr_engine* e, void* const* blocks) {
+    return guard([&] {
+        if (!e || !blocks || !e->d_xchg) fail(SINKR_INVALID_ARGUMENT, "peer merge not set up");
+        CK(cudaSetDevice(e->device));
+        std::vector<uint8_t*> b(e->world);
+        for (uint32_t q = 0; q < e->world; ++q) b[q] = static_cast<uint8_t*>(blocks[q]);
+        peer_tables(e, b);
+    });
+}
+
+void* sinkr_peer_block(sinkr_engine* e) { return e ? e->d_xchg : nullptr; }
+
+sinkr_status sinkr_routed_decode_peer_async(sinkr_engine* e, const float* d_queries, size_t layer,
+                                            const sinkr_routing_config* config,
+                                            const sinkr_engine_options* options,
+                                            float* d_outputs) {
+    return guard([&] {
+        if (!e || !d_queries || !d_outputs) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        if (!e->d_peer_xchg) fail(SINKR_INVALID_ARGUMENT, "peer merge not set up (sinkr_peer_open)");
+        CK(cudaSetDevice(e->device));
+        stage_params(e, layer, config, options, false);
+        run_graph(e, d_queries, d_outputs, 3);
     });
 }
 

@@ -41,7 +41,8 @@ struct StepState {
     unsigned int exit_count;
     unsigned int error;
     unsigned int route_done;  // CTAs that published their units' decisions (distributed routing)
-    unsigned int pad[3];
+    unsigned int peer_epoch;  // mode 3: steps completed (advanced by the last CTA at exit)
+    unsigned int pad[2];
 };
 
 struct StepTables {
@@ -68,7 +69,15 @@ struct StepTables {
     uint32_t* ovf;                 // [U] spill-slot lock (bit0) + valid (bit1)
     float* partials;               // [U][S][r*(D+2)]: m[r], l[r], acc[r][D]
     float* out;                    // mode 0: [B][Hq][D]; mode 1: [U][r][D+2]
-    uint32_t B, Hq, Hkv, r, cap, S, mode;
+    uint32_t B, Hq, Hkv, r, cap, S, mode;  // mode 0 outputs, 1 rank partial, 3 peer merge
+    // mode 3 (sequence-sharded peer merge over NVLink): every rank's exchange
+    // block holds [2][world][U][r*(D+2)] rank partials (step parity) + an
+    // arrival counter
+    float* const* peer_xchg;              // [world] partial areas of every rank's block
+    unsigned int* const* peer_arrive;     // [world] arrival counters of every rank's block
+    const float* xchg_local;              // this rank's partial area
+    const unsigned int* arrive_local;     // this rank's arrival counter
+    uint32_t world, rank;
     float qscale;                  // (1/sqrt(D)) * log2(e)
     unsigned long long* trace;     // optional [grid][4] per-CTA globaltimer stamps
 };
@@ -120,7 +129,7 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 // rank partial (mode 1).
 template <int D>
 __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
-                                           uint32_t lane) {
+                                           uint32_t lane, size_t xoff) {
     const uint32_t r = t.r, PS = r * (D + 2);
     const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
     const float* base = t.partials + size_t(u) * t.S * PS;
@@ -161,13 +170,22 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
     }
     if (t.mode == 0) {
         t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
-    } else {
+    } else if (t.mode == 1) {
         float* P = t.out + size_t(u) * PS;
         if (d == 0) {
             P[h] = mx;
             P[r + h] = lsum;
         }
         P[2 * r + h * D + d] = acc;
+    } else {  // mode 3: this rank's partial straight into every rank's exchange block
+        for (uint32_t q = 0; q < t.world; ++q) {
+            float* P = t.peer_xchg[q] + xoff + size_t(u) * PS;
+            if (d == 0) {
+                P[h] = mx;
+                P[r + h] = lsum;
+            }
+            P[2 * r + h * D + d] = acc;
+        }
     }
 }
 
@@ -769,9 +787,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // many groups: the CTA that streams a group's last rows merges it.
     const bool queue_mode = 4 * nact <= G;
     const bool lean_fast = lean && misc[kMiscFast] != 0;
+    // mode 3: partial slots double-buffered by step parity (a rank one step
+    // ahead never overwrites partials a slower rank is still merging).  The
+    // step number lives on the device (advanced by the last CTA at exit, after
+    // every CTA has read it), so the graph needs no per-step parameter patch.
+    const uint32_t epoch = t.mode == 3 ? ld_volatile(&t.ss->peer_epoch) : 0u;
+    const size_t xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
     // zero surrogate rows of Sink groups (router.cpp:97): sink unit u is
     // written by CTA u mod G (binary search of the sorted Active list)
-    if (lean && t.mode == 0 && nact < U) {  // (the distributed form's owners did it)
+    if (lean && t.mode != 1 && nact < U) {  // (the distributed form's owners did it)
         for (uint32_t u = bid; u < U; u += G) {
             uint32_t lo = 0, hi = nact;
             while (lo < hi) {
@@ -1059,7 +1083,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // merge every partial of unit u (consumers only; few partials)
         auto merge_unit = [&](uint32_t u, uint32_t L) {
             for (uint32_t task = cw; task < r * (D / 32); task += kCWarps)
-                warp_merge<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane);
+                warp_merge<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff);
             if (ctid == 0) t.tokens[u] = L;
         };
         auto flush = [&](uint32_t u, uint32_t L) {
@@ -1272,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
             }
             __syncwarp();
-            warp_merge<D>(t, u, h, d - lane, lane);
+            warp_merge<D>(t, u, h, d - lane, lane, xoff);
             if (h == 0 && d == 0) t.tokens[u] = L;
         }
     }
@@ -1282,10 +1306,60 @@ __global__ void __launch_bounds__(kThreads, 1)
     STAMP(10);
     if (t.trace && tid == 0) t.trace[bid * 8 + 2] = globaltimer();
     if (tid == 0) {
-        __threadfence();
+        if (t.mode == 3) __threadfence_system();  // this CTA's peer stores before the count
+        else __threadfence();
         misc[kMiscLast] = (atomicAdd(&t.ss->exit_count, 1u) == G - 1) ? 1u : 0u;
     }
     __syncthreads();
+    if (t.mode == 3) {
+        // every CTA's partial stores are fenced (system scope) and counted: the
+        // last CTA tells every rank (NVLink atomics); then ALL CTAs wait for
+        // every rank's partials of this step and merge a share of the outputs
+        if (misc[kMiscLast] && tid < t.world) {
+            unsigned int* ctr = t.peer_arrive[tid];
+            asm volatile("red.release.sys.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
+        }
+        if (tid == 0) {
+            const unsigned int want = (epoch + 1u) * t.world;
+            const unsigned long long t_spin = globaltimer();
+            for (;;) {
+                unsigned int v;
+                asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(t.arrive_local) : "memory");
+                if ((int)(v - want) >= 0) break;
+                if (globaltimer() - t_spin > 2000000000ull) {
+                    atomicExch(&t.ss->error, 5u);
+                    break;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t PSx = r * (D + 2);
+        const float* X = t.xchg_local + size_t((epoch & 1u) * t.world) * U * PSx;
+        for (uint32_t e = bid * kThreads + tid; e < nact * r * D; e += G * kThreads) {
+            const uint32_t a = e / (r * D), h = (e / D) % r, d = e % D;
+            const uint32_t u = act_unit[a];
+            float mq[8], aq[8], lq[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const bool ok = (uint32_t)q < t.world;
+                const float* Pq = X + (size_t(q) * U + u) * PSx;
+                mq[q] = ok ? __ldcg(Pq + h) : -INFINITY;
+                lq[q] = ok ? __ldcg(Pq + r + h) : 0.f;
+                aq[q] = ok ? __ldcg(Pq + 2 * r + h * D + d) : 0.f;
+            }
+            float mx = mq[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) mx = fmaxf(mx, mq[q]);
+            float acc = 0.f, lsum = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float w = mq[q] == -INFINITY ? 0.f : ptx::ex2(mq[q] - mx);
+                acc += aq[q] * w;
+                lsum += lq[q] * w;
+            }
+            t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
+        }
+    }
     STAMP(11);
     if (misc[kMiscLast]) {
         __threadfence();
@@ -1306,6 +1380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             t.ss->merge_next = 0;
             t.ss->exit_count = 0;
             t.ss->route_done = 0;
+            if (t.mode == 3) t.ss->peer_epoch = epoch + 1u;
         }
     }
 }

@@ -448,6 +448,18 @@ def merge_rank_partials_async(cache: KvCache, d_gathered: int, num_ranks: int,
                                                 C.c_size_t(num_ranks), C.c_void_p(d_outputs)))
 
 
+def routed_decode_peer_async(d_queries: int, layer: int, cache: KvCache, config: RoutingConfig,
+                             options: Optional[EngineOptions], d_outputs: int) -> None:
+    """Sequence-sharded step with the merge fused into the kernel (peer memory);
+    needs sharding.PeerMerge set up on every rank."""
+    c, keep = config._c()
+    o = (options or EngineOptions())._c()
+    check(lib().sinkr_routed_decode_peer_async(cache.handle, C.c_void_p(d_queries),
+                                               C.c_size_t(layer), C.byref(c), C.byref(o),
+                                               C.c_void_p(d_outputs)))
+    del keep
+
+
 KvCache.rank_partial_floats = rank_partial_floats
 
 

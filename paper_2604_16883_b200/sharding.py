@@ -79,6 +79,55 @@ def anchor_norm(k0) -> float:
     return float(np.float32(math.sqrt(s)))
 
 
+class PeerMerge:
+    """The fused alternative to all-gather + combine: each rank's step kernel
+    writes its LSE partials straight into every rank's exchange block (CUDA IPC
+    mappings over NVLink) and merges all ranks' partials itself.  Set up once
+    per engine; then `step` is one kernel launch per rank per step.
+
+    One process per rank: PeerMerge(P, cache, world, rank, dist, torch) exchanges
+    the blocks' CUDA IPC handles over the process group.  Ranks in one process
+    (tests): peer_merge_in_process(P, caches)."""
+
+    def __init__(self, P, cache, world: int, rank: int, dist=None, torch=None):
+        import ctypes as C
+
+        from ._abi import check, lib
+
+        self.P, self.cache, self.world = P, cache, world
+        nbytes = C.c_size_t()
+        check(lib().sinkr_peer_setup(cache.handle, world, rank, C.byref(nbytes)))
+        self.block = lib().sinkr_peer_block(cache.handle)
+        if dist is not None:
+            h = (C.c_uint8 * 64)()
+            check(lib().sinkr_peer_ipc_handle(cache.handle, h))
+            mine = torch.tensor(list(bytes(h)), dtype=torch.uint8, device="cuda")
+            allh = torch.empty(world * 64, dtype=torch.uint8, device="cuda")
+            dist.all_gather_into_tensor(allh, mine)
+            buf = (C.c_uint8 * (world * 64))(*allh.cpu().tolist())
+            check(lib().sinkr_peer_open(cache.handle, buf))
+
+    def connect_local(self, blocks) -> None:
+        import ctypes as C
+
+        from ._abi import check, lib
+
+        arr = (C.c_void_p * self.world)(*blocks)
+        check(lib().sinkr_peer_set_blocks(self.cache.handle, arr))
+
+    def step(self, dq, dout, cfg, opts, layer: int = 0):
+        self.P.routed_decode_peer_async(dq.data_ptr(), layer, self.cache, cfg, opts, dout.data_ptr())
+
+
+def peer_merge_in_process(P, caches):
+    """Peer merge between engines of one process (same or different GPUs)."""
+    world = len(caches)
+    pms = [PeerMerge(P, c, world, k) for k, c in enumerate(caches)]
+    for pm in pms:
+        pm.connect_local([x.block for x in pms])
+    return pms
+
+
 def sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world: int):
     """One sequence-sharded decode step on this rank's engine stream."""
     P.decode_rank_partial_async(dq.data_ptr(), 0, cache, cfg, opts, partial.data_ptr())
@@ -106,6 +155,23 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
     partial = torch.empty(nf, dtype=torch.float32, device="cuda")
     gathered = torch.empty(world * nf, dtype=torch.float32, device="cuda")
     stream = torch.cuda.ExternalStream(cache.stream)
+    # the merge fused into the step kernel over peer memory; NCCL all-gather +
+    # combine kernel when peer mappings are unavailable (both timed below)
+    pm, peer_err = None, None
+    try:
+        pm = PeerMerge(P, cache, world, rank, dist, torch)
+    except Exception as ex:  # no P2P / IPC on this node
+        peer_err = f"{type(ex).__name__}: {ex}"
+    ok = torch.tensor([0 if pm is None else 1], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 0:
+        pm = None
+
+    def step(cfg):
+        if pm is not None:
+            pm.step(dq, dout, cfg, opts)
+        else:
+            sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world)
 
     def maxed(x: float) -> float:
         t = torch.tensor([x], device="cuda")
@@ -116,7 +182,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
     clocks = None
     for name, cfg in (("routed", routed_cfg), ("dense", dense_cfg)):
         for _ in range(max(3, args.warmup)):
-            sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world)
+            step(cfg)
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
@@ -127,7 +193,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
             sampler.__enter__()
         e0.record(stream)
         for _ in range(args.steps):
-            sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, world)
+            step(cfg)
         e1.record(stream)
         torch.cuda.synchronize()
         if sampler:
@@ -138,11 +204,27 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         if name == "routed":
             n_act = P.fetch_step_info(cache).counters.groups_active
 
+    # the all-gather + combine path beside it (same steps, same clock)
+    nccl_us = None
+    if pm is not None:
+        for _ in range(3):
+            sharded_step(P, torch, dist, cache, routed_cfg, opts, dq, partial, gathered, dout, world)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            sharded_step(P, torch, dist, cache, routed_cfg, opts, dq, partial, gathered, dout, world)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        nccl_us = maxed(e0.elapsed_time(e1) / args.steps) * 1e3
+
     # e2e: host queries in (pinned H2D), sharded step, host outputs out, per step
     for _ in range(2):
         with torch.cuda.stream(stream):
             dq.copy_(q_host, non_blocking=True)
-        sharded_step(P, torch, dist, cache, routed_cfg, opts, dq, partial, gathered, dout, world)
+        step(routed_cfg)
         with torch.cuda.stream(stream):
             out_host.copy_(dout, non_blocking=True)
         stream.synchronize()
@@ -151,7 +233,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             dq.copy_(q_host, non_blocking=True)
-        sharded_step(P, torch, dist, cache, routed_cfg, opts, dq, partial, gathered, dout, world)
+        step(routed_cfg)
         with torch.cuda.stream(stream):
             out_host.copy_(dout, non_blocking=True)
         stream.synchronize()
@@ -174,7 +256,9 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         "data": "synthetic planted-sink KV (device generator, seeded); fp32 queries",
         "config": {"workload": f"llama3.1-8b-attn L={spec.length} B=1 "
                                f"routed={spec.sink_fraction} sequence-sharded",
-                   "parallelism": f"sequence-shard x{world} + NCCL all-gather LSE merge",
+                   "parallelism": (f"sequence-shard x{world} + LSE merge fused into the step kernel "
+                                   "over peer memory (NVLink)") if pm is not None else
+                                  f"sequence-shard x{world} + NCCL all-gather + combine kernel",
                    "context": spec.length, "tokens_per_rank": hi - lo,
                    "l2": "per-rank KV larger than L2 at N <= 8"},
         "dense_us_per_step": round(res["dense"] * 1e3, 2),
@@ -189,7 +273,9 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         "e2e": {"value": round(e2e_us, 2), "unit": "us/step",
                 "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes},
-        "gpu_launches": 2 * args.steps,  # rank-partial step kernel + LSE combine (NCCL's own not counted)
+        "gpu_launches": (1 if pm is not None else 2) * args.steps,  # ours only (NCCL's not counted)
+        "allgather_combine_us_per_step": round(nccl_us, 2) if nccl_us is not None else None,
+        "peer_merge_unavailable": peer_err,
         "clocks": clocks,
         "note": json.dumps({"partial_bytes_per_rank": nf * 4}),
     }

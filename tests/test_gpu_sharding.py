@@ -73,3 +73,65 @@ def test_unit_shards_match_single():
                 res = P.routed_decode_step(q[a * r:b * r], 0, part, cfg)
                 assert np.array_equal(res.route_bitmap, ref.route_bitmap[a:b])
                 np.testing.assert_allclose(res.outputs, ref.outputs[a * r:b * r], atol=1e-6)
+
+
+def _one_gpu_peer_setup(P, caches):
+    return sharding.peer_merge_in_process(P, caches)
+
+
+def test_peer_merge_world1_matches_fused_step():
+    """The fused peer-merge step at world 1 (the kernel writes its partial into
+    its own exchange block, counts itself in, merges) equals the plain step,
+    over several steps (step-parity buffers, monotonic arrival counters)."""
+    spec = WorkloadSpec(length=40000, sink_fraction=0.5, seed=3)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as cache:
+        spec.fill(cache)
+        q = torch.from_numpy(spec.queries()[0]).cuda()
+        ref = torch.empty_like(q)
+        P.routed_decode_async(q.data_ptr(), 0, cache, cfg, d_outputs=ref.data_ptr())
+        torch.cuda.synchronize()
+        (pm,) = _one_gpu_peer_setup(P, [cache])
+        out = torch.empty_like(q)
+        for _ in range(5):
+            out.fill_(float("nan"))
+            pm.step(q, out, cfg, P.EngineOptions())
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref) or (out - ref).abs().max().item() <= 1e-6
+        info = P.fetch_step_info(cache)
+        assert info.counters.groups_skipped == 4
+
+
+@pytest.mark.parametrize("world", [2])
+def test_peer_merge_two_ranks_on_one_gpu(world, monkeypatch):
+    """Two sequence-shard engines on one GPU, each with half the SMs
+    (SINKR_DEBUG_GRID), exchanging partials through each other's blocks inside
+    their step kernels: both produce the single-engine step's outputs."""
+    from paper_2604_16883_b200 import sharding
+
+    monkeypatch.setenv("SINKR_DEBUG_GRID", "74")
+    L = 65536
+    spec = WorkloadSpec(length=L, sink_fraction=0.625, seed=8)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    q = torch.from_numpy(spec.queries()[0]).cuda()
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, L)) as full:
+        spec.fill(full)
+        ref = torch.empty_like(q)
+        P.routed_decode_async(q.data_ptr(), 0, full, cfg, d_outputs=ref.data_ptr())
+        torch.cuda.synchronize()
+    shards = [sharding.build_sequence_shard(P, spec, k, world, 0)[0] for k in range(world)]
+    pms = _one_gpu_peer_setup(P, shards)
+    opts = P.EngineOptions(global_context_len=L)
+    outs = [torch.empty_like(q) for _ in range(world)]
+    for _ in range(3):
+        for pm, o in zip(pms, outs):
+            o.fill_(float("nan"))
+            pm.step(q, o, cfg, opts)
+        torch.cuda.synchronize()
+        for o in outs:
+            assert (o - ref).abs().max().item() <= 2e-3
+            assert torch.linalg.norm(o - ref).item() <= 1e-3 * torch.linalg.norm(ref).item()
+    for s_ in shards:
+        info = P.fetch_step_info(s_)
+        assert info.counters.groups_skipped == 5
+        s_.close()
