@@ -1,20 +1,25 @@
 // step.cuh — the whole SinkRouter decode step in ONE persistent, cooperative
 // sm_100a kernel (one CTA per SM):
 //
-//   phase R  routing (router.cpp:36-75,100-125): every CTA redundantly scores
-//            the query heads against the cached token-0 keys (exact fp64
-//            products, sequential sums, IEEE sqrt/div — bit-exact with the
-//            reference), takes the sequential group mean, compares with tau
-//            and compacts the Active groups into a work list in its own shared
-//            memory.  No inter-CTA traffic; CTA 0 publishes the routing record.
+//   phase R  routing (router.cpp:36-75,100-125).  Single-sequence steps: every
+//            CTA scores the query heads against the cached token-0 keys itself
+//            (no inter-CTA traffic) -- an fp32 estimate decides when every
+//            group clears tau by kRouteMargin, else the exact fp64 scores
+//            (products exact, sequential sums, IEEE sqrt/div: bit-exact with
+//            the reference) decide first.  Batched steps: each CTA scores its
+//            share of the groups, one grid barrier.  The exact record (head and
+//            group scores) is always published; the Active groups form a work
+//            list in every CTA's shared memory.
 //   phase S  Split-K flash-decode (attend_chunk, attention.cpp:101-142) over the
 //            Active groups only: TMA producer warp + 4 mma.sync consumer warps
-//            per CTA, unit-affine dynamic chunk claims (or guided claims over
-//            one global token space when there are more Active groups than SMs).
+//            per CTA, unit-affine guided claims (or guided claims over one
+//            global token space when there are more Active groups than SMs).
 //   phase M  LSE merge (merge_partials, attention.cpp:159-183): with few Active
-//            groups the (group, head, 32-dim) merge tasks are spread over all
-//            CTAs once a group's last row has been streamed; with many groups
-//            the CTA that streams a group's last rows merges it.
+//            groups the (group, head, 32-dim) slices are claimed by warps once
+//            a group's last row has been counted; with many groups the CTA that
+//            streams a group's last rows merges it.  Mode 3 writes the rank
+//            partials into every rank's exchange block instead and merges all
+//            ranks' partials after a cross-GPU arrival count.
 //
 // The last CTA to leave restores the cross-CTA counters to zero for the next
 // step, so the launch needs no memset and replays as a single graph node.
@@ -28,7 +33,6 @@ namespace dev {
 constexpr int kMaxUnits = 1280;      // B * H_kv per step (LLaVA-13B B=32 x 40)
 constexpr int kMaxStepHeads = 4096;  // B * H_q per step
 constexpr int kRouteTile = 64;       // heads per routing tile
-constexpr int kRouteSub = 32;        // heads per load batch
 constexpr uint32_t kFlatMinTok = 512;  // smallest claim of the global token-space scheduler
 // an fp32 estimate of a group score decides the route when it clears tau by
 // this much (its own error is ~1e-6); closer calls wait for the exact score
@@ -107,7 +111,7 @@ struct StepCfg {
 };
 
 // misc smem words
-enum : int { kMiscNact = 0, kMiscChunk, kMiscQueue, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast };
+enum : int { kMiscNact = 0, kMiscChunk, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast };
 
 
 __device__ __forceinline__ unsigned long long globaltimer() {
