@@ -126,11 +126,11 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 
 // One warp LSE-merges the n Split-K partials of (unit, head h) for the 32
 // dims d0 .. d0+31 (merge_partials, attention.cpp:159-183): partials come in
-// groups of 96 -- lane j holds (m, l) of partials j, j+32, j+64, every lane
-// holds its dim of all 96 acc rows, all loads of a group in flight at once --
-// and the weights 2^(m_j - max) reach the lanes by shuffle.  One L2 round trip
-// per 96 partials.  Writes the normalised row (mode 0) or an un-normalised
-// rank partial (mode 1).
+// groups of 64 -- lane j holds (m, l) of partials j, j+32, every lane holds its
+// dim of all 64 acc rows, all loads of a group in flight at once -- and the
+// weights 2^(m_j - max) reach the lanes by shuffle.  One L2 round trip per 64
+// partials.  Writes the normalised row (mode 0), an un-normalised rank partial
+// (mode 1), or that partial into every rank's exchange block (mode 3).
 template <int D>
 __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
                                            uint32_t lane, size_t xoff) {
@@ -139,18 +139,18 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
     const float* base = t.partials + size_t(u) * t.S * PS;
     const uint32_t d = d0 + lane;
     float mx = -INFINITY, lsum = 0.f, acc = 0.f;
-    for (uint32_t j0 = 0; j0 < n; j0 += 96) {
-        float mv[3], lv[3], av[96];
+    for (uint32_t j0 = 0; j0 < n; j0 += 64) {
+        float mv[2], lv[2], av[64];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < 2; ++c) {
             const uint32_t j = j0 + 32 * c + lane;
             mv[c] = j < n ? __ldcg(base + size_t(j) * PS + h) : -INFINITY;
             lv[c] = j < n ? __ldcg(base + size_t(j) * PS + r + h) : 0.f;
         }
 #pragma unroll
-        for (int k = 0; k < 96; ++k)
+        for (int k = 0; k < 64; ++k)
             av[k] = (j0 + k < n) ? __ldcg(base + size_t(j0 + k) * PS + 2 * r + h * D + d) : 0.f;
-        float cm = fmaxf(fmaxf(mv[0], mv[1]), mv[2]);
+        float cm = fmaxf(mv[0], mv[1]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
         const float nm = fmaxf(mx, cm);
@@ -160,9 +160,9 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
             lsum *= sc;
             mx = nm;
         }
-        float w[3], lw = 0.f;
+        float w[2], lw = 0.f;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < 2; ++c) {
             w[c] = mv[c] == -INFINITY ? 0.f : ptx::ex2(mv[c] - mx);
             lw += lv[c] * w[c];
         }
@@ -170,7 +170,7 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
         for (int o = 16; o > 0; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
         lsum += lw;
 #pragma unroll
-        for (int k = 0; k < 96; ++k) acc += av[k] * __shfl_sync(0xffffffffu, w[k / 32], k % 32);
+        for (int k = 0; k < 64; ++k) acc += av[k] * __shfl_sync(0xffffffffu, w[k / 32], k % 32);
     }
     if (t.mode == 0) {
         t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
@@ -1274,7 +1274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= phase M: distributed merge ========================
     // Tasks (active entry, head, 32-dim slice) are claimed by WARPS: a warp
     // waits until its unit's last rows are counted, then merges the slice with
-    // warp_merge (one L2 round trip per 96 partials, no block barrier).
+    // warp_merge (one L2 round trip per 64 partials, no block barrier).
     if (queue_mode && nact > 0) {
         constexpr uint32_t nd = D / 32;
         const uint32_t ntasks = nact * r * nd;
