@@ -683,9 +683,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         P[r + h] = 0.f;
                     }
                     for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
-                } else {  // zero surrogate rows (router.cpp:97), written by the owner
-                    float4* row = reinterpret_cast<float4*>(t.out + size_t(u) * r * D);
-                    for (uint32_t k = 0; k < r * D / 4; ++k) row[k] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
         }
@@ -797,20 +794,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // every CTA has read it), so the graph needs no per-step parameter patch.
     const uint32_t epoch = t.mode == 3 ? ld_volatile(&t.ss->peer_epoch) : 0u;
     const size_t xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
-    // zero surrogate rows of Sink groups (router.cpp:97): sink unit u is
-    // written by CTA u mod G (binary search of the sorted Active list)
-    if (lean && t.mode != 1 && nact < U) {  // (the distributed form's owners did it)
-        for (uint32_t u = bid; u < U; u += G) {
-            uint32_t lo = 0, hi = nact;
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (act_unit[mid] < u) lo = mid + 1; else hi = mid;
-            }
-            if (lo < nact && act_unit[lo] == u) continue;
-            float4* row = reinterpret_cast<float4*>(t.out + size_t(u) * r * D);
-            for (uint32_t k = tid; k < r * D / 4; k += kThreads) row[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    }
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
     if (t.trace && tid == 0) t.trace[bid * 8 + 0] = globaltimer();
@@ -972,6 +955,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------ consumers ------------------------------
         const int cw = warp - 1;
         const uint32_t ctid = tid - 32;
+        // zero surrogate rows of Sink groups (router.cpp:97), written while the
+        // first stages are in flight: single-sequence steps, CTA u mod G for
+        // unit u (binary search of the sorted Active list); batched steps, the
+        // CTA that routed the unit
+        if (t.mode != 1 && nact < U) {
+            uint32_t z_lo = bid, z_step = G, z_hi = U;
+            if (!lean) {
+                const uint32_t up = (U + G - 1) / G;
+                z_lo = min(U, bid * up);
+                z_hi = min(U, z_lo + up);
+                z_step = 1;
+            }
+            for (uint32_t u = z_lo; u < z_hi; u += z_step) {
+                bool sink;
+                if (lean) {
+                    uint32_t lo = 0, hi = nact;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (act_unit[mid] < u) lo = mid + 1; else hi = mid;
+                    }
+                    sink = !(lo < nact && act_unit[lo] == u);
+                } else {
+                    sink = !(__ldcg(&t.route_flags[u]) & kActive);
+                }
+                if (!sink) continue;
+                float4* row = reinterpret_cast<float4*>(t.out + size_t(u) * r * D);
+                for (uint32_t k = ctid; k < r * D / 4; k += kCWarps * 32) row[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
         if ((lean_fast && lead) || exact_later) {
             // the routing record's exact fp64 scores (the decisions were taken
             // from fp32 estimates that cleared tau by kRouteMargin), computed
