@@ -101,9 +101,11 @@ class PeerMerge:
         if dist is not None:
             h = (C.c_uint8 * 64)()
             check(lib().sinkr_peer_ipc_handle(cache.handle, h))
-            mine = torch.tensor(list(bytes(h)), dtype=torch.uint8, device="cuda")
-            allh = torch.empty(world * 64, dtype=torch.uint8, device="cuda")
-            dist.all_gather_into_tensor(allh, mine)
+            dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+            mine = torch.tensor(list(bytes(h)), dtype=torch.uint8, device=dev)
+            parts = [torch.empty(64, dtype=torch.uint8, device=dev) for _ in range(world)]
+            dist.all_gather(parts, mine)
+            allh = torch.cat(parts)
             buf = (C.c_uint8 * (world * 64))(*allh.cpu().tolist())
             check(lib().sinkr_peer_open(cache.handle, buf))
 

@@ -135,3 +135,25 @@ def test_peer_merge_two_ranks_on_one_gpu(world, monkeypatch):
         info = P.fetch_step_info(s_)
         assert info.counters.groups_skipped == 5
         s_.close()
+
+
+def test_peer_merge_across_processes_ipc():
+    """The fused peer merge between two PROCESSES (one engine each, CUDA IPC
+    mappings of each other's exchange blocks, gloo for the handle exchange), on
+    one GPU with half the SMs each: both ranks reproduce the unsharded step."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ, SINKR_DEBUG_GRID="74")
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", str(port), os.path.join(root, "scripts", "ipc_peer_check.py")],
+                         capture_output=True, text=True, timeout=240, env=env, cwd=root)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
+    assert "rank 0 ok" in res.stdout and "rank 1 ok" in res.stdout
