@@ -1322,9 +1322,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     STAMP(10);
     if (t.trace && tid == 0) t.trace[bid * 8 + 2] = globaltimer();
     if (tid == 0) {
-        if (t.mode == 3) __threadfence_system();  // this CTA's peer stores before the count
-        else __threadfence();
-        misc[kMiscLast] = (atomicAdd(&t.ss->exit_count, 1u) == G - 1) ? 1u : 0u;
+        // gpu-scope acq_rel count: releases this CTA's writes (ordered before
+        // tid 0 by the barrier) and, for the last CTA, acquires everyone's
+        if (t.mode == 3) __threadfence_system();  // peer stores reach system scope first
+        misc[kMiscLast] = (ptx::atom_add_acq_rel(&t.ss->exit_count, 1u) == G - 1) ? 1u : 0u;
     }
     __syncthreads();
     if (t.mode == 3) {
@@ -1378,7 +1379,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     STAMP(11);
     if (misc[kMiscLast]) {
-        __threadfence();
         for (uint32_t a = tid; a < nact; a += kThreads) {
             const uint32_t u = act_unit[a];
             t.cursor[a] = 0;
