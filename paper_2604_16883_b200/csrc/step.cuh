@@ -1054,6 +1054,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (degen) sink = false;
                 const bool active = (flags & kObserveOnly) || !sink;
                 t.group_scores[u] = S;
+                // the exact flags (the estimate pass cannot see a degenerate head
+                // when observe-only or an excluded layer made every decision certain)
+                t.unit_flags[u] = (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
                 const bool taken = lean ? act_prefix[u] != 0u : (t.route_flags[u] & kActive) != 0u;
                 if (active != taken) atomicExch(&t.ss->error, 4u);  // never: margin >> error
             }

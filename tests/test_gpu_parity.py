@@ -342,3 +342,65 @@ def test_partial_spill_slot(oracle_libs, monkeypatch, slots):
         assert [g.kv_floats_loaded for g in r_.groups] == list(ref.group_kv_floats)
         assert np.abs(r_.outputs - ref.outputs).max() <= 2e-3
         assert np.linalg.norm(r_.outputs - ref.outputs) <= 1e-3 * np.linalg.norm(ref.outputs)
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_randomized_parity(oracle_libs, seed):
+    """SPEC.md acceptance 1-2 style: random shapes (D 32/64/128, r 1-8, B 1-3,
+    L 1-5000), random keys and queries at random cosines to the anchor (so
+    groups land on both sides of tau and near it), random routing options
+    (tau, sink_on_tie, observe_only, excluded layers) -- bit-exact routing,
+    exact skipped-block record, outputs within tolerance of the oracle."""
+    import oracle
+
+    _, orc = oracle_libs
+    rng = np.random.default_rng(1000 + seed)
+    D = int(rng.choice([32, 64, 128]))
+    r = int(rng.choice([1, 2, 3, 4, 8]))
+    hkv = int(rng.choice([1, 2, 4, 8]))
+    B = int(rng.choice([1, 1, 2, 3]))
+    L = int(rng.choice([1, 2, 63, 64, 65, 777, 2048, 5000]))
+    layers = 2
+    layer = int(rng.integers(layers))
+    hq = hkv * r
+    cc = P.CacheConfig(layers, hq, hkv, D, L, B)
+    k = rng.standard_normal((B, layers, hkv, L, D)).astype(np.float32) * np.float32(rng.uniform(0.5, 3))
+    v = rng.standard_normal((B, layers, hkv, L, D)).astype(np.float32)
+    q = np.zeros((B, hq, D), np.float32)
+    for b in range(B):
+        for g in range(hkv):
+            kh = k[b, layer, g, 0].astype(np.float64)
+            kh /= np.linalg.norm(kh)
+            for i in range(r):
+                n = rng.standard_normal(D)
+                n -= (n @ kh) * kh
+                n /= np.linalg.norm(n)
+                c = rng.uniform(-0.5, 0.95)
+                q[b, g * r + i] = (np.sqrt(D) * (c * kh + np.sqrt(1 - c * c) * n)).astype(np.float32)
+    if seed % 7 == 3:
+        q[0, 0] = 0.0  # degenerate query
+    excl = [(), (0,), (1,), (0, 1)][int(rng.integers(4))] if seed % 3 else ()
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(float(rng.uniform(0.1, 0.6))),
+                          excluded_layers=excl, sink_on_tie=bool(seed % 5 == 1))
+    opts = P.EngineOptions(observe_only=bool(seed % 6 == 2))
+    with P.KvCache(cc) as cache:
+        for b in range(B):
+            for l_ in range(layers):
+                for g in range(hkv):
+                    cache.append(l_, g, k[b, l_, g], v[b, l_, g], seq=b)
+        res = P.routed_decode_step(q if B > 1 else q[0], layer, cache, cfg, opts)
+        if seed % 4 == 0:  # a tie: tau equal to a group score (exact-first routing)
+            tie = res.groups[0].decision.group_score
+            cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(tie), excluded_layers=excl,
+                                  sink_on_tie=cfg.sink_on_tie)
+            res = P.routed_decode_step(q if B > 1 else q[0], layer, cache, cfg, opts)
+        outs = res.outputs if B > 1 else res.outputs[None]
+        for b in range(B):
+            kb = np.stack([cache.historical(layer, g, 0, L, seq=b)[0] for g in range(hkv)])
+            vb = np.stack([cache.historical(layer, g, 0, L, seq=b)[1] for g in range(hkv)])
+            k0 = kb[:, 0, :].copy()
+            k0n = np.array([orc.anchor_norm(k0[g]) for g in range(hkv)], dtype=np.float32)
+            ref = orc.routed_decode_step(kb, vb, k0, k0n, q[b], layer, oracle_profile(cfg.profile),
+                                         excluded=excl, sink_on_tie=cfg.sink_on_tie,
+                                         observe_only=opts.observe_only, threads=8)
+            assert_parity(outs[b], ref, r, D, res.groups[b * hkv:(b + 1) * hkv])
