@@ -404,3 +404,11 @@ def test_randomized_parity(oracle_libs, seed):
                                          excluded=excl, sink_on_tie=cfg.sink_on_tie,
                                          observe_only=opts.observe_only, threads=8)
             assert_parity(outs[b], ref, r, D, res.groups[b * hkv:(b + 1) * hkv])
+
+
+@pytest.mark.parametrize("hq,hkv,D,L,p", CASES[3:7])
+def test_three_kernel_pipeline_parity(oracle_libs, monkeypatch, hq, hkv, D, L, p):
+    """The A/B three-kernel form (probe -> decode -> combine, SINKR_FUSED=0)
+    meets the same bar as the fused step kernel."""
+    monkeypatch.setenv("SINKR_FUSED", "0")
+    test_planted_parity(oracle_libs, hq, hkv, D, L, p)
