@@ -391,8 +391,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if ((flags & kObserveOnly) || (flags & kLayerExcluded)) certain = true;
                 L = s_len[seq];
                 if (!exact) act_prefix[u] = active ? 1u : 0u;  // estimate decisions, checked later
-                if (lead) {
-                    if (exact) t.group_scores[u] = S;
+                if (lead && exact) {  // (fast path: the consumers publish the record)
+                    t.group_scores[u] = S;
                     t.unit_flags[u] =
                         (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
                     if (!active) {
@@ -1057,6 +1057,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // the exact flags (the estimate pass cannot see a degenerate head
                 // when observe-only or an excluded layer made every decision certain)
                 t.unit_flags[u] = (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
+                if (lean && !active) {
+                    t.tokens[u] = 0ull;
+                    if (t.mode == 1) {  // rank partial of a skipped group: empty
+                        float* P = t.out + size_t(u) * r * (D + 2);
+                        for (uint32_t h = 0; h < r; ++h) {
+                            P[h] = -INFINITY;
+                            P[r + h] = 0.f;
+                        }
+                        for (uint32_t k = 0; k < r * D; ++k) P[2 * r + k] = 0.f;
+                    }
+                }
                 const bool taken = lean ? act_prefix[u] != 0u : (t.route_flags[u] & kActive) != 0u;
                 if (active != taken) atomicExch(&t.ss->error, 4u);  // never: margin >> error
             }
