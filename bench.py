@@ -376,6 +376,97 @@ def other_configs(P, torch, args, spec_cls, dense_cfg, routed_cfg):
     return out
 
 
+def next_rows(P, torch, args, spec_cls, peak):
+    """The §8 "next" rows measured beside the hot path, each against the
+    compiled reference on this host: f1 GPU score collection (routing phase
+    alone) vs the reference's observe-only decode step its calibration runs;
+    f2 snapshot replay; f4 the full-attention BOS-mass pass vs HBM and vs the
+    reference's attention_weights."""
+    import tempfile
+
+    import oracle
+    from paper_2604_16883_b200 import analysis as A
+    from paper_2604_16883_b200 import calibration as cal
+
+    out = {}
+    threads = os.cpu_count() or 1
+    # f1: one calibration sample = one routing pass (C1 shape, 32K)
+    spec = spec_cls(**SHAPE, length=32768, sink_fraction=0.625, seed=args.seed)
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as cache:
+        spec.fill(cache)
+        q = spec.queries()[0]
+        for _ in range(5):
+            cal.collect_scores(cache, q, 0)
+        t0 = time.perf_counter()
+        for _ in range(50):
+            cal.collect_scores(cache, q, 0)
+        gpu_us = (time.perf_counter() - t0) / 50 * 1e6
+        k = np.stack([cache.historical(0, g, 0, spec.length)[0] for g in range(8)])
+        v = np.stack([cache.historical(0, g, 0, spec.length)[1] for g in range(8)])
+    rc = oracle.RefCache(oracle.ref(), 1, 32, 8, 128, spec.length)
+    for g in range(8):
+        rc.append_rows(0, g, k[g], v[g])
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        rc.routed_decode_step(q, 0, oracle.Profile.constant(0.5), excluded=(), workers=threads,
+                              observe_only=True)
+        ts.append(time.perf_counter() - t0)
+    out["f1_score_collection"] = {
+        "context": spec.length, "gpu_us_per_sample": round(gpu_us, 1),
+        "reference_observe_only_step_us": round(statistics.median(ts) * 1e6, 1),
+        "reference_threads": threads,
+        "note": "collect_scores (blocking C-ABI call: H2D q, probe kernel, D2H scores) vs the "
+                "reference's observe-only routed_decode_step, which its calibration runs per sample"}
+    # f2: snapshot replay, reference-written snapshot of the same cache
+    with tempfile.TemporaryDirectory() as d:
+        rc.save_snapshot(d)
+        nbytes = 2 * 8 * spec.length * 128 * 4
+        t0 = time.perf_counter()
+        c2 = P.KvCache.load_snapshot(d)
+        ours_s = time.perf_counter() - t0
+        c2.close()
+        t0 = time.perf_counter()
+        r2 = oracle.ref().load_snapshot(d, 1, 32, 8, 128)
+        ref_s = time.perf_counter() - t0
+        r2.close()
+    rc.close()
+    out["f2_snapshot_load"] = {"context": spec.length, "bytes": nbytes,
+                               "engine_s": round(ours_s, 3), "engine_gbs": round(nbytes / ours_s / 1e9, 2),
+                               "reference_s": round(ref_s, 3),
+                               "note": "reference-written SNKT snapshot; engine: file read + one H2D + "
+                                       "device bf16 conversion per slot; reference: row-by-row append"}
+    # f4: BOS mass over the headline cache (K rows of all 8 groups, 512K)
+    L = args.length
+    spec = spec_cls(**SHAPE, length=L, sink_fraction=args.sink_fraction, seed=args.seed)
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, L)) as cache:
+        spec.fill(cache)
+        q = spec.queries()[0]
+        A.attention_bos_mass(cache, q, 0)
+        st = torch.cuda.ExternalStream(cache.stream)
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            A.attention_bos_mass(cache, q, 0)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        k_bytes = 8 * L * 128 * 2
+        us = statistics.median(ts)
+        k1 = cache.historical(0, 0, 0, 32768)[0]
+    t0 = time.perf_counter()
+    oracle.ref().attention_weights(q[:4], k1)
+    ref_ms = (time.perf_counter() - t0) * 1e3
+    out["f4_bos_mass"] = {"context": L, "k_bytes": k_bytes, "gpu_us": round(us, 1),
+                          "gbs": round(k_bytes / (us * 1e-6) / 1e9, 1),
+                          "frac_of_peak": round(k_bytes / (us * 1e-6) / 1e9 / peak, 3),
+                          "reference_attention_weights_ms_one_group_32k": round(ref_ms, 1),
+                          "note": "attention_bos_mass: alpha0 of all 32 heads, one K-only pass "
+                                  "(CUDA events around the blocking call incl. its small copies)"}
+    return out
+
+
 def run_ours(args, world, rank, local_rank):
     import torch
 
@@ -538,6 +629,10 @@ def run_ours(args, world, rank, local_rank):
     cache.close()
     if not args.no_sweep:
         line["other_configs"] = other_configs(P, torch, args, WorkloadSpec, dense_cfg, routed_cfg)
+        try:
+            line["next_rows"] = next_rows(P, torch, args, WorkloadSpec, peak)
+        except Exception as e:  # reported, never silently dropped
+            line["next_rows"] = {"failed": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
 
 
