@@ -342,6 +342,11 @@ sinkr_status sinkr_attention_bos_mass(sinkr_engine* e, const float* queries, siz
  * GPU: weights [r][len] f32 over the slot's cached rows. */
 sinkr_status sinkr_attention_weights(sinkr_engine* e, const float* queries, size_t seq,
                                      size_t layer, size_t kv_head, float* weights);
+/* Device time of the last sinkr_attention_bos_mass / sinkr_attention_weights
+ * call's kernels (stream pass, finish, weights), from CUDA events on the
+ * engine stream; host staging and copies excluded.  No reference
+ * counterpart (measurement hook, SURVEY.md §8 d). */
+sinkr_status sinkr_attention_last_kernel_seconds(sinkr_engine* e, double* seconds);
 /* oracle labels (analysis.hpp:12-22) from BOS masses: mode 0 = per head
  * (alpha0 > gamma, strict), mode 1 = group mean over `group` consecutive
  * heads.  n_heads % group == 0.  Outputs have n_heads (mode 0) or

@@ -68,6 +68,14 @@ def attention_bos_mass(cache: KvCache, queries, layer: int) -> np.ndarray:
     return out
 
 
+def last_kernel_seconds(cache: KvCache) -> float:
+    """Device time of the last attention_bos_mass / attention_weights call's
+    kernels (CUDA events on the engine stream; host staging excluded)."""
+    out = C.c_double()
+    check(lib().sinkr_attention_last_kernel_seconds(cache.handle, C.byref(out)))
+    return out.value
+
+
 def attention_weights(cache: KvCache, group_queries, layer: int, kv_head: int,
                       seq: int = 0) -> np.ndarray:
     """attention_weights (attention.cpp:75-99) for one GQA group over the

@@ -4,171 +4,333 @@
 // sink label needs only its token-0 entry alpha0 (analysis.hpp:12-22,
 // SPEC.md oracle_labels).  One K-only streaming pass per layer:
 //
-//   bos_partial_kernel  grid (chunks, units): each CTA streams a token chunk
-//                       of one unit's K rows (bf16, 16-byte vector loads), one
-//                       token per thread, r head logits per row from the
-//                       unit's queries in smem; per-head online (max, sum) in
-//                       the log2 domain, reduced over the CTA -> partial.
-//   bos_finish_kernel   per head: LSE-merge of the chunk partials and
+//   bos_stream_kernel   one CTA per SM; the units' K rows are one flat token
+//                       space cut into num_sms equal ranges.  A TMA producer
+//                       warp streams 64-token K tiles (128B-swizzled, the
+//                       decode stream's layout) into a smem ring; 4 consumer
+//                       warps take 16 tokens each and compute the head logits
+//                       on the tensor cores: z = Q.K^T with the fp32 query
+//                       split three ways into bf16 (hi, lo, lo2; ~24 mantissa
+//                       bits, products exact in fp32) — A1 = [hi; lo] and
+//                       A2 = [lo2; 0] as 16-row mma.sync operands.  Per-head
+//                       online (max, sum) in the log2 domain; one partial per
+//                       (unit, CTA) the CTA's range touches.
+//   bos_finish_kernel   per head: LSE-merge of the CTA partials and
 //                       alpha0 = 2^(z0 - M) / L (z0 = token 0's logit).
-//   weights_kernel      attention_weights rows: 2^(z_t - M) / L per token.
+//   weights_kernel      attention_weights rows: 2^(z_t - M) / L per token, from
+//                       the logits the stream pass wrote (same z, to the bit).
 //
 // K traffic: 2 * L * D bytes per unit (half a decode step's), so the pass is
-// HBM bound like the decode stream.  Arithmetic is fp32 (q fp32, K bf16);
-// the reference computes in fp64 — alpha0 agrees to ~1e-6 (tests).
+// HBM bound like the decode stream.  The reference computes in fp64 — alpha0
+// agrees to ~1e-7 (tests).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+
+#include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace sinkr {
 namespace dev {
 
-constexpr int kBosThreads = 256;
-constexpr int kBosHeads = 8;  // heads per pass (a GQA group; more -> several passes)
+constexpr int kBosCWarps = 8;                  // consumer warps, 16 tokens each
+constexpr int kBosThreads = 32 * (1 + kBosCWarps);
+constexpr int kBosTok = kWarpTok * kBosCWarps;  // tokens per stage (2 per SMSP in flight)
+constexpr int kBosBoxes = kBosTok / kStageTok;  // 64-row TMA boxes per stage and half
+constexpr int kBosHeads = 8;                   // heads per pass (mma rows 0-7)
 
 struct BosArgs {
-    const __nv_bfloat16* k;   // cache K base
+    const uint32_t* pre;      // [n_units + 1] token prefix over the launch's units
     const float* q;           // [B*Hq][D] queries
-    const uint32_t* len;      // [U] rows per unit (this layer)
-    float* part;              // [U][chunks][r][2]: m, l (log2 domain)
+    float* part;              // [n_units][G][r][2]: m, l (log2 domain)
     float* z0;                // [U*r] token-0 logit (log2 domain)
     float* stats;             // [U*r][2]: M, L after finish
     double* alpha0;           // [U*r]
-    float* weights;           // weights_kernel: [r][len] of unit u_first
-    uint32_t U, r, Hkv, cap, chunks, slot0;  // slot0 = layer * U
-    uint32_t u_first;         // first unit of the launch (grid.y offset)
-    float qscale;             // log2(e) / sqrt(D)
+    float* zout;              // logits [r][L] of the launch's only unit, or null
+    float* weights;           // weights_kernel: [r][L] of unit u_first
+    uint32_t U, r, cap, slot0;  // slot0 = layer * U
+    uint32_t u_first, n_units;  // units of this launch
+    uint32_t G;                 // stream CTAs
+    float qscale;               // log2(e) / sqrt(D)
 };
 
 template <int D>
-__device__ __forceinline__ void load_row(const __nv_bfloat16* row, float (&k)[D]) {
-#pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(row) + c);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            k[8 * c + 2 * e] = __uint_as_float(w[e] << 16);
-            k[8 * c + 2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
-        }
+struct BosCfg {
+    static constexpr int kHalves = Cfg<D>::kHalves;
+    static constexpr int kBoxDim = Cfg<D>::kBoxDim;
+    static constexpr int kStageBytes = kBosTok * D * 2;     // K only
+    static constexpr int kStages = (192 * 1024) / kStageBytes > 16 ? 16 : (192 * 1024) / kStageBytes;
+    static constexpr int kNK = D / 16;
+    static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStages * (16 + 16) +
+                                      kBosCWarps * kBosHeads * 2 * 4;
+};
+
+// byte offset of (token, 16-byte chunk) in a K stage: swz<D> with kBosTok rows per half
+template <int D>
+__device__ __forceinline__ uint32_t bos_swz(uint32_t tok, uint32_t chunk) {
+    if constexpr (D >= 64) {
+        const uint32_t half = chunk >> 3, c = chunk & 7;
+        return half * (kBosTok * 128) + tok * 128 + ((c ^ (tok & 7)) << 4);
+    } else {
+        const uint32_t o = tok * 64 + chunk * 16;
+        return o ^ (((o >> 7) & 3) << 4);
     }
 }
 
+__device__ __forceinline__ uint32_t bos_range_start(const BosArgs& a, uint32_t c) {
+    return (uint32_t)((uint64_t)c * a.pre[a.n_units] / a.G);
+}
+
 template <int D>
-__global__ void __launch_bounds__(kBosThreads) bos_partial_kernel(BosArgs a, uint32_t h0) {
-    __shared__ float sq[kBosHeads][D];
-    __shared__ float red[kBosThreads / 32][kBosHeads][2];
-    const uint32_t u = a.u_first + blockIdx.y, chunk = blockIdx.x;
-    const uint32_t nh = min((uint32_t)kBosHeads, a.r - h0);
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t i = tid; i < kBosHeads * D; i += kBosThreads) {
-        const uint32_t h = i / D, j = i % D;
-        sq[h][j] = h < nh ? a.q[(size_t(u) * a.r + h0 + h) * D + j] * a.qscale : 0.f;
+__global__ void __launch_bounds__(kBosThreads, 1)
+    bos_stream_kernel(const __grid_constant__ CUtensorMap tmk, BosArgs a, uint32_t h0) {
+    using C = BosCfg<D>;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* ring = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    StageMeta* meta = reinterpret_cast<StageMeta*>(empty + C::kStages);
+    float* sm_ml = reinterpret_cast<float*>(meta + C::kStages);  // [kBosCWarps][kBosHeads][2]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t c = blockIdx.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], kBosCWarps);
+        }
+        ptx::fence_mbar_init();
     }
     __syncthreads();
-    const uint32_t L = a.len[u];
-    const uint32_t per = (L + a.chunks - 1) / a.chunks;
-    const uint32_t t0 = min(L, chunk * per), t1 = min(L, t0 + per);
-    const __nv_bfloat16* base = a.k + size_t(a.slot0 + u) * a.cap * D;
-    float m[kBosHeads], l[kBosHeads];
+
+    if (warp == 0) {
+        // ------------------------------ producer ------------------------------
+        if (lane == 0) {
+            ptx::tma_prefetch_desc(&tmk);
+            const uint64_t pol = ptx::policy_evict_first();
+            const uint32_t p0 = bos_range_start(a, c), p1 = bos_range_start(a, c + 1);
+            uint32_t i = 0;  // launch-relative unit holding p0
+            while (i + 1 < a.n_units && a.pre[i + 1] <= p0) ++i;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (uint32_t p = p0; p < p1; ++i) {
+                const uint32_t ub = a.pre[i], ue = min(a.pre[i + 1], p1);
+                const int32_t row0 = (int32_t)(size_t(a.slot0 + a.u_first + i) * a.cap);
+                for (uint32_t tk = p - ub; tk < ue - ub; tk += kBosTok) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
+                    meta[stage].unit = i;
+                    meta[stage].tok0 = tk;
+                    meta[stage].ntok = min((uint32_t)kBosTok, ue - ub - tk);
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                    uint8_t* kd = ring + stage * C::kStageBytes;
 #pragma unroll
-    for (int h = 0; h < kBosHeads; ++h) {
-        m[h] = -INFINITY;
-        l[h] = 0.f;
+                    for (int hh = 0; hh < C::kHalves; ++hh)
+#pragma unroll
+                        for (int bx = 0; bx < kBosBoxes; ++bx)
+                            ptx::tma_load_2d(kd + (hh * kBosTok + bx * kStageTok) * (D >= 64 ? 128 : 2 * D),
+                                             &tmk, hh * C::kBoxDim, row0 + (int32_t)(tk + bx * kStageTok),
+                                             &full[stage], pol);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                p = ue;
+            }
+            ptx::mbar_wait(&empty[stage], phase ^ 1u);
+            meta[stage].unit = kEnd;
+            ptx::mbar_arrive(&full[stage]);
+        }
+        return;
     }
-    for (uint32_t t = t0 + tid; t < t1; t += kBosThreads) {
-        float k[D];
-        load_row<D>(base + size_t(t) * D, k);
+
+    // ------------------------------ consumers ------------------------------
+    const int cw = warp - 1;
+    const uint32_t ctid = threadIdx.x - 32;
+    const int tb = cw * kWarpTok;
+    const int grp = lane >> 2, qd = lane & 3;
+    const int lj = lane >> 3, li = lane & 7;
+    const uint32_t k_tok = tb + ((lj >> 1) << 3) + li, k_csel = lj & 1;
+    const uint32_t nh = min((uint32_t)kBosHeads, a.r - h0);
+    const bool live = grp < (int)nh;
+
+    uint32_t q1[C::kNK][4], q2[C::kNK][2];  // A1 = [hi; lo], A2 = [lo2; 0]
+    float m = -INFINITY, l = 0.f;
+    uint32_t cur = kEnd;
+
+    auto load_q = [&](uint32_t i) {
+        const float* qrow = a.q + (size_t(a.u_first + i) * a.r + h0 + (live ? grp : 0)) * D;
 #pragma unroll
-        for (int h = 0; h < kBosHeads; ++h) {
-            if (h < (int)nh) {
-                float z = 0.f;
+        for (int kk = 0; kk < C::kNK; ++kk) {
 #pragma unroll
-                for (int j = 0; j < D; ++j) z = fmaf(sq[h][j], k[j], z);
-                if (t == 0) a.z0[size_t(u) * a.r + h0 + h] = z;
-                if (z > m[h]) {
-                    l[h] = l[h] * exp2f(m[h] - z) + 1.f;
-                    m[h] = z;
-                } else {
-                    l[h] += exp2f(z - m[h]);
+            for (int hv = 0; hv < 2; ++hv) {
+                float2 x = make_float2(0.f, 0.f);
+                if (live) x = *reinterpret_cast<const float2*>(qrow + 16 * kk + 8 * hv + 2 * qd);
+                x.x *= a.qscale;
+                x.y *= a.qscale;
+                const uint32_t hi = ptx::pack_bf16(x.x, x.y);
+                const float r0 = x.x - ptx::bf16_lo_as_f32(hi), r1 = x.y - ptx::bf16_hi_as_f32(hi);
+                const uint32_t lo = ptx::pack_bf16(r0, r1);
+                q1[kk][2 * hv] = hi;
+                q1[kk][2 * hv + 1] = lo;
+                q2[kk][hv] = ptx::pack_bf16(r0 - ptx::bf16_lo_as_f32(lo), r1 - ptx::bf16_hi_as_f32(lo));
+            }
+        }
+    };
+    auto flush = [&](uint32_t i) {
+        float mo = __shfl_xor_sync(0xffffffffu, m, 1), lo = __shfl_xor_sync(0xffffffffu, l, 1);
+        float mx = fmaxf(m, mo);
+        l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
+        m = mx;
+        mo = __shfl_xor_sync(0xffffffffu, m, 2);
+        lo = __shfl_xor_sync(0xffffffffu, l, 2);
+        mx = fmaxf(m, mo);
+        l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
+        m = mx;
+        if (qd == 0) {
+            sm_ml[(cw * kBosHeads + grp) * 2] = m;
+            sm_ml[(cw * kBosHeads + grp) * 2 + 1] = l;
+        }
+        ptx::named_bar_sync(1, kBosCWarps * 32);
+        if (ctid < nh) {
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kBosCWarps; ++w) M = fmaxf(M, sm_ml[(w * kBosHeads + ctid) * 2]);
+            float S = 0.f;
+            if (M != -INFINITY)
+#pragma unroll
+                for (int w = 0; w < kBosCWarps; ++w)
+                    S += sm_ml[(w * kBosHeads + ctid) * 2 + 1] * exp2f(sm_ml[(w * kBosHeads + ctid) * 2] - M);
+            float* P = a.part + ((size_t(i) * a.G + c) * a.r + h0 + ctid) * 2;
+            P[0] = M;
+            P[1] = S;
+        }
+        ptx::named_bar_sync(1, kBosCWarps * 32);
+    };
+
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+        ptx::mbar_wait(&full[stage], phase);
+        const uint32_t unit = meta[stage].unit;
+        if (unit == kEnd) break;
+        if (unit != cur) {
+            if (cur != kEnd) flush(cur);
+            cur = unit;
+            load_q(unit);
+            m = -INFINITY;
+            l = 0.f;
+        }
+        const uint32_t tok0 = meta[stage].tok0;
+        const int n = (int)meta[stage].ntok - tb;
+        if (n > 0) {
+            const uint32_t kbase = ptx::smem_u32(ring + stage * C::kStageBytes);
+            float s1[2][2][4], s2[2][4];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                s2[x][0] = s2[x][1] = s2[x][2] = s2[x][3] = 0.f;
+#pragma unroll
+                for (int y = 0; y < 2; ++y) s1[x][y][0] = s1[x][y][1] = s1[x][y][2] = s1[x][y][3] = 0.f;
+            }
+#pragma unroll
+            for (int kk = 0; kk < C::kNK; ++kk) {
+                uint32_t b[4];
+                ptx::ldsm_x4(b, kbase + bos_swz<D>(k_tok, 2 * kk + k_csel));
+                const uint32_t a2[4] = {q2[kk][0], 0u, q2[kk][1], 0u};
+                ptx::mma_bf16(s1[0][kk & 1], q1[kk], b[0], b[1]);
+                ptx::mma_bf16(s1[1][kk & 1], q1[kk], b[2], b[3]);
+                ptx::mma_bf16(s2[0], a2, b[0], b[1]);
+                ptx::mma_bf16(s2[1], a2, b[2], b[3]);
+            }
+            float z[4];
+            float bm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int nt = j >> 1, col = j & 1;
+                const float hi = s1[nt][0][col] + s1[nt][1][col];
+                const float lo = s1[nt][0][col + 2] + s1[nt][1][col + 2];
+                const int tok = nt * 8 + 2 * qd + col;
+                z[j] = tok < n ? (hi + lo) + s2[nt][col] : -INFINITY;
+                bm = fmaxf(bm, z[j]);
+            }
+            if (tok0 + tb == 0 && live && qd == 0)  // token 0 of the unit: j = 0 of lane quad 0
+                a.z0[size_t(a.u_first + unit) * a.r + h0 + grp] = z[0];
+            if (a.zout != nullptr && live) {  // attention_weights: keep every logit
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int tok = (j >> 1) * 8 + 2 * qd + (j & 1);
+                    if (tok < n) a.zout[size_t(h0 + grp) * a.pre[1] + tok0 + tb + tok] = z[j];
                 }
             }
-        }
-    }
-    // CTA reduction of (m, l) per head
-#pragma unroll
-    for (int h = 0; h < kBosHeads; ++h) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float mo = __shfl_xor_sync(0xffffffffu, m[h], o);
-            const float lo = __shfl_xor_sync(0xffffffffu, l[h], o);
-            const float mx = fmaxf(m[h], mo);
-            l[h] = (mx == -INFINITY) ? 0.f : l[h] * exp2f(m[h] - mx) + lo * exp2f(mo - mx);
-            m[h] = mx;
-        }
-        if (lane == 0) {
-            red[warp][h][0] = m[h];
-            red[warp][h][1] = l[h];
-        }
-    }
-    __syncthreads();
-    if (tid < nh) {
-        float M = -INFINITY;
-        for (int w = 0; w < kBosThreads / 32; ++w) M = fmaxf(M, red[w][tid][0]);
-        float S = 0.f;
-        if (M != -INFINITY)
-            for (int w = 0; w < kBosThreads / 32; ++w) S += red[w][tid][1] * exp2f(red[w][tid][0] - M);
-        float* P = a.part + ((size_t(u) * a.chunks + chunk) * a.r + h0 + tid) * 2;
-        P[0] = M;
-        P[1] = S;
-    }
-}
-
-__global__ void bos_finish_kernel(BosArgs a, uint32_t n_units) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;  // head index within the launch
-    if (i >= n_units * a.r) return;
-    const uint32_t u = a.u_first + i / a.r, h = i % a.r;
-    double M = -INFINITY;
-    for (uint32_t c = 0; c < a.chunks; ++c)
-        M = fmax(M, (double)a.part[((size_t(u) * a.chunks + c) * a.r + h) * 2]);
-    double S = 0.0;
-    for (uint32_t c = 0; c < a.chunks; ++c) {
-        const float* P = a.part + ((size_t(u) * a.chunks + c) * a.r + h) * 2;
-        if (P[0] != -INFINITY) S += (double)P[1] * exp2((double)P[0] - M);
-    }
-    const size_t gi = size_t(u) * a.r + h;
-    a.stats[gi * 2] = (float)M;
-    a.stats[gi * 2 + 1] = (float)S;
-    a.alpha0[gi] = exp2((double)a.z0[gi] - M) / S;
-}
-
-template <int D>
-__global__ void __launch_bounds__(kBosThreads) weights_kernel(BosArgs a) {
-    __shared__ float sq[kBosHeads][D];
-    const uint32_t u = a.u_first;
-    const uint32_t h0 = blockIdx.y * kBosHeads, nh = min((uint32_t)kBosHeads, a.r - h0);
-    for (uint32_t i = threadIdx.x; i < kBosHeads * D; i += kBosThreads) {
-        const uint32_t h = i / D, j = i % D;
-        sq[h][j] = h < nh ? a.q[(size_t(u) * a.r + h0 + h) * D + j] * a.qscale : 0.f;
-    }
-    __syncthreads();
-    const uint32_t L = a.len[u];
-    const __nv_bfloat16* base = a.k + size_t(a.slot0 + u) * a.cap * D;
-    for (uint32_t t = blockIdx.x * kBosThreads + threadIdx.x; t < L; t += gridDim.x * kBosThreads) {
-        float k[D];
-        load_row<D>(base + size_t(t) * D, k);
-#pragma unroll
-        for (int h = 0; h < kBosHeads; ++h) {
-            if (h < (int)nh) {
-                float z = 0.f;
-#pragma unroll
-                for (int j = 0; j < D; ++j) z = fmaf(sq[h][j], k[j], z);
-                const size_t gi = size_t(u) * a.r + h0 + h;
-                a.weights[size_t(h0 + h) * L + t] =
-                    (float)(exp2((double)z - (double)a.stats[gi * 2]) / (double)a.stats[gi * 2 + 1]);
+            if (bm != -INFINITY) {
+                const float mn = fmaxf(m, bm);
+                l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) +
+                    ((exp2f(z[0] - mn) + exp2f(z[1] - mn)) + (exp2f(z[2] - mn) + exp2f(z[3] - mn)));
+                m = mn;
             }
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+        if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
+    if (cur != kEnd) flush(cur);
+}
+
+constexpr int kBosMaxG = 1024;  // stream CTAs the finish kernel can index
+
+// one warp per head: the lanes fold the CTA partials of the head's unit
+__global__ void __launch_bounds__(256) bos_finish_kernel(BosArgs a) {
+    __shared__ uint32_t s_start[kBosMaxG + 1];  // CTA range starts, computed once per block
+    for (uint32_t c = threadIdx.x; c <= a.G; c += blockDim.x) s_start[c] = bos_range_start(a, c);
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // head within the launch
+    if (idx >= a.n_units * a.r) return;
+    const uint32_t i = idx / a.r, h = idx % a.r;
+    const uint32_t ub = a.pre[i], ue = a.pre[i + 1];
+    // first CTA whose range ends past ub (ranges are sorted and contiguous)
+    uint32_t lo = 0, hi = a.G;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_start[mid + 1] <= ub) lo = mid + 1; else hi = mid;
+    }
+    double M = -INFINITY;
+    for (uint32_t c = lo + lane; c < a.G && s_start[c] < ue; c += 32)
+        if (s_start[c] < s_start[c + 1])  // an empty range wrote no partial
+            M = fmax(M, (double)a.part[((size_t(i) * a.G + c) * a.r + h) * 2]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+    double S = 0.0;
+    for (uint32_t c = lo + lane; c < a.G && s_start[c] < ue; c += 32) {
+        if (s_start[c] == s_start[c + 1]) continue;
+        const float* P = a.part + ((size_t(i) * a.G + c) * a.r + h) * 2;
+        if (P[0] != -INFINITY) S += (double)P[1] * exp2((double)P[0] - M);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+    if (lane == 0) {
+        const size_t gi = size_t(a.u_first + i) * a.r + h;
+        a.stats[gi * 2] = (float)M;
+        a.stats[gi * 2 + 1] = (float)S;
+        a.alpha0[gi] = exp2((double)a.z0[gi] - M) / S;
+    }
+}
+
+// attention_weights of unit u_first from the stream pass's logits
+__global__ void weights_kernel(BosArgs a) {
+    const uint32_t L = a.pre[1];
+    const size_t n = size_t(a.r) * L;
+    for (size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < n;
+         idx += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t h = (uint32_t)(idx / L);
+        const size_t gi = size_t(a.u_first) * a.r + h;
+        a.weights[idx] =
+            (float)(exp2((double)a.zout[idx] - (double)a.stats[gi * 2]) / (double)a.stats[gi * 2 + 1]);
     }
 }
 

@@ -129,6 +129,12 @@ struct sinkr_engine {
     uint32_t* d_cursor = nullptr;
     uint32_t* d_tokens_done = nullptr;
     uint32_t* d_route_flags = nullptr;  // distributed routing decisions [U]
+    uint8_t* d_bos = nullptr;            // analysis scratch (run_bos), grown on demand
+    size_t bos_bytes = 0;
+    uint8_t* h_bos = nullptr;            // pinned staging for run_bos (prefix up, alpha0 down)
+    cudaEvent_t ev_bos[2] = {};          // around run_bos's kernels (device time)
+    float bos_ms = -1.f;
+    size_t h_bos_bytes = 0;
     uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [U]
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
     // sequence-sharded peer merge (mode 3): this rank's exchange block
@@ -789,6 +795,12 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaFuncSetAttribute(dev::decode_kernel<128>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem_bytes<128>()));
+            CK(cudaFuncSetAttribute(dev::bos_stream_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dev::BosCfg<32>::kSmemBytes));
+            CK(cudaFuncSetAttribute(dev::bos_stream_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dev::BosCfg<64>::kSmemBytes));
+            CK(cudaFuncSetAttribute(dev::bos_stream_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dev::BosCfg<128>::kSmemBytes));
             CK(cudaFuncSetAttribute(dev::step_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     dev::StepCfg<32>::kSmemBytes));
             CK(cudaFuncSetAttribute(dev::step_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -812,6 +824,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
                                         cudaSharedmemCarveoutMaxShared));
             for (auto& ev : e->ev) CK(cudaEventCreate(&ev));
             CK(cudaEventCreateWithFlags(&e->ev_in, cudaEventDisableTiming));
+            CK(cudaEventCreate(&e->ev_bos[0]));
+            CK(cudaEventCreate(&e->ev_bos[1]));
             CK(cudaEventRecord(e->ev_in, e->stream));
             CK(cudaStreamSynchronize(e->stream));
         } catch (...) {
@@ -846,6 +860,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_cursor);
     cudaFree(e->d_tokens_done);
     cudaFree(e->d_route_flags);
+    cudaFree(e->d_bos);
     for (void* pb : e->ipc_opened) cudaIpcCloseMemHandle(pb);
     cudaFree(e->d_xchg);
     cudaFree(e->d_peer_xchg);
@@ -858,6 +873,9 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_partials);
     if (e->h_in) cudaFreeHost(e->h_in);
     if (e->h_res) cudaFreeHost(e->h_res);
+    if (e->h_bos) cudaFreeHost(e->h_bos);
+    for (auto ev : e->ev_bos)
+        if (ev) cudaEventDestroy(ev);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
     return SINKR_OK;
@@ -1234,87 +1252,116 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
     });
 }
 
+static void launch_bos(sinkr_engine* e, const dev::BosArgs& a, uint32_t h0) {
+#define SINKR_BOS_LAUNCH(DD)                                                                     \
+    {                                                                                            \
+        constexpr int smem = dev::BosCfg<DD>::kSmemBytes; /* attribute set at creation */     \
+        dev::bos_stream_kernel<DD><<<a.G, dev::kBosThreads, smem, e->stream>>>(e->tmk, a, h0);   \
+    }
+    switch (e->D) {
+        case 32: SINKR_BOS_LAUNCH(32) break;
+        case 64: SINKR_BOS_LAUNCH(64) break;
+        default: SINKR_BOS_LAUNCH(128) break;
+    }
+#undef SINKR_BOS_LAUNCH
+}
+
 // Full-attention BOS mass (analysis.cuh).  Queries are staged in the input
-// block's query area; the scratch is allocated per call (analysis path).
+// block's query area; the scratch persists in the engine, grown on demand.
 static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size_t q_offset,
                     size_t layer, uint32_t u_first, uint32_t n_units, double* alpha0,
                     float* weights) {
     if (layer >= e->layers) fail(SINKR_OUT_OF_RANGE, "layer index out of range");
     const size_t U = e->U, r = e->r, D = e->D;
-    std::vector<uint32_t> lens(U);
-    uint32_t max_len = 0;
-    for (size_t u = u_first; u < u_first + n_units; ++u) {
-        const size_t L = e->len[layer * U + u];
+    std::vector<uint32_t> pre(n_units + 1, 0);
+    for (uint32_t i = 0; i < n_units; ++i) {
+        const size_t L = e->len[layer * U + u_first + i];
         if (L == 0) fail(SINKR_RUNTIME_ERROR, "attention over an empty cache slot");
-        lens[u] = (uint32_t)L;
-        max_len = std::max<uint32_t>(max_len, (uint32_t)L);
+        pre[i + 1] = pre[i] + (uint32_t)L;
     }
-    uint32_t chunks = (uint32_t)std::max<size_t>(1, (4 * (size_t)e->num_sms + n_units - 1) / n_units);
-    chunks = std::min<uint32_t>(chunks, std::max<uint32_t>(1, (max_len + 255) / 256));
-    // scratch: len[U] | part[U][chunks][r][2] | z0[U*r] | stats[U*r][2] | alpha0[U*r] f64 | weights
-    const size_t off_part = align_up(U * 4, 256);
-    const size_t off_z0 = align_up(off_part + U * chunks * r * 2 * 4, 256);
+    const uint32_t T = pre[n_units];
+    // one stream CTA per SM (the ring takes ~128 KB), >= one stage of tokens each
+    const uint32_t G = std::max<uint32_t>(
+        1, std::min<uint32_t>({(uint32_t)e->num_sms, (T + dev::kStageTok - 1) / dev::kStageTok,
+                               (uint32_t)dev::kBosMaxG}));
+    // scratch: pre[n+1] | part[n][G][r][2] | z0[U*r] | stats[U*r][2] | alpha0[U*r] f64 | logits | weights
+    const size_t off_part = align_up((n_units + 1) * 4, 256);
+    const size_t off_z0 = align_up(off_part + (size_t)n_units * G * r * 2 * 4, 256);
     const size_t off_st = align_up(off_z0 + U * r * 4, 256);
     const size_t off_a0 = align_up(off_st + U * r * 2 * 4, 256);
-    const size_t off_w = align_up(off_a0 + U * r * 8, 256);
-    const size_t wbytes = weights ? r * (size_t)max_len * 4 : 0;
-    uint8_t* scratch = nullptr;
-    CK(cudaMalloc(&scratch, off_w + wbytes));
-    try {
-        CK(cudaEventSynchronize(e->ev_in));  // the input block is free
-        std::memcpy(e->h_in + e->off_q + q_offset * 4, queries, q_floats * 4);
-        CK(cudaMemcpyAsync(e->d_in + e->off_q + q_offset * 4, e->h_in + e->off_q + q_offset * 4,
-                           q_floats * 4, cudaMemcpyHostToDevice, e->stream));
-        CK(cudaMemcpyAsync(scratch, lens.data(), U * 4, cudaMemcpyHostToDevice, e->stream));
-        dev::BosArgs a{};
-        a.k = e->d_k;
-        a.q = reinterpret_cast<const float*>(e->d_in + e->off_q);
-        a.len = reinterpret_cast<const uint32_t*>(scratch);
-        a.part = reinterpret_cast<float*>(scratch + off_part);
-        a.z0 = reinterpret_cast<float*>(scratch + off_z0);
-        a.stats = reinterpret_cast<float*>(scratch + off_st);
-        a.alpha0 = reinterpret_cast<double*>(scratch + off_a0);
-        a.weights = reinterpret_cast<float*>(scratch + off_w);
-        a.U = (uint32_t)U;
-        a.r = (uint32_t)r;
-        a.Hkv = (uint32_t)e->cfg.num_kv_heads;
-        a.cap = (uint32_t)e->cap;
-        a.chunks = chunks;
-        a.slot0 = (uint32_t)(layer * U);
-        a.u_first = u_first;
-        a.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
-        for (uint32_t h0 = 0; h0 < r; h0 += dev::kBosHeads) {
-            const dim3 g(chunks, n_units);
-            switch (D) {
-                case 32: dev::bos_partial_kernel<32><<<g, dev::kBosThreads, 0, e->stream>>>(a, h0); break;
-                case 64: dev::bos_partial_kernel<64><<<g, dev::kBosThreads, 0, e->stream>>>(a, h0); break;
-                default: dev::bos_partial_kernel<128><<<g, dev::kBosThreads, 0, e->stream>>>(a, h0); break;
-            }
-        }
-        const uint32_t nh = n_units * (uint32_t)r;
-        dev::bos_finish_kernel<<<(nh + 127) / 128, 128, 0, e->stream>>>(a, n_units);
-        if (weights) {
-            const dim3 g(std::min<uint32_t>((max_len + dev::kBosThreads - 1) / dev::kBosThreads,
-                                            8u * (uint32_t)e->num_sms),
-                         (uint32_t)((r + dev::kBosHeads - 1) / dev::kBosHeads));
-            switch (D) {
-                case 32: dev::weights_kernel<32><<<g, dev::kBosThreads, 0, e->stream>>>(a); break;
-                case 64: dev::weights_kernel<64><<<g, dev::kBosThreads, 0, e->stream>>>(a); break;
-                default: dev::weights_kernel<128><<<g, dev::kBosThreads, 0, e->stream>>>(a); break;
-            }
-        }
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(alpha0, scratch + off_a0 + (size_t)u_first * r * 8, (size_t)nh * 8,
-                           cudaMemcpyDeviceToHost, e->stream));
-        if (weights)
-            CK(cudaMemcpyAsync(weights, scratch + off_w, wbytes, cudaMemcpyDeviceToHost, e->stream));
+    const size_t off_z = align_up(off_a0 + U * r * 8, 256);
+    const size_t wbytes = weights ? r * (size_t)T * 4 : 0;
+    const size_t off_w = align_up(off_z + wbytes, 256);
+    const size_t need = off_w + wbytes;
+    if (e->bos_bytes < need) {
         CK(cudaStreamSynchronize(e->stream));
-    } catch (...) {
-        cudaStreamSynchronize(e->stream);
-        cudaFree(scratch);
-        throw;
+        cudaFree(e->d_bos);
+        e->d_bos = nullptr;
+        e->bos_bytes = 0;
+        CK(cudaMalloc(&e->d_bos, need));
+        e->bos_bytes = need;
     }
-    CK(cudaFree(scratch));
+    uint8_t* scratch = e->d_bos;
+    const uint32_t nh = n_units * (uint32_t)r;
+    const size_t h_a0 = align_up((n_units + 1) * 4, 64), h_need = h_a0 + (size_t)nh * 8;
+    if (e->h_bos_bytes < h_need) {
+        CK(cudaStreamSynchronize(e->stream));
+        if (e->h_bos) cudaFreeHost(e->h_bos);
+        e->h_bos = nullptr;
+        e->h_bos_bytes = 0;
+        CK(cudaMallocHost(&e->h_bos, h_need));
+        e->h_bos_bytes = h_need;
+    }
+    CK(cudaEventSynchronize(e->ev_in));  // the input block is free
+    std::memcpy(e->h_in + e->off_q + q_offset * 4, queries, q_floats * 4);
+    std::memcpy(e->h_bos, pre.data(), (n_units + 1) * 4);
+    CK(cudaMemcpyAsync(e->d_in + e->off_q + q_offset * 4, e->h_in + e->off_q + q_offset * 4,
+                       q_floats * 4, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(scratch, e->h_bos, (n_units + 1) * 4, cudaMemcpyHostToDevice, e->stream));
+    dev::BosArgs a{};
+    a.pre = reinterpret_cast<const uint32_t*>(scratch);
+    a.q = reinterpret_cast<const float*>(e->d_in + e->off_q);
+    a.part = reinterpret_cast<float*>(scratch + off_part);
+    a.z0 = reinterpret_cast<float*>(scratch + off_z0);
+    a.stats = reinterpret_cast<float*>(scratch + off_st);
+    a.alpha0 = reinterpret_cast<double*>(scratch + off_a0);
+    a.zout = weights ? reinterpret_cast<float*>(scratch + off_z) : nullptr;
+    a.weights = reinterpret_cast<float*>(scratch + off_w);
+    a.U = (uint32_t)U;
+    a.r = (uint32_t)r;
+    a.cap = (uint32_t)e->cap;
+    a.slot0 = (uint32_t)(layer * U);
+    a.u_first = u_first;
+    a.n_units = n_units;
+    a.G = G;
+    a.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
+    CK(cudaEventRecord(e->ev_bos[0], e->stream));
+    for (uint32_t h0 = 0; h0 < r; h0 += dev::kBosHeads) {
+        launch_bos(e, a, h0);
+    }
+    dev::bos_finish_kernel<<<(nh + 7) / 8, 256, 0, e->stream>>>(a);
+    if (weights) {
+        const uint32_t blocks = std::min<uint32_t>((uint32_t)((r * (size_t)T + 255) / 256),
+                                                   8u * (uint32_t)e->num_sms);
+        dev::weights_kernel<<<blocks, 256, 0, e->stream>>>(a);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e->ev_bos[1], e->stream));
+    CK(cudaMemcpyAsync(e->h_bos + h_a0, scratch + off_a0 + (size_t)u_first * r * 8, (size_t)nh * 8,
+                       cudaMemcpyDeviceToHost, e->stream));
+    if (weights)
+        CK(cudaMemcpyAsync(weights, scratch + off_w, wbytes, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    std::memcpy(alpha0, e->h_bos + h_a0, (size_t)nh * 8);
+    CK(cudaEventElapsedTime(&e->bos_ms, e->ev_bos[0], e->ev_bos[1]));
+}
+
+sinkr_status sinkr_attention_last_kernel_seconds(sinkr_engine* e, double* seconds) {
+    return guard([&] {
+        if (!e || !seconds) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        if (e->bos_ms < 0.f) fail(SINKR_RUNTIME_ERROR, "no analysis pass has run on this engine");
+        *seconds = e->bos_ms * 1e-3;
+    });
 }
 
 sinkr_status sinkr_attention_bos_mass(sinkr_engine* e, const float* queries, size_t layer,

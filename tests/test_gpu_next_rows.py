@@ -210,6 +210,40 @@ def test_bos_mass_and_weights_vs_reference(ref, L, p, seed):
         assert np.abs(a0[g * r:(g + 1) * r] - rw[:, 0]).max() <= 1e-6
 
 
+@pytest.mark.parametrize("B,hq,hkv,D", [(2, 32, 4, 128), (3, 8, 8, 64), (1, 16, 4, 32), (2, 64, 8, 128)])
+def test_bos_mass_ragged_shapes(ref, B, hq, hkv, D):
+    """BOS pass over ragged slots (units of different lengths share the flat
+    token space and CTA ranges straddle units), r = 8, r = 1
+    and D = 64/32; alpha0 and weights against attention_weights
+    (attention.cpp:75-99) per group, layer 1 of 2."""
+    rng = np.random.default_rng(B * 1000 + hq + D)
+    r = hq // hkv
+    cap = 9000
+    lens = rng.integers(1, cap, size=(B, hkv))
+    lens[0, 0] = 1
+    lens[-1, -1] = cap
+    ks = {}
+    with P.KvCache(P.CacheConfig(2, hq, hkv, D, cap, B)) as cache:
+        for s in range(B):
+            for g in range(hkv):
+                k = (rng.standard_normal((lens[s, g], D)) * 1.5).astype(np.float32)
+                k[0] *= 6.0
+                k = round_bf16(k)  # the cache stores bf16: compare on representable rows
+                v = round_bf16(rng.standard_normal((lens[s, g], D)).astype(np.float32))
+                cache.append(1, g, k, v, seq=s)
+                ks[s, g] = k
+        q = (rng.standard_normal((B, hq, D)) * np.sqrt(D) * 0.3).astype(np.float32)
+        a0 = A.attention_bos_mass(cache, q, 1)
+        for s in range(B):
+            for g in range(hkv):
+                rw = ref.attention_weights(q[s, g * r:(g + 1) * r], ks[s, g])
+                assert np.abs(a0[s, g * r:(g + 1) * r] - rw[:, 0]).max() <= 1e-6, (s, g)
+        for s, g in [(0, 0), (B - 1, hkv - 1), (B // 2, hkv // 2)]:
+            w = A.attention_weights(cache, q[s, g * r:(g + 1) * r], 1, g, seq=s)
+            rw = ref.attention_weights(q[s, g * r:(g + 1) * r], ks[s, g])
+            assert np.abs(w - rw).max() <= 1e-6, (s, g, np.abs(w - rw).max())
+
+
 def test_route_eval_planted_workload():
     """SPEC.md analysis invariant: on the planted workload the proxy at tau 0.5
     gives precision = recall = 1 against oracle labels with gamma 0.65, and the
