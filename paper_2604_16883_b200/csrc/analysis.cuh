@@ -5,7 +5,7 @@
 // SPEC.md oracle_labels).  One K-only streaming pass per layer:
 //
 //   bos_stream_kernel   one CTA per SM; the units' K rows are one flat token
-//                       space cut into num_sms equal ranges.  A TMA producer
+//                       space, claimed by guided self-scheduling.  A TMA producer
 //                       warp streams 64-token K tiles (128B-swizzled, the
 //                       decode stream's layout) into a smem ring; 4 consumer
 //                       warps take 16 tokens each and compute the head logits
@@ -14,9 +14,11 @@
 //                       bits, products exact in fp32) — A1 = [hi; lo] and
 //                       A2 = [lo2; 0] as 16-row mma.sync operands.  Per-head
 //                       online (max, sum) in the log2 domain; one partial per
-//                       (unit, CTA) the CTA's range touches.
-//   bos_finish_kernel   per head: LSE-merge of the CTA partials and
-//                       alpha0 = 2^(z0 - M) / L (z0 = token 0's logit).
+//                       (unit, CTA) the CTA's claims touched.
+//   bos_finish_kernel   one warp per head: LSE-merge of the unit's partials
+//                       (fp64) and alpha0 = 2^(z0 - M) / L (z0 = token 0's
+//                       logit).  (Merging in the stream kernel, by the last CTA
+//                       or by each unit's last flusher, measured 10 us slower.)
 //   weights_kernel      attention_weights rows: 2^(z_t - M) / L per token, from
 //                       the logits the stream pass wrote (same z, to the bit).
 //
@@ -40,11 +42,16 @@ constexpr int kBosThreads = 32 * (1 + kBosCWarps);
 constexpr int kBosTok = kWarpTok * kBosCWarps;  // tokens per stage (2 per SMSP in flight)
 constexpr int kBosBoxes = kBosTok / kStageTok;  // 64-row TMA boxes per stage and half
 constexpr int kBosHeads = 8;                   // heads per pass (mma rows 0-7)
+static_assert(kBosCWarps >= kMaxR, "the unit merge takes one consumer warp per head");
 
 struct BosArgs {
     const uint32_t* pre;      // [n_units + 1] token prefix over the launch's units
     const float* q;           // [B*Hq][D] queries
-    float* part;              // [n_units][G][r][2]: m, l (log2 domain)
+    float* part;              // [n_units][G][r][2]: m, l (log2 domain), slot-indexed
+    uint32_t* ctr;            // [1 + n_units]: token cursor, partial slots per unit; zero
+                              // on entry (two sets used alternately, see bos_finish_kernel)
+    uint32_t* ctr_next;       // the other set: zeroed by bos_finish_kernel for the next call
+    uint32_t ctr_len;         // entries per set
     float* z0;                // [U*r] token-0 logit (log2 domain)
     float* stats;             // [U*r][2]: M, L after finish
     double* alpha0;           // [U*r]
@@ -64,7 +71,7 @@ struct BosCfg {
     static constexpr int kStages = (192 * 1024) / kStageBytes > 16 ? 16 : (192 * 1024) / kStageBytes;
     static constexpr int kNK = D / 16;
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStages * (16 + 16) +
-                                      kBosCWarps * kBosHeads * 2 * 4;
+                                      kBosCWarps * kBosHeads * 2 * 4 + 16;  // + sm_slot[4]
 };
 
 // byte offset of (token, 16-byte chunk) in a K stage: swz<D> with kBosTok rows per half
@@ -79,8 +86,33 @@ __device__ __forceinline__ uint32_t bos_swz(uint32_t tok, uint32_t chunk) {
     }
 }
 
-__device__ __forceinline__ uint32_t bos_range_start(const BosArgs& a, uint32_t c) {
-    return (uint32_t)((uint64_t)c * a.pre[a.n_units] / a.G);
+__device__ __forceinline__ uint32_t bos_ld_volatile(const uint32_t* p) {
+    return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// one warp per head: the lanes fold the unit's partials (one per CTA that
+// streamed part of it; at most G), read from L2
+__device__ __forceinline__ void bos_finish_head(const BosArgs& a, uint32_t i, uint32_t h, uint32_t lane) {
+    const uint32_t n = min(__ldcg(&a.ctr[1 + i]), a.G);
+    double M = -INFINITY;
+    for (uint32_t j = lane; j < n; j += 32)
+        M = fmax(M, (double)__ldcg(&a.part[((size_t(i) * a.G + j) * a.r + h) * 2]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+    double S = 0.0;
+    for (uint32_t j = lane; j < n; j += 32) {
+        const float* P = a.part + ((size_t(i) * a.G + j) * a.r + h) * 2;
+        const float pm = __ldcg(P);
+        if (pm != -INFINITY) S += (double)__ldcg(P + 1) * exp2((double)pm - M);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+    if (lane == 0) {
+        const size_t gi = size_t(a.u_first + i) * a.r + h;
+        a.stats[gi * 2] = (float)M;
+        a.stats[gi * 2 + 1] = (float)S;
+        a.alpha0[gi] = exp2((double)__ldcg(&a.z0[gi]) - M) / S;
+    }
 }
 
 template <int D>
@@ -93,6 +125,7 @@ __global__ void __launch_bounds__(kBosThreads, 1)
     uint64_t* empty = full + C::kStages;
     StageMeta* meta = reinterpret_cast<StageMeta*>(empty + C::kStages);
     float* sm_ml = reinterpret_cast<float*>(meta + C::kStages);  // [kBosCWarps][kBosHeads][2]
+    uint32_t* sm_slot = reinterpret_cast<uint32_t*>(sm_ml + kBosCWarps * kBosHeads * 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t c = blockIdx.x;
@@ -110,215 +143,215 @@ __global__ void __launch_bounds__(kBosThreads, 1)
         if (lane == 0) {
             ptx::tma_prefetch_desc(&tmk);
             const uint64_t pol = ptx::policy_evict_first();
-            const uint32_t p0 = bos_range_start(a, c), p1 = bos_range_start(a, c + 1);
-            uint32_t i = 0;  // launch-relative unit holding p0
-            while (i + 1 < a.n_units && a.pre[i + 1] <= p0) ++i;
+            // guided self-scheduling over the flat token space (the units laid
+            // end to end): a static first range of 2T/(3G) tokens per CTA, then
+            // claims from one cursor whose size shrinks with the remaining
+            // tokens, (T - pos)/(2G), down to one stage, so all SMs finish
+            // within about a stage of each other.  Claims only move forward, so
+            // a CTA meets each unit in one run and flushes it at most once.
+            const uint32_t T = a.pre[a.n_units], G = gridDim.x;
+            const uint32_t S0 = (uint32_t)((uint64_t)T * 2 / (3ull * G)) / kBosTok * kBosTok;
+            const uint32_t base = (uint32_t)min((uint64_t)S0 * G, (uint64_t)T);
+            const uint32_t cap_tok = max(S0, (uint32_t)kBosTok);
+            auto guided = [&](uint32_t pos) {
+                const uint32_t rem = T > pos ? T - pos : 0u;
+                const uint32_t sz = rem / (2 * G) / kBosTok * kBosTok;
+                return sz < (uint32_t)kBosTok ? (uint32_t)kBosTok : (sz > cap_tok ? cap_tok : sz);
+            };
             int stage = 0;
             uint32_t phase = 0;
-            for (uint32_t p = p0; p < p1; ++i) {
-                const uint32_t ub = a.pre[i], ue = min(a.pre[i + 1], p1);
-                const int32_t row0 = (int32_t)(size_t(a.slot0 + a.u_first + i) * a.cap);
-                for (uint32_t tk = p - ub; tk < ue - ub; tk += kBosTok) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1u);
-                    meta[stage].unit = i;
-                    meta[stage].tok0 = tk;
-                    meta[stage].ntok = min((uint32_t)kBosTok, ue - ub - tk);
-                    ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                    uint8_t* kd = ring + stage * C::kStageBytes;
-#pragma unroll
-                    for (int hh = 0; hh < C::kHalves; ++hh)
-#pragma unroll
-                        for (int bx = 0; bx < kBosBoxes; ++bx)
-                            ptx::tma_load_2d(kd + (hh * kBosTok + bx * kStageTok) * (D >= 64 ? 128 : 2 * D),
-                                             &tmk, hh * C::kBoxDim, row0 + (int32_t)(tk + bx * kStageTok),
-                                             &full[stage], pol);
-                    if (++stage == C::kStages) {
-                        stage = 0;
-                        phase ^= 1u;
+            uint32_t i = 0;  // launch-relative unit of g0
+            uint32_t g0 = min(c * S0, base), g1 = min(g0 + S0, base);
+            for (;;) {
+                // prefetch the next claim, sized from the live cursor
+                const uint32_t sz = guided(base + bos_ld_volatile(a.ctr));
+                const uint32_t n0 = base + atomicAdd(a.ctr, sz);
+                while (g0 < g1) {
+                    if (a.pre[i + 1] <= g0) {  // binary search forward
+                        uint32_t lo = i + 1, hi = a.n_units;
+                        while (hi - lo > 1) {
+                            const uint32_t mid = (lo + hi) >> 1;
+                            if (a.pre[mid] <= g0) lo = mid; else hi = mid;
+                        }
+                        i = lo;
                     }
+                    const uint32_t ub = a.pre[i], ue = min(a.pre[i + 1], g1);
+                    const int32_t row0 = (int32_t)(size_t(a.slot0 + a.u_first + i) * a.cap);
+                    for (uint32_t tk = g0 - ub; tk < ue - ub; tk += kBosTok) {
+                        ptx::mbar_wait(&empty[stage], phase ^ 1u);
+                        meta[stage].unit = i;
+                        meta[stage].tok0 = tk;
+                        meta[stage].ntok = min((uint32_t)kBosTok, ue - ub - tk);
+                        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+                        uint8_t* kd = ring + stage * C::kStageBytes;
+#pragma unroll
+                        for (int hh = 0; hh < C::kHalves; ++hh)
+#pragma unroll
+                            for (int bx = 0; bx < kBosBoxes; ++bx)
+                                ptx::tma_load_2d(kd + (hh * kBosTok + bx * kStageTok) * (D >= 64 ? 128 : 2 * D),
+                                                 &tmk, hh * C::kBoxDim, row0 + (int32_t)(tk + bx * kStageTok),
+                                                 &full[stage], pol);
+                        if (++stage == C::kStages) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    }
+                    g0 = ue;
                 }
-                p = ue;
+                if (n0 >= T) break;
+                g0 = n0;
+                g1 = min(n0 + sz, T);
             }
             ptx::mbar_wait(&empty[stage], phase ^ 1u);
             meta[stage].unit = kEnd;
             ptx::mbar_arrive(&full[stage]);
         }
-        return;
-    }
+    } else {
+        // ------------------------------ consumers ------------------------------
+        const int cw = warp - 1;
+        const uint32_t ctid = threadIdx.x - 32;
+        const int tb = cw * kWarpTok;
+        const int grp = lane >> 2, qd = lane & 3;
+        const int lj = lane >> 3, li = lane & 7;
+        const uint32_t k_tok = tb + ((lj >> 1) << 3) + li, k_csel = lj & 1;
+        const uint32_t nh = min((uint32_t)kBosHeads, a.r - h0);
+        const bool live = grp < (int)nh;
 
-    // ------------------------------ consumers ------------------------------
-    const int cw = warp - 1;
-    const uint32_t ctid = threadIdx.x - 32;
-    const int tb = cw * kWarpTok;
-    const int grp = lane >> 2, qd = lane & 3;
-    const int lj = lane >> 3, li = lane & 7;
-    const uint32_t k_tok = tb + ((lj >> 1) << 3) + li, k_csel = lj & 1;
-    const uint32_t nh = min((uint32_t)kBosHeads, a.r - h0);
-    const bool live = grp < (int)nh;
+        uint32_t q1[C::kNK][4], q2[C::kNK][2];  // A1 = [hi; lo], A2 = [lo2; 0]
+        float m = -INFINITY, l = 0.f;
+        uint32_t cur = kEnd;
 
-    uint32_t q1[C::kNK][4], q2[C::kNK][2];  // A1 = [hi; lo], A2 = [lo2; 0]
-    float m = -INFINITY, l = 0.f;
-    uint32_t cur = kEnd;
-
-    auto load_q = [&](uint32_t i) {
-        const float* qrow = a.q + (size_t(a.u_first + i) * a.r + h0 + (live ? grp : 0)) * D;
-#pragma unroll
-        for (int kk = 0; kk < C::kNK; ++kk) {
-#pragma unroll
-            for (int hv = 0; hv < 2; ++hv) {
-                float2 x = make_float2(0.f, 0.f);
-                if (live) x = *reinterpret_cast<const float2*>(qrow + 16 * kk + 8 * hv + 2 * qd);
-                x.x *= a.qscale;
-                x.y *= a.qscale;
-                const uint32_t hi = ptx::pack_bf16(x.x, x.y);
-                const float r0 = x.x - ptx::bf16_lo_as_f32(hi), r1 = x.y - ptx::bf16_hi_as_f32(hi);
-                const uint32_t lo = ptx::pack_bf16(r0, r1);
-                q1[kk][2 * hv] = hi;
-                q1[kk][2 * hv + 1] = lo;
-                q2[kk][hv] = ptx::pack_bf16(r0 - ptx::bf16_lo_as_f32(lo), r1 - ptx::bf16_hi_as_f32(lo));
-            }
-        }
-    };
-    auto flush = [&](uint32_t i) {
-        float mo = __shfl_xor_sync(0xffffffffu, m, 1), lo = __shfl_xor_sync(0xffffffffu, l, 1);
-        float mx = fmaxf(m, mo);
-        l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
-        m = mx;
-        mo = __shfl_xor_sync(0xffffffffu, m, 2);
-        lo = __shfl_xor_sync(0xffffffffu, l, 2);
-        mx = fmaxf(m, mo);
-        l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
-        m = mx;
-        if (qd == 0) {
-            sm_ml[(cw * kBosHeads + grp) * 2] = m;
-            sm_ml[(cw * kBosHeads + grp) * 2 + 1] = l;
-        }
-        ptx::named_bar_sync(1, kBosCWarps * 32);
-        if (ctid < nh) {
-            float M = -INFINITY;
-#pragma unroll
-            for (int w = 0; w < kBosCWarps; ++w) M = fmaxf(M, sm_ml[(w * kBosHeads + ctid) * 2]);
-            float S = 0.f;
-            if (M != -INFINITY)
-#pragma unroll
-                for (int w = 0; w < kBosCWarps; ++w)
-                    S += sm_ml[(w * kBosHeads + ctid) * 2 + 1] * exp2f(sm_ml[(w * kBosHeads + ctid) * 2] - M);
-            float* P = a.part + ((size_t(i) * a.G + c) * a.r + h0 + ctid) * 2;
-            P[0] = M;
-            P[1] = S;
-        }
-        ptx::named_bar_sync(1, kBosCWarps * 32);
-    };
-
-    int stage = 0;
-    uint32_t phase = 0;
-    for (;;) {
-        ptx::mbar_wait(&full[stage], phase);
-        const uint32_t unit = meta[stage].unit;
-        if (unit == kEnd) break;
-        if (unit != cur) {
-            if (cur != kEnd) flush(cur);
-            cur = unit;
-            load_q(unit);
-            m = -INFINITY;
-            l = 0.f;
-        }
-        const uint32_t tok0 = meta[stage].tok0;
-        const int n = (int)meta[stage].ntok - tb;
-        if (n > 0) {
-            const uint32_t kbase = ptx::smem_u32(ring + stage * C::kStageBytes);
-            float s1[2][2][4], s2[2][4];
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-                s2[x][0] = s2[x][1] = s2[x][2] = s2[x][3] = 0.f;
-#pragma unroll
-                for (int y = 0; y < 2; ++y) s1[x][y][0] = s1[x][y][1] = s1[x][y][2] = s1[x][y][3] = 0.f;
-            }
+        auto load_q = [&](uint32_t i) {
+            const float* qrow = a.q + (size_t(a.u_first + i) * a.r + h0 + (live ? grp : 0)) * D;
 #pragma unroll
             for (int kk = 0; kk < C::kNK; ++kk) {
-                uint32_t b[4];
-                ptx::ldsm_x4(b, kbase + bos_swz<D>(k_tok, 2 * kk + k_csel));
-                const uint32_t a2[4] = {q2[kk][0], 0u, q2[kk][1], 0u};
-                ptx::mma_bf16(s1[0][kk & 1], q1[kk], b[0], b[1]);
-                ptx::mma_bf16(s1[1][kk & 1], q1[kk], b[2], b[3]);
-                ptx::mma_bf16(s2[0], a2, b[0], b[1]);
-                ptx::mma_bf16(s2[1], a2, b[2], b[3]);
-            }
-            float z[4];
-            float bm = -INFINITY;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int nt = j >> 1, col = j & 1;
-                const float hi = s1[nt][0][col] + s1[nt][1][col];
-                const float lo = s1[nt][0][col + 2] + s1[nt][1][col + 2];
-                const int tok = nt * 8 + 2 * qd + col;
-                z[j] = tok < n ? (hi + lo) + s2[nt][col] : -INFINITY;
-                bm = fmaxf(bm, z[j]);
-            }
-            if (tok0 + tb == 0 && live && qd == 0)  // token 0 of the unit: j = 0 of lane quad 0
-                a.z0[size_t(a.u_first + unit) * a.r + h0 + grp] = z[0];
-            if (a.zout != nullptr && live) {  // attention_weights: keep every logit
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int tok = (j >> 1) * 8 + 2 * qd + (j & 1);
-                    if (tok < n) a.zout[size_t(h0 + grp) * a.pre[1] + tok0 + tb + tok] = z[j];
+                for (int hv = 0; hv < 2; ++hv) {
+                    float2 x = make_float2(0.f, 0.f);
+                    if (live) x = *reinterpret_cast<const float2*>(qrow + 16 * kk + 8 * hv + 2 * qd);
+                    x.x *= a.qscale;
+                    x.y *= a.qscale;
+                    const uint32_t hi = ptx::pack_bf16(x.x, x.y);
+                    const float r0 = x.x - ptx::bf16_lo_as_f32(hi), r1 = x.y - ptx::bf16_hi_as_f32(hi);
+                    const uint32_t lo = ptx::pack_bf16(r0, r1);
+                    q1[kk][2 * hv] = hi;
+                    q1[kk][2 * hv + 1] = lo;
+                    q2[kk][hv] = ptx::pack_bf16(r0 - ptx::bf16_lo_as_f32(lo), r1 - ptx::bf16_hi_as_f32(lo));
                 }
             }
-            if (bm != -INFINITY) {
-                const float mn = fmaxf(m, bm);
-                l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) +
-                    ((exp2f(z[0] - mn) + exp2f(z[1] - mn)) + (exp2f(z[2] - mn) + exp2f(z[3] - mn)));
-                m = mn;
+        };
+        auto flush = [&](uint32_t i) {
+            float mo = __shfl_xor_sync(0xffffffffu, m, 1), lo = __shfl_xor_sync(0xffffffffu, l, 1);
+            float mx = fmaxf(m, mo);
+            l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
+            m = mx;
+            mo = __shfl_xor_sync(0xffffffffu, m, 2);
+            lo = __shfl_xor_sync(0xffffffffu, l, 2);
+            mx = fmaxf(m, mo);
+            l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
+            m = mx;
+            if (qd == 0) {
+                sm_ml[(cw * kBosHeads + grp) * 2] = m;
+                sm_ml[(cw * kBosHeads + grp) * 2 + 1] = l;
+            }
+            if (ctid == 0) sm_slot[0] = atomicAdd(&a.ctr[1 + i], 1u);
+            ptx::named_bar_sync(1, kBosCWarps * 32);
+            if (ctid < nh) {
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kBosCWarps; ++w) M = fmaxf(M, sm_ml[(w * kBosHeads + ctid) * 2]);
+                float S = 0.f;
+                if (M != -INFINITY)
+#pragma unroll
+                    for (int w = 0; w < kBosCWarps; ++w)
+                        S += sm_ml[(w * kBosHeads + ctid) * 2 + 1] * exp2f(sm_ml[(w * kBosHeads + ctid) * 2] - M);
+                float* P = a.part + ((size_t(i) * a.G + sm_slot[0]) * a.r + h0 + ctid) * 2;
+                P[0] = M;
+                P[1] = S;
+            }
+            ptx::named_bar_sync(1, kBosCWarps * 32);
+        };
+
+        int stage = 0;
+        uint32_t phase = 0;
+        for (;;) {
+            ptx::mbar_wait(&full[stage], phase);
+            const uint32_t unit = meta[stage].unit;
+            if (unit == kEnd) break;
+            if (unit != cur) {
+                if (cur != kEnd) flush(cur);
+                cur = unit;
+                load_q(unit);
+                m = -INFINITY;
+                l = 0.f;
+            }
+            const uint32_t tok0 = meta[stage].tok0;
+            const int n = (int)meta[stage].ntok - tb;
+            if (n > 0) {
+                const uint32_t kbase = ptx::smem_u32(ring + stage * C::kStageBytes);
+                float s1[2][2][4], s2[2][4];
+#pragma unroll
+                for (int x = 0; x < 2; ++x) {
+                    s2[x][0] = s2[x][1] = s2[x][2] = s2[x][3] = 0.f;
+#pragma unroll
+                    for (int y = 0; y < 2; ++y) s1[x][y][0] = s1[x][y][1] = s1[x][y][2] = s1[x][y][3] = 0.f;
+                }
+#pragma unroll
+                for (int kk = 0; kk < C::kNK; ++kk) {
+                    uint32_t b[4];
+                    ptx::ldsm_x4(b, kbase + bos_swz<D>(k_tok, 2 * kk + k_csel));
+                    const uint32_t a2[4] = {q2[kk][0], 0u, q2[kk][1], 0u};
+                    ptx::mma_bf16(s1[0][kk & 1], q1[kk], b[0], b[1]);
+                    ptx::mma_bf16(s1[1][kk & 1], q1[kk], b[2], b[3]);
+                    ptx::mma_bf16(s2[0], a2, b[0], b[1]);
+                    ptx::mma_bf16(s2[1], a2, b[2], b[3]);
+                }
+                float z[4];
+                float bm = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int nt = j >> 1, col = j & 1;
+                    const float hi = s1[nt][0][col] + s1[nt][1][col];
+                    const float lo = s1[nt][0][col + 2] + s1[nt][1][col + 2];
+                    const int tok = nt * 8 + 2 * qd + col;
+                    z[j] = tok < n ? (hi + lo) + s2[nt][col] : -INFINITY;
+                    bm = fmaxf(bm, z[j]);
+                }
+                if (tok0 + tb == 0 && live && qd == 0)  // token 0 of the unit: j = 0 of lane quad 0
+                    a.z0[size_t(a.u_first + unit) * a.r + h0 + grp] = z[0];
+                if (a.zout != nullptr && live) {  // attention_weights: keep every logit
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int tok = (j >> 1) * 8 + 2 * qd + (j & 1);
+                        if (tok < n) a.zout[size_t(h0 + grp) * a.pre[1] + tok0 + tb + tok] = z[j];
+                    }
+                }
+                if (bm != -INFINITY) {
+                    const float mn = fmaxf(m, bm);
+                    l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) +
+                        ((exp2f(z[0] - mn) + exp2f(z[1] - mn)) + (exp2f(z[2] - mn) + exp2f(z[3] - mn)));
+                    m = mn;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+            if (++stage == C::kStages) {
+                stage = 0;
+                phase ^= 1u;
             }
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[stage]);
-        if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1u;
-        }
+        if (cur != kEnd) flush(cur);
     }
-    if (cur != kEnd) flush(cur);
+
 }
 
-constexpr int kBosMaxG = 1024;  // stream CTAs the finish kernel can index
-
-// one warp per head: the lanes fold the CTA partials of the head's unit
+// one warp per head (grid-wide), then zero the counter set of the next call
 __global__ void __launch_bounds__(256) bos_finish_kernel(BosArgs a) {
-    __shared__ uint32_t s_start[kBosMaxG + 1];  // CTA range starts, computed once per block
-    for (uint32_t c = threadIdx.x; c <= a.G; c += blockDim.x) s_start[c] = bos_range_start(a, c);
-    __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // head within the launch
-    if (idx >= a.n_units * a.r) return;
-    const uint32_t i = idx / a.r, h = idx % a.r;
-    const uint32_t ub = a.pre[i], ue = a.pre[i + 1];
-    // first CTA whose range ends past ub (ranges are sorted and contiguous)
-    uint32_t lo = 0, hi = a.G;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_start[mid + 1] <= ub) lo = mid + 1; else hi = mid;
-    }
-    double M = -INFINITY;
-    for (uint32_t c = lo + lane; c < a.G && s_start[c] < ue; c += 32)
-        if (s_start[c] < s_start[c + 1])  // an empty range wrote no partial
-            M = fmax(M, (double)a.part[((size_t(i) * a.G + c) * a.r + h) * 2]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
-    double S = 0.0;
-    for (uint32_t c = lo + lane; c < a.G && s_start[c] < ue; c += 32) {
-        if (s_start[c] == s_start[c + 1]) continue;
-        const float* P = a.part + ((size_t(i) * a.G + c) * a.r + h) * 2;
-        if (P[0] != -INFINITY) S += (double)P[1] * exp2((double)P[0] - M);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
-    if (lane == 0) {
-        const size_t gi = size_t(a.u_first + i) * a.r + h;
-        a.stats[gi * 2] = (float)M;
-        a.stats[gi * 2 + 1] = (float)S;
-        a.alpha0[gi] = exp2((double)a.z0[gi] - M) / S;
-    }
+    const uint32_t idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.ctr_len; j += gridDim.x * blockDim.x)
+        a.ctr_next[j] = 0;
+    if (idx < a.n_units * a.r) bos_finish_head(a, idx / a.r, idx % a.r, lane);
 }
 
 // attention_weights of unit u_first from the stream pass's logits

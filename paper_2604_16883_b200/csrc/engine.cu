@@ -133,6 +133,7 @@ struct sinkr_engine {
     size_t bos_bytes = 0;
     uint8_t* h_bos = nullptr;            // pinned staging for run_bos (prefix up, alpha0 down)
     cudaEvent_t ev_bos[2] = {};          // around run_bos's kernels (device time)
+    uint32_t bos_parity = 0;             // which counter set the next run_bos uses
     float bos_ms = -1.f;
     size_t h_bos_bytes = 0;
     uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [U]
@@ -1282,10 +1283,11 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     const uint32_t T = pre[n_units];
     // one stream CTA per SM (the ring takes ~128 KB), >= one stage of tokens each
     const uint32_t G = std::max<uint32_t>(
-        1, std::min<uint32_t>({(uint32_t)e->num_sms, (T + dev::kStageTok - 1) / dev::kStageTok,
-                               (uint32_t)dev::kBosMaxG}));
-    // scratch: pre[n+1] | part[n][G][r][2] | z0[U*r] | stats[U*r][2] | alpha0[U*r] f64 | logits | weights
-    const size_t off_part = align_up((n_units + 1) * 4, 256);
+        1, std::min<uint32_t>((uint32_t)e->num_sms, (T + dev::kBosTok - 1) / dev::kBosTok));
+    // scratch: ctr[2][1+U] (zeroed at allocation; each call's finish zeroes the other set) | pre[n+1] |
+    //          part[n][G][r][2] | z0[U*r] | stats[U*r][2] | alpha0[U*r] f64 | logits | weights
+    const size_t off_pre = align_up(2 * (1 + U) * 4, 256);
+    const size_t off_part = align_up(off_pre + (n_units + 1) * 4, 256);
     const size_t off_z0 = align_up(off_part + (size_t)n_units * G * r * 2 * 4, 256);
     const size_t off_st = align_up(off_z0 + U * r * 4, 256);
     const size_t off_a0 = align_up(off_st + U * r * 2 * 4, 256);
@@ -1299,6 +1301,8 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
         e->d_bos = nullptr;
         e->bos_bytes = 0;
         CK(cudaMalloc(&e->d_bos, need));
+        CK(cudaMemsetAsync(e->d_bos, 0, 2 * (1 + U) * 4, e->stream));
+        e->bos_parity = 0;
         e->bos_bytes = need;
     }
     uint8_t* scratch = e->d_bos;
@@ -1317,11 +1321,15 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     std::memcpy(e->h_bos, pre.data(), (n_units + 1) * 4);
     CK(cudaMemcpyAsync(e->d_in + e->off_q + q_offset * 4, e->h_in + e->off_q + q_offset * 4,
                        q_floats * 4, cudaMemcpyHostToDevice, e->stream));
-    CK(cudaMemcpyAsync(scratch, e->h_bos, (n_units + 1) * 4, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(scratch + off_pre, e->h_bos, (n_units + 1) * 4, cudaMemcpyHostToDevice, e->stream));
     dev::BosArgs a{};
-    a.pre = reinterpret_cast<const uint32_t*>(scratch);
+    a.pre = reinterpret_cast<const uint32_t*>(scratch + off_pre);
     a.q = reinterpret_cast<const float*>(e->d_in + e->off_q);
     a.part = reinterpret_cast<float*>(scratch + off_part);
+    a.ctr = reinterpret_cast<uint32_t*>(scratch) + e->bos_parity * (1 + U);
+    a.ctr_next = reinterpret_cast<uint32_t*>(scratch) + (1 - e->bos_parity) * (1 + U);
+    a.ctr_len = (uint32_t)(1 + U);
+    e->bos_parity ^= 1u;
     a.z0 = reinterpret_cast<float*>(scratch + off_z0);
     a.stats = reinterpret_cast<float*>(scratch + off_st);
     a.alpha0 = reinterpret_cast<double*>(scratch + off_a0);
@@ -1336,10 +1344,9 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     a.G = G;
     a.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
     CK(cudaEventRecord(e->ev_bos[0], e->stream));
-    for (uint32_t h0 = 0; h0 < r; h0 += dev::kBosHeads) {
-        launch_bos(e, a, h0);
-    }
-    dev::bos_finish_kernel<<<(nh + 7) / 8, 256, 0, e->stream>>>(a);
+    static_assert(dev::kBosHeads >= dev::kMaxR, "one stream pass covers a GQA group");
+    launch_bos(e, a, 0);
+    dev::bos_finish_kernel<<<std::max<uint32_t>(1, (nh + 7) / 8), 256, 0, e->stream>>>(a);
     if (weights) {
         const uint32_t blocks = std::min<uint32_t>((uint32_t)((r * (size_t)T + 255) / 256),
                                                    8u * (uint32_t)e->num_sms);
