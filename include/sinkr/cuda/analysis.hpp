@@ -81,4 +81,11 @@ inline std::vector<float> attention_weights(const KvCache& cache, std::span<cons
     return w;
 }
 
+// Device time of the last attention_bos_mass / attention_weights call's kernels.
+inline double last_kernel_seconds(const KvCache& cache) {
+    double s = 0.0;
+    check(sinkr_attention_last_kernel_seconds(cache.handle(), &s));
+    return s;
+}
+
 }  // namespace sinkr::cuda

@@ -114,6 +114,7 @@ int main() {
     for (double a : a0) REQUIRE(a > 0.0 && a < 1.0);
     const auto w = sc::attention_weights(cache, std::span<const float>(q.data(), 4 * D), 1, 0);
     REQUIRE(w.size() == 4 * L && std::fabs(w[0] - a0[0]) < 1e-6);
+    REQUIRE(sc::last_kernel_seconds(cache) > 0.0);
     const auto labs = sc::oracle_labels(w, 4, L, 0.65, sc::OracleMode::GroupMean);
     REQUIRE(labs.size() == 1 && !labs[0].is_sink);
     const std::vector<double> sco{0.9, 0.8, 0.3, 0.1};
