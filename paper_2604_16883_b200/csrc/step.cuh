@@ -842,11 +842,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // An exhausted unit hands the CTA on to the unit with the most
                 // unclaimed rows (all cursors read in parallel, 16 loads in
                 // flight), so the tail is spent streaming, not probing.
+                // The lead CTA (bid 0) has no static range: its consumers are
+                // busy with the routing record for the first microseconds, so
+                // it starts on dynamic claims; entry 0's static ranges go to
+                // CTAs nact, 2 nact, ... (chunk k - 1).
                 const uint32_t cpu = (G + nact - 1) / nact;  // CTAs per unit
+                auto static_end = [&](uint32_t e) {        // statically covered prefix of entry e
+                    return (((G - e + nact - 1) / nact) - (e == 0 ? 1u : 0u)) * Ck;
+                };
                 uint32_t a = bid % nact;
                 uint32_t u = act_unit[a], L = act_len[a];
-                uint32_t first = ((G - a + nact - 1) / nact) * Ck;
-                uint32_t t0 = (bid / nact) * Ck, t1 = min(t0 + Ck, L);
+                uint32_t first = static_end(a);
+                const uint32_t k0 = bid / nact - (a == 0 ? 1u : 0u);  // bid 0: wraps, no static range
+                uint32_t t0 = bid == 0 ? L : k0 * Ck, t1 = min(t0 + Ck, L);
                 auto guided = [&](uint32_t hint) {
                     const uint32_t rem = L > hint ? L - hint : 0u;
                     uint32_t sz = rem / (3 * cpu);
@@ -865,7 +873,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int k = 0; k < 16; ++k) {
                                 const uint32_t b = b0 + k;
                                 if (b < nact) {
-                                    const uint32_t pos = ((G - b + nact - 1) / nact) * Ck + cur[k];
+                                    const uint32_t pos = static_end(b) + cur[k];
                                     const uint32_t rem = act_len[b] > pos ? act_len[b] - pos : 0u;
                                     if (rem > best_rem) {
                                         best_rem = rem;
@@ -878,7 +886,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         a = best;
                         u = act_unit[a];
                         L = act_len[a];
-                        first = ((G - a + nact - 1) / nact) * Ck;
+                        first = static_end(a);
                         // a hand-off claim is sized from the unit's live remainder
                         const uint32_t sz = guided(L - best_rem);
                         t0 = first + atomicAdd(&t.cursor[a], sz);
