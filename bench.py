@@ -195,8 +195,10 @@ def run_reference_arm(args, world, rank):
     threads = os.cpu_count() or 1
     spec = WorkloadSpec(**SHAPE, length=args.length, sink_fraction=args.sink_fraction,
                         seed=args.seed)
-    steps = max(1, min(args.steps, 10))
-    warm = max(0, min(args.warmup, 1))
+    # a routed step of the reference is ~70 ms on 16 host threads: honour K and
+    # W up to 50 / 10 (a few seconds); the cache fill dominates the run
+    steps = max(1, min(args.steps, 50))
+    warm = max(0, min(args.warmup, 10))
     _, res, ts = time_reference(spec, steps, warm, threads)
     us = sum(ts) / len(ts) * 1e6
     n_act = int(res.counters["groups_active"])
