@@ -780,9 +780,10 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             if (const char* ds = std::getenv("SINKR_DEBUG_SLOTS"); ds && std::atoi(ds) >= 2)
                 e->S = (size_t)std::atoi(ds);
             e->PS = e->r * (e->D + 2);
-            CK(cudaMalloc(&e->d_partials, e->U * e->S * e->PS * 4));
+            // + 64 slots: warp_merge loads groups of 64 slots unpredicated
+            CK(cudaMalloc(&e->d_partials, (e->U * e->S + 64) * e->PS * 4));
             // combine reads candidate slots speculatively: keep them finite
-            CK(cudaMemsetAsync(e->d_partials, 0, e->U * e->S * e->PS * 4, e->stream));
+            CK(cudaMemsetAsync(e->d_partials, 0, (e->U * e->S + 64) * e->PS * 4, e->stream));
 
             make_tmap(&e->tmk, e->d_k, rows, e->D);
             make_tmap(&e->tmv, e->d_v, rows, e->D);

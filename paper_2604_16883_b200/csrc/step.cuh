@@ -131,10 +131,16 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 // weights 2^(m_j - max) reach the lanes by shuffle.  One L2 round trip per 64
 // partials.  Writes the normalised row (mode 0), an un-normalised rank partial
 // (mode 1), or that partial into every rank's exchange block (mode 3).
-template <int D>
+template <int D, int R>
 __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
                                            uint32_t lane, size_t xoff) {
-    const uint32_t r = t.r, PS = r * (D + 2);
+    // R = t.r at compile time: the partial stride is an immediate, so each of
+    // the 64 acc loads is one LDG with an immediate offset.  This loop is cold
+    // code at the end of every step, and instruction fetch from DRAM costs
+    // (DESIGN.md §4).  Loads past slot_count are unpredicated: the partial
+    // block is padded by 64 slots and zero-initialised, every slot holds
+    // finite values, and their weights are 0.
+    constexpr uint32_t r = R, PS = R * (D + 2);
     const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
     const float* base = t.partials + size_t(u) * t.S * PS;
     const uint32_t d = d0 + lane;
@@ -147,9 +153,9 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
             mv[c] = j < n ? __ldcg(base + size_t(j) * PS + h) : -INFINITY;
             lv[c] = j < n ? __ldcg(base + size_t(j) * PS + r + h) : 0.f;
         }
+        const float* pa = base + size_t(j0) * PS + 2 * r + h * D + d;
 #pragma unroll
-        for (int k = 0; k < 64; ++k)
-            av[k] = (j0 + k < n) ? __ldcg(base + size_t(j0 + k) * PS + 2 * r + h * D + d) : 0.f;
+        for (int k = 0; k < 64; ++k) av[k] = __ldcg(pa + k * PS);
         float cm = fmaxf(mv[0], mv[1]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
@@ -190,6 +196,22 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
             }
             P[2 * r + h * D + d] = acc;
         }
+    }
+}
+
+// warp_merge for the runtime GQA width
+template <int D>
+__device__ __forceinline__ void warp_merge_r(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
+                                             uint32_t lane, size_t xoff) {
+    switch (t.r) {
+        case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff); break;
+        case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff); break;
+        case 3: warp_merge<D, 3>(t, u, h, d0, lane, xoff); break;
+        case 4: warp_merge<D, 4>(t, u, h, d0, lane, xoff); break;
+        case 5: warp_merge<D, 5>(t, u, h, d0, lane, xoff); break;
+        case 6: warp_merge<D, 6>(t, u, h, d0, lane, xoff); break;
+        case 7: warp_merge<D, 7>(t, u, h, d0, lane, xoff); break;
+        default: warp_merge<D, 8>(t, u, h, d0, lane, xoff); break;
     }
 }
 
@@ -1121,7 +1143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // merge every partial of unit u (consumers only; few partials)
         auto merge_unit = [&](uint32_t u, uint32_t L) {
             for (uint32_t task = cw; task < r * (D / 32); task += kCWarps)
-                warp_merge<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff);
+                warp_merge_r<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff);
             if (ctid == 0) t.tokens[u] = L;
         };
         auto flush = [&](uint32_t u, uint32_t L) {
@@ -1334,7 +1356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
             }
             __syncwarp();
-            warp_merge<D>(t, u, h, d - lane, lane, xoff);
+            warp_merge_r<D>(t, u, h, d - lane, lane, xoff);
             if (h == 0 && d == 0) t.tokens[u] = L;
         }
     }
