@@ -41,7 +41,7 @@ constexpr int kBosCWarps = 8;                  // consumer warps, 16 tokens each
 constexpr int kBosThreads = 32 * (1 + kBosCWarps);
 constexpr int kBosTok = kWarpTok * kBosCWarps;  // tokens per stage (2 per SMSP in flight)
 constexpr int kBosBoxes = kBosTok / kStageTok;  // 64-row TMA boxes per stage and half
-constexpr int kBosHeads = 8;                   // heads per pass (mma rows 0-7)
+constexpr int kBosHeads = 8;                   // heads per unit (mma rows 0-7)
 static_assert(kBosCWarps >= kMaxR, "the unit merge takes one consumer warp per head");
 
 struct BosArgs {
@@ -57,7 +57,7 @@ struct BosArgs {
     double* alpha0;           // [U*r]
     float* zout;              // logits [r][L] of the launch's only unit, or null
     float* weights;           // weights_kernel: [r][L] of unit u_first
-    uint32_t U, r, cap, slot0;  // slot0 = layer * U
+    uint32_t r, cap, slot0;     // slot0 = layer * (units per layer)
     uint32_t u_first, n_units;  // units of this launch
     uint32_t G;                 // stream CTAs
     float qscale;               // log2(e) / sqrt(D)
@@ -117,7 +117,7 @@ __device__ __forceinline__ void bos_finish_head(const BosArgs& a, uint32_t i, ui
 
 template <int D>
 __global__ void __launch_bounds__(kBosThreads, 1)
-    bos_stream_kernel(const __grid_constant__ CUtensorMap tmk, BosArgs a, uint32_t h0) {
+    bos_stream_kernel(const __grid_constant__ CUtensorMap tmk, BosArgs a) {
     using C = BosCfg<D>;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     uint8_t* ring = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kBosThreads, 1)
         const int grp = lane >> 2, qd = lane & 3;
         const int lj = lane >> 3, li = lane & 7;
         const uint32_t k_tok = tb + ((lj >> 1) << 3) + li, k_csel = lj & 1;
-        const uint32_t nh = min((uint32_t)kBosHeads, a.r - h0);
+        const uint32_t nh = a.r;  // <= kMaxR <= kBosHeads: one pass covers the group
         const bool live = grp < (int)nh;
 
         uint32_t q1[C::kNK][4], q2[C::kNK][2];  // A1 = [hi; lo], A2 = [lo2; 0]
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kBosThreads, 1)
         uint32_t cur = kEnd;
 
         auto load_q = [&](uint32_t i) {
-            const float* qrow = a.q + (size_t(a.u_first + i) * a.r + h0 + (live ? grp : 0)) * D;
+            const float* qrow = a.q + (size_t(a.u_first + i) * a.r + (live ? grp : 0)) * D;
 #pragma unroll
             for (int kk = 0; kk < C::kNK; ++kk) {
 #pragma unroll
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kBosThreads, 1)
 #pragma unroll
                     for (int w = 0; w < kBosCWarps; ++w)
                         S += sm_ml[(w * kBosHeads + ctid) * 2 + 1] * exp2f(sm_ml[(w * kBosHeads + ctid) * 2] - M);
-                float* P = a.part + ((size_t(i) * a.G + sm_slot[0]) * a.r + h0 + ctid) * 2;
+                float* P = a.part + ((size_t(i) * a.G + sm_slot[0]) * a.r + ctid) * 2;
                 P[0] = M;
                 P[1] = S;
             }
@@ -318,12 +318,12 @@ __global__ void __launch_bounds__(kBosThreads, 1)
                     bm = fmaxf(bm, z[j]);
                 }
                 if (tok0 + tb == 0 && live && qd == 0)  // token 0 of the unit: j = 0 of lane quad 0
-                    a.z0[size_t(a.u_first + unit) * a.r + h0 + grp] = z[0];
+                    a.z0[size_t(a.u_first + unit) * a.r + grp] = z[0];
                 if (a.zout != nullptr && live) {  // attention_weights: keep every logit
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const int tok = (j >> 1) * 8 + 2 * qd + (j & 1);
-                        if (tok < n) a.zout[size_t(h0 + grp) * a.pre[1] + tok0 + tb + tok] = z[j];
+                        if (tok < n) a.zout[size_t(grp) * a.pre[1] + tok0 + tb + tok] = z[j];
                     }
                 }
                 if (bm != -INFINITY) {

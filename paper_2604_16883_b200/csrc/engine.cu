@@ -1254,11 +1254,11 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
     });
 }
 
-static void launch_bos(sinkr_engine* e, const dev::BosArgs& a, uint32_t h0) {
+static void launch_bos(sinkr_engine* e, const dev::BosArgs& a) {
 #define SINKR_BOS_LAUNCH(DD)                                                                     \
     {                                                                                            \
         constexpr int smem = dev::BosCfg<DD>::kSmemBytes; /* attribute set at creation */     \
-        dev::bos_stream_kernel<DD><<<a.G, dev::kBosThreads, smem, e->stream>>>(e->tmk, a, h0);   \
+        dev::bos_stream_kernel<DD><<<a.G, dev::kBosThreads, smem, e->stream>>>(e->tmk, a);       \
     }
     switch (e->D) {
         case 32: SINKR_BOS_LAUNCH(32) break;
@@ -1336,7 +1336,6 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     a.alpha0 = reinterpret_cast<double*>(scratch + off_a0);
     a.zout = weights ? reinterpret_cast<float*>(scratch + off_z) : nullptr;
     a.weights = reinterpret_cast<float*>(scratch + off_w);
-    a.U = (uint32_t)U;
     a.r = (uint32_t)r;
     a.cap = (uint32_t)e->cap;
     a.slot0 = (uint32_t)(layer * U);
@@ -1346,7 +1345,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     a.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
     CK(cudaEventRecord(e->ev_bos[0], e->stream));
     static_assert(dev::kBosHeads >= dev::kMaxR, "one stream pass covers a GQA group");
-    launch_bos(e, a, 0);
+    launch_bos(e, a);
     dev::bos_finish_kernel<<<std::max<uint32_t>(1, (nh + 7) / 8), 256, 0, e->stream>>>(a);
     if (weights) {
         const uint32_t blocks = std::min<uint32_t>((uint32_t)((r * (size_t)T + 255) / 256),
