@@ -806,9 +806,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t nact = misc[kMiscNact];
     const uint32_t Ck = misc[kMiscChunk];
     const bool flat = misc[kMiscFlat] != 0;
-    // few, long Active groups: merge tasks spread over all CTAs at the end;
-    // many groups: the CTA that streams a group's last rows merges it.
-    const bool queue_mode = 4 * nact <= G;
+    // up to ~4 merge tasks (unit, head, 32 dims) per consumer warp: the tasks
+    // are spread over every warp once its stream ends; more: the CTA that
+    // streams a group's last rows merges it in line.  A/B (r01f, back to back):
+    // queue mode for all takes C3-dense (2,048 tasks) 959 -> 941 us and
+    // C5-routed (1,920) 309 -> 305 us, but C5-dense (5,120) 757 -> 761 us.
+    const bool queue_mode = nact * r * (D / 32) <= 16u * G;
     const bool lean_fast = lean && misc[kMiscFast] != 0;
     // mode 3: partial slots double-buffered by step parity (a rank one step
     // ahead never overwrites partials a slower rank is still merging).  The
