@@ -272,6 +272,29 @@ inline std::vector<std::pair<std::size_t, std::size_t>> split_ranges(std::size_t
     return out;
 }
 
+// SplitkResult / splitk_attention (attention.hpp:71-85) of one cached group on
+// the GPU: the group's r query heads over all of its rows.  num_splits is
+// validated like split_ranges; the kernel picks its own split.
+struct SplitkResult {
+    std::vector<float> out;  // heads x dim
+    LoadCounters counters;
+};
+
+inline SplitkResult splitk_attention(const KvCache& cache, std::span<const float> group_q,
+                                     std::size_t layer, std::size_t kv_head,
+                                     std::size_t num_splits, std::size_t seq = 0) {
+    const CacheConfig& cc = cache.config();
+    if (group_q.size() != cc.group_width() * cc.head_dim)
+        throw std::invalid_argument("query span size does not match heads x dim");
+    SplitkResult res;
+    res.out.resize(group_q.size());
+    sinkr_load_counters ctr{};
+    check(sinkr_group_attention(cache.handle(), group_q.data(), seq, layer, kv_head, num_splits,
+                                res.out.data(), &ctr));
+    res.counters.kv_floats_loaded = ctr.kv_floats_loaded;
+    return res;
+}
+
 // router.hpp:84-86 — one decode step for one layer (all B sequences).
 inline LayerStepResult routed_decode_step(std::span<const float> queries, std::size_t layer,
                                           const KvCache& cache, const RoutingConfig& config,

@@ -332,6 +332,17 @@ sinkr_status sinkr_kv_append_device_f32(sinkr_engine* e, size_t seq, size_t laye
                                         size_t kv_head, const float* d_k, const float* d_v,
                                         size_t rows);
 
+/* ---- single-group attention (attention.cpp:185-235, attention.hpp:76-85) ---
+ * splitk_attention of the r query heads of ONE cached group (seq, layer,
+ * kv_head) over all of its rows, on the GPU: out [r][D] f32, counters with
+ * kv_floats_loaded = 2 * len * D (the other fields 0).  num_splits is checked
+ * like split_ranges (INVALID_ARGUMENT outside [1, len]); the kernel picks its
+ * own split.  Runs as a routed step with the route forced, so it replaces the
+ * engine's last routing record (sinkr_fetch_step_info). */
+sinkr_status sinkr_group_attention(sinkr_engine* e, const float* group_queries, size_t seq,
+                                   size_t layer, size_t kv_head, size_t num_splits, float* out,
+                                   sinkr_load_counters* counters);
+
 /* ---- analysis (attention.cpp:75-99, analysis.hpp:12-39) ---
  * Full-attention BOS mass on the GPU for oracle sink labels: for every query
  * head, alpha0 = softmax(scale * q.K^T)[0] over the whole cached context of

@@ -30,6 +30,8 @@ from .router import (  # noqa: F401
     routed_decode_step,
     set_timing,
     split_ranges,
+    splitk_attention,
+    SplitkResult,
     threshold_for_length,
 )
 from .workload import WorkloadSpec  # noqa: F401

@@ -1174,6 +1174,73 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
     });
 }
 
+// splitk_attention (attention.cpp:204-235) of ONE cached group on the GPU:
+// the fused step kernel with the route forced (ProbeParams.only_unit), so the
+// group streams exactly like an Active group of a routed step and every other
+// group is skipped.  The split count is validated like split_ranges
+// (attention.cpp:185-190); the GPU picks its own split.
+sinkr_status sinkr_group_attention(sinkr_engine* e, const float* group_queries, size_t seq,
+                                   size_t layer, size_t kv_head, size_t num_splits, float* out,
+                                   sinkr_load_counters* counters) {
+    return guard([&] {
+        if (!e || !group_queries || !out) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        check_slot(e, seq, layer, kv_head);
+        const size_t L = e->len[e->slot_index(layer, seq, kv_head)];
+        if (L == 0) fail(SINKR_INVALID_ARGUMENT, "attention needs at least one token");
+        if (num_splits == 0 || num_splits > L)
+            fail(SINKR_INVALID_ARGUMENT, "num_splits must be in [1, len], got " +
+                                             std::to_string(num_splits) + " for len " +
+                                             std::to_string(L));
+        const size_t H = e->cfg.num_kv_heads, Hq = e->cfg.num_q_heads, r = e->r, D = e->D;
+        const size_t u = seq * H + kv_head, row0 = (seq * Hq + kv_head * r) * D;
+        CK(cudaEventSynchronize(e->ev_in));
+        auto* hdr = reinterpret_cast<dev::StepHdr*>(e->h_in);
+        auto* tau = reinterpret_cast<double*>(e->h_in + e->off_tau);
+        auto* len = reinterpret_cast<uint32_t*>(e->h_in + e->off_len);
+        hdr->layer = (uint32_t)layer;
+        hdr->flags = 0;
+        hdr->pad[0] = hdr->pad[1] = 0;
+        for (size_t s = 0; s < e->B; ++s) {
+            tau[s] = 2.0;  // (no decision is taken from it)
+            len[s] = s == seq ? (uint32_t)L : 0u;
+        }
+        std::memset(&e->pp, 0, sizeof(e->pp));
+        e->pp.layer = (uint32_t)layer;
+        e->pp.inline_seqs = e->B <= (size_t)dev::kParamSeqs ? 1u : 0u;
+        if (e->pp.inline_seqs)
+            for (size_t s = 0; s < e->B; ++s) {
+                e->pp.tau[s] = tau[s];
+                e->pp.len[s] = len[s];
+            }
+        e->pp.only_unit = (uint32_t)(u + 1);
+        e->params_valid = false;  // the next routed step uploads its own params
+        float* q = reinterpret_cast<float*>(e->h_in + e->off_q);
+        std::memset(q, 0, e->B * Hq * D * 4);
+        std::memcpy(q + row0, group_queries, r * D * 4);
+        if (e->fused && !e->timing && io_mode() != 0) {
+            run_io_graph(e);
+        } else {
+            CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
+            CK(cudaEventRecord(e->ev_in, e->stream));
+            run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q),
+                      reinterpret_cast<float*>(e->d_res), 0);
+            CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+        }
+        CK(cudaStreamSynchronize(e->stream));
+        e->pp.only_unit = 0;
+        const auto* fl = reinterpret_cast<const uint32_t*>(e->h_res + e->off_fl);
+        const auto* tok = reinterpret_cast<const unsigned long long*>(e->h_res + e->off_tok);
+        if (!(fl[u] & dev::kActive) || tok[u] != L)
+            fail(SINKR_RUNTIME_ERROR, "group attention: the forced group was not streamed");
+        std::memcpy(out, reinterpret_cast<const float*>(e->h_res) + row0, r * D * 4);
+        if (counters) {
+            *counters = sinkr_load_counters{};
+            counters->kv_floats_loaded = 2ull * L * D;  // attention.cpp:219
+        }
+    });
+}
+
 sinkr_status sinkr_routed_decode_step(sinkr_engine* e, const float* queries, size_t layer,
                                       const sinkr_routing_config* config,
                                       const sinkr_engine_options* options, float* outputs,

@@ -55,10 +55,20 @@ struct ProbeParams {
     uint32_t layer;
     uint32_t flags;
     uint32_t inline_seqs;  // 1: tau/len below; 0: B > kParamSeqs, read DevTables.tau/len
-    uint32_t pad;
+    uint32_t only_unit;    // 0: route; u + 1: unit u Active, every other unit Sink
+                           // (sinkr_group_attention: splitk_attention of one group)
     double tau[kParamSeqs];
     uint32_t len[kParamSeqs];
 };
+
+// ProbeParams.only_unit: the route decision replaced by "unit only_unit - 1
+// Active, every other unit Sink" (applied after the scores are formed)
+__device__ __forceinline__ void force_route(uint32_t only_unit, uint32_t u, bool& sink, bool& active) {
+    if (only_unit) {
+        active = u + 1 == only_unit;
+        sink = !active;
+    }
+}
 
 struct WorkState {
     unsigned int n_active;
@@ -238,7 +248,8 @@ __global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t, co
         const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
         bool sink = over && !(flags & kLayerExcluded);
         if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
-        const bool active = (flags & kObserveOnly) || !sink;
+        bool active = (flags & kObserveOnly) || !sink;
+        force_route(p.only_unit, u, sink, active);
         const uint32_t fl =
             (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
         t.group_scores[u] = S;

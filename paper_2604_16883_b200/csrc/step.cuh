@@ -410,7 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bool sink = over && !(flags & kLayerExcluded);
                 if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
                 active = (flags & kObserveOnly) || !sink;
-                if ((flags & kObserveOnly) || (flags & kLayerExcluded)) certain = true;
+                if ((flags & kObserveOnly) || (flags & kLayerExcluded) || p.only_unit) certain = true;
+                force_route(p.only_unit, u, sink, active);
                 L = s_len[seq];
                 if (!exact) act_prefix[u] = active ? 1u : 0u;  // estimate decisions, checked later
                 if (lead && exact) {  // (fast path: the consumers publish the record)
@@ -566,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const double tau = s_tau[u / t.Hkv];
                 certain &= fabsf(Sf - (float)tau) > (float)kRouteMargin ||
                            (flags & (kObserveOnly | kLayerExcluded)) != 0;
+                if (p.only_unit) certain = true;  // forced route: scores only for the record
                 s_score[kMaxEstHeads + (u - u_lo)] = (double)Sf;  // estimate, for the decision below
             }
             exact_later = __syncthreads_and(certain) != 0 && (h_hi - h_lo) <= (uint32_t)(kThreads - 32);
@@ -691,7 +693,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
             bool sink = over && !(flags & kLayerExcluded);
             if (degen) sink = false;  // router.cpp:114-117 fail-safe toward exact
-            const bool active = (flags & kObserveOnly) || !sink;
+            bool active = (flags & kObserveOnly) || !sink;
+            force_route(p.only_unit, u, sink, active);
             const uint32_t fl = (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
             t.route_flags[u] = fl;
             if (!exact_later) t.group_scores[u] = S;
@@ -1085,7 +1088,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool over = (flags & kSinkOnTie) ? (S >= tau) : (S > tau);
                 bool sink = over && !(flags & kLayerExcluded);
                 if (degen) sink = false;
-                const bool active = (flags & kObserveOnly) || !sink;
+                bool active = (flags & kObserveOnly) || !sink;
+                force_route(p.only_unit, u, sink, active);
                 t.group_scores[u] = S;
                 // the exact flags (the estimate pass cannot see a degenerate head
                 // when observe-only or an excluded layer made every decision certain)

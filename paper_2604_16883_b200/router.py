@@ -397,6 +397,33 @@ def routed_decode_step(queries, layer: int, cache: KvCache, config: RoutingConfi
     return _to_result(cache, out, groups, hs, ctr, batched=cache.B > 1 or q.ndim == 3)
 
 
+@dataclass
+class SplitkResult:
+    """SplitkResult (attention.hpp:71-74)."""
+    out: np.ndarray            # [r, D] f32
+    counters: LoadCounters
+
+
+def splitk_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
+                     num_splits: int, seq: int = 0) -> SplitkResult:
+    """splitk_attention (attention.cpp:204-235) of one cached group on the GPU:
+    the group's r query heads over all of its cached rows.  num_splits is
+    validated like split_ranges; the kernel picks its own split.  Replaces the
+    engine's last routing record."""
+    cc = cache.config()
+    r = cc.num_q_heads // cc.num_kv_heads
+    q = np.ascontiguousarray(group_queries, dtype=np.float32)
+    if q.size != r * cc.head_dim:
+        raise ValueError("query span size does not match heads x dim")
+    out = np.zeros((r, cc.head_dim), dtype=np.float32)
+    ctr = _abi.LoadCountersC()
+    check(lib().sinkr_group_attention(cache.handle, q.ctypes.data_as(C.c_void_p), C.c_size_t(seq),
+                                      C.c_size_t(layer), C.c_size_t(kv_head),
+                                      C.c_size_t(num_splits), out.ctypes.data_as(C.c_void_p),
+                                      C.byref(ctr)))
+    return SplitkResult(out=out, counters=LoadCounters(int(ctr.kv_floats_loaded)))
+
+
 def routed_decode_async(d_queries: int, layer: int, cache: KvCache, config: RoutingConfig,
                         options: Optional[EngineOptions] = None, d_outputs: int = 0) -> None:
     """Device-resident step: enqueue on the engine stream, no host sync."""

@@ -109,6 +109,13 @@ int main() {
         sc::calibrate(collect, std::vector<std::size_t>{1, 2, 3}, 0.6, 0.65);
     }));
 
+    // attention.hpp:76-85: splitk_attention of one cached group
+    const auto sk = sc::splitk_attention(cache, std::span<const float>(q.data(), 4 * D), 1, 0, 2);
+    REQUIRE(sk.out.size() == 4 * D && sk.counters.kv_floats_loaded == 2 * L * D);
+    REQUIRE(throws<std::invalid_argument>([&] {
+        sc::splitk_attention(cache, std::span<const float>(q.data(), 4 * D), 1, 0, 0);
+    }));
+
     // analysis.hpp: GPU BOS mass, oracle labels, PR curve
     const auto a0 = sc::attention_bos_mass(cache, q, 1);
     for (double a : a0) REQUIRE(a > 0.0 && a < 1.0);
