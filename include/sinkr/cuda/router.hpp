@@ -295,6 +295,23 @@ inline SplitkResult splitk_attention(const KvCache& cache, std::span<const float
     return res;
 }
 
+// dense_attention / online_attention (attention.cpp:42-73,144-157) of one
+// cached group: the same GPU group attention (block_size checked like
+// attend_chunk, attention.cpp:107).
+inline std::vector<float> dense_attention(const KvCache& cache, std::span<const float> group_q,
+                                          std::size_t layer, std::size_t kv_head,
+                                          std::size_t seq = 0) {
+    return splitk_attention(cache, group_q, layer, kv_head, 1, seq).out;
+}
+
+inline std::vector<float> online_attention(const KvCache& cache, std::span<const float> group_q,
+                                           std::size_t layer, std::size_t kv_head,
+                                           std::size_t block_size = kDefaultBlockSize,
+                                           std::size_t seq = 0) {
+    if (block_size == 0) throw std::invalid_argument("block_size must be positive");
+    return splitk_attention(cache, group_q, layer, kv_head, 1, seq).out;
+}
+
 // router.hpp:84-86 — one decode step for one layer (all B sequences).
 inline LayerStepResult routed_decode_step(std::span<const float> queries, std::size_t layer,
                                           const KvCache& cache, const RoutingConfig& config,

@@ -19,7 +19,9 @@ from .router import (  # noqa: F401
     ThresholdProfile,
     auto_num_splits,
     decode_rank_partial_async,
+    dense_attention,
     merge_rank_partials_async,
+    online_attention,
     rank_partial_floats,
     fetch_step_info,
     kDefaultBlockSize,

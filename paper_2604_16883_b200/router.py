@@ -424,6 +424,23 @@ def splitk_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
     return SplitkResult(out=out, counters=LoadCounters(int(ctr.kv_floats_loaded)))
 
 
+def dense_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
+                    seq: int = 0) -> np.ndarray:
+    """dense_attention (attention.cpp:42-73) of one cached group: [r, D] f32
+    (the GPU group attention; exact softmax to fp32 accumulation)."""
+    return splitk_attention(cache, group_queries, layer, kv_head, 1, seq).out
+
+
+def online_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
+                     block_size: int = kDefaultBlockSize, seq: int = 0) -> np.ndarray:
+    """online_attention (attention.cpp:144-157) of one cached group: [r, D] f32.
+    block_size is validated like attend_chunk (attention.cpp:107); the GPU
+    streams in its own 64-token stages."""
+    if block_size == 0:
+        raise ValueError("block_size must be positive")
+    return splitk_attention(cache, group_queries, layer, kv_head, 1, seq).out
+
+
 def routed_decode_async(d_queries: int, layer: int, cache: KvCache, config: RoutingConfig,
                         options: Optional[EngineOptions] = None, d_outputs: int = 0) -> None:
     """Device-resident step: enqueue on the engine stream, no host sync."""

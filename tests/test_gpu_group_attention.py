@@ -97,3 +97,20 @@ def test_group_attention_other_slots_empty(ref):
         assert _close(res.out, want)[0]
         with pytest.raises(ValueError, match="at least one token"):
             P.splitk_attention(cache, q, 0, 2, 1, seq=1)
+
+
+def test_dense_and_online_attention_vs_reference(ref):
+    rng = np.random.default_rng(11)
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, 5000)) as cache:
+        ks = {}
+        for g in range(8):
+            k = round_bf16(rng.standard_normal((4321, 128)).astype(np.float32) * 2.0)
+            v = round_bf16(rng.standard_normal((4321, 128)).astype(np.float32))
+            cache.append(0, g, k, v)
+            ks[g] = (k, v)
+        q = (rng.standard_normal((4, 128)) * 1.5).astype(np.float32)
+        k, v = ks[5]
+        assert _close(P.dense_attention(cache, q, 0, 5), ref.dense_attention(q, k, v))[0]
+        assert _close(P.online_attention(cache, q, 0, 5, 96), ref.online_attention(q, k, v, 96))[0]
+        with pytest.raises(ValueError, match="block_size must be positive"):
+            P.online_attention(cache, q, 0, 5, 0)
