@@ -19,6 +19,8 @@ for B, L in ((1, 4096), (4, 3000), (40, 600)):
         for _ in range(2):
             res = P.routed_decode_step(q[0] if B == 1 else q, 0, cache, cfg)
         assert np.isfinite(res.outputs).all()
+        g = P.splitk_attention(cache, q.reshape(B, 32, 128)[B - 1, 4:8], 0, 1, 1, seq=B - 1)
+        assert np.isfinite(g.out).all()
         a0 = A.attention_bos_mass(cache, q, 0)
         w = A.attention_weights(cache, q[0, :4], 0, 1)
         assert np.isfinite(a0).all() and np.isfinite(w).all()
