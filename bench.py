@@ -483,8 +483,16 @@ def run_ours(args, world, rank, local_rank):
     torch.cuda.set_device(dev)
     dist = None
     if world > 1 or args.force_sharded:
+        import socket
+
         import torch.distributed as dist
 
+        if "RANK" not in os.environ:  # --force-sharded run without a launcher: world of one
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
+                              MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     L = args.length
     D = SHAPE["head_dim"]

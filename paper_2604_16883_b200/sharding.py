@@ -270,7 +270,9 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
                      "peak": peak_gbs, "unit": "GB/s",
                      "frac": round(per_gpu_gbs / peak_gbs, 4) if peak_gbs else None,
                      "traffic": None,
-                     "kernel": "step_kernel<128> rank partial (per GPU) + combine_kernel",
+                     "kernel": ("step_kernel<128> with the rank merge fused over peer memory (mode 3)"
+                                if pm is not None else
+                                "step_kernel<128> rank partial (per GPU) + NCCL all-gather + combine_kernel"),
                      "peak_source": peak_src},
         "e2e": {"value": round(e2e_us, 2), "unit": "us/step",
                 "h2d_bytes_per_step": h2d_bytes,
