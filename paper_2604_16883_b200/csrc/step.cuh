@@ -46,7 +46,8 @@ struct StepState {
     unsigned int error;
     unsigned int route_done;  // CTAs that published their units' decisions (distributed routing)
     unsigned int peer_epoch;  // mode 3: steps completed (advanced by the last CTA at exit)
-    unsigned int pad[2];
+    unsigned int peer_base;   // mode 3: arrivals counted on this rank before this step
+    unsigned int pad;
 };
 
 struct StepTables {
@@ -196,6 +197,12 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
             }
             P[2 * r + h * D + d] = acc;
         }
+        // one arrival per task on every rank, as soon as its slice is stored:
+        // the warp's stores, then a release add per rank (system scope)
+        __syncwarp();
+        if (lane == 0)
+            for (uint32_t q = 0; q < t.world; ++q)
+                asm volatile("red.release.sys.global.add.u32 [%0], 1;" :: "l"(t.peer_arrive[q]) : "memory");
     }
 }
 
@@ -821,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // step number lives on the device (advanced by the last CTA at exit, after
     // every CTA has read it), so the graph needs no per-step parameter patch.
     const uint32_t epoch = t.mode == 3 ? ld_volatile(&t.ss->peer_epoch) : 0u;
+    const uint32_t peer_base = t.mode == 3 ? ld_volatile(&t.ss->peer_base) : 0u;
     const size_t xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
@@ -1375,20 +1383,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) {
         // gpu-scope acq_rel count: releases this CTA's writes (ordered before
         // tid 0 by the barrier) and, for the last CTA, acquires everyone's
-        if (t.mode == 3) __threadfence_system();  // peer stores reach system scope first
         misc[kMiscLast] = (ptx::atom_add_acq_rel(&t.ss->exit_count, 1u) == G - 1) ? 1u : 0u;
     }
     __syncthreads();
-    if (t.mode == 3) {
-        // every CTA's partial stores are fenced (system scope) and counted: the
-        // last CTA tells every rank (NVLink atomics); then ALL CTAs wait for
-        // every rank's partials of this step and merge a share of the outputs
-        if (misc[kMiscLast] && tid < t.world) {
-            unsigned int* ctr = t.peer_arrive[tid];
-            asm volatile("red.release.sys.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
-        }
+    // mode 3: every merge task signalled every rank once (warp_merge), so this
+    // step's partials are all here when the arrivals reach base + world *
+    // tasks (a rank a step ahead only adds arrivals that causally follow every
+    // partial of this step); the CTAs that own output elements wait, then
+    // merge them (the others leave at once)
+    const uint32_t peer_want = peer_base + t.world * (nact * r * (D / 32));
+    if (t.mode == 3 && bid * kThreads < nact * r * D) {
         if (tid == 0) {
-            const unsigned int want = (epoch + 1u) * t.world;
+            const unsigned int want = peer_want;
             const unsigned long long t_spin = globaltimer();
             for (;;) {
                 unsigned int v;
@@ -1447,7 +1453,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             t.ss->merge_next = 0;
             t.ss->exit_count = 0;
             t.ss->route_done = 0;
-            if (t.mode == 3) t.ss->peer_epoch = epoch + 1u;
+            if (t.mode == 3) {
+                t.ss->peer_epoch = epoch + 1u;
+                t.ss->peer_base = peer_want;
+            }
         }
     }
 }
