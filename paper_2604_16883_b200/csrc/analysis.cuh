@@ -42,7 +42,7 @@ constexpr int kBosThreads = 32 * (1 + kBosCWarps);
 constexpr int kBosTok = kWarpTok * kBosCWarps;  // tokens per stage (2 per SMSP in flight)
 constexpr int kBosBoxes = kBosTok / kStageTok;  // 64-row TMA boxes per stage and half
 constexpr int kBosHeads = 8;                   // heads per unit (mma rows 0-7)
-static_assert(kBosCWarps >= kMaxR, "the unit merge takes one consumer warp per head");
+static_assert(kBosHeads >= kMaxR, "one stream pass covers a GQA group (mma rows 0-7)");
 
 struct BosArgs {
     const uint32_t* pre;      // [n_units + 1] token prefix over the launch's units
@@ -71,7 +71,7 @@ struct BosCfg {
     static constexpr int kStages = (192 * 1024) / kStageBytes > 16 ? 16 : (192 * 1024) / kStageBytes;
     static constexpr int kNK = D / 16;
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStages * (16 + 16) +
-                                      kBosCWarps * kBosHeads * 2 * 4 + 16;  // + sm_slot[4]
+                                      kBosCWarps * kBosHeads * 2 * 4 + 16;  // + the flush's slot index
 };
 
 // byte offset of (token, 16-byte chunk) in a K stage: swz<D> with kBosTok rows per half
