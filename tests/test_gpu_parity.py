@@ -412,3 +412,51 @@ def test_three_kernel_pipeline_parity(oracle_libs, monkeypatch, hq, hkv, D, L, p
     meets the same bar as the fused step kernel."""
     monkeypatch.setenv("SINKR_FUSED", "0")
     test_planted_parity(oracle_libs, hq, hkv, D, L, p)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_randomized_batched_parity(oracle_libs, seed):
+    """Batched steps across the kernel's batched regimes -- distributed routing
+    (U > 32), unit-affine and flat global-token scheduling (Active units above
+    the SM count), queue-mode and last-flusher merges -- with a different
+    length per sequence and a length-dependent cubic tau(L): bit-exact routing
+    and skipped-block record per sequence, outputs within tolerance."""
+    _, orc = oracle_libs
+    rng = np.random.default_rng(5000 + seed)
+    D = int(rng.choice([64, 128]))
+    r = int(rng.choice([1, 2, 4, 8]))
+    hkv = int(rng.choice([4, 8]))
+    B = int(rng.choice([5, 12, 24, 40]))
+    hq = hkv * r
+    cap = 2600
+    lens = rng.integers(1, cap + 1, size=B)
+    cc = P.CacheConfig(1, hq, hkv, D, cap, B)
+    # tau rises with L over the sampled range, so sequences route differently
+    prof = P.ThresholdProfile(coeffs=(0.0, 0.0, 0.3, 0.2), length_normalizer=float(cap),
+                              clamp_lo=0.0, clamp_hi=1.0)
+    cfg = P.RoutingConfig(profile=prof, excluded_layers=(), sink_on_tie=bool(seed % 2))
+    q = np.zeros((B, hq, D), np.float32)
+    kv = []
+    with P.KvCache(cc) as cache:
+        for b in range(B):
+            k = (rng.standard_normal((hkv, lens[b], D)) * rng.uniform(0.5, 2.0)).astype(np.float32)
+            v = rng.standard_normal((hkv, lens[b], D)).astype(np.float32)
+            for g in range(hkv):
+                cache.append(0, g, k[g], v[g], seq=b)
+                kh = k[g, 0].astype(np.float64) / np.linalg.norm(k[g, 0])
+                for i in range(r):
+                    n = rng.standard_normal(D)
+                    n -= (n @ kh) * kh
+                    n /= np.linalg.norm(n)
+                    c = rng.uniform(-0.3, 0.95)
+                    q[b, g * r + i] = (np.sqrt(D) * (c * kh + np.sqrt(1 - c * c) * n)).astype(np.float32)
+            kv.append((k, v))
+        res = P.routed_decode_step(q, 0, cache, cfg)
+        for b in range(B):
+            kb = np.stack([cache.historical(0, g, 0, int(lens[b]), seq=b)[0] for g in range(hkv)])
+            vb = np.stack([cache.historical(0, g, 0, int(lens[b]), seq=b)[1] for g in range(hkv)])
+            k0 = kb[:, 0, :].copy()
+            k0n = np.array([orc.anchor_norm(k0[g]) for g in range(hkv)], dtype=np.float32)
+            ref = orc.routed_decode_step(kb, vb, k0, k0n, q[b], 0, oracle_profile(prof), excluded=(),
+                                         sink_on_tie=cfg.sink_on_tie, observe_only=False, threads=8)
+            assert_parity(res.outputs[b], ref, r, D, res.groups[b * hkv:(b + 1) * hkv])
