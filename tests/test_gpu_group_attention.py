@@ -84,10 +84,11 @@ def test_group_attention_errors_and_next_step(ref):
         assert after.counters.kv_floats_loaded == before.counters.kv_floats_loaded
 
 
-def test_group_attention_other_slots_empty(ref):
+@pytest.mark.parametrize("B", [2, 8])  # 16 units (lean routing) / 64 units (distributed)
+def test_group_attention_other_slots_empty(ref, B):
     """Only (seq 1, layer 0, head 3) holds rows: the rest of the cache is empty."""
     rng = np.random.default_rng(5)
-    with P.KvCache(P.CacheConfig(1, 32, 8, 128, 2048, 2)) as cache:
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, 2048, B)) as cache:
         k = round_bf16(rng.standard_normal((777, 128)).astype(np.float32))
         v = round_bf16(rng.standard_normal((777, 128)).astype(np.float32))
         cache.append(0, 3, k, v, seq=1)
