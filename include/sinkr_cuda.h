@@ -251,6 +251,13 @@ sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches,
 /* Bytes one sinkr_routed_decode_step call copies host->device (queries +
  * step parameters) and device->host (outputs + routing record). */
 sinkr_status sinkr_step_io_bytes(sinkr_engine* e, size_t* h2d, size_t* d2h);
+/* The engine's pinned step buffers: queries [B][H_q][D] f32 (inside the
+ * pinned input block the step uploads) and outputs [B][H_q][D] f32 (inside the
+ * mapped result block the step kernel writes).  A caller that fills *queries
+ * and passes it as sinkr_routed_decode_batch's queries (and *outputs as its
+ * outputs) skips both host copies; valid for the engine's lifetime, and only
+ * between blocking calls. */
+sinkr_status sinkr_step_io_buffers(sinkr_engine* e, float** queries, const float** outputs);
 /* Enables per-kernel event timing on the async path (costs two event records). */
 sinkr_status sinkr_set_timing(sinkr_engine* e, int enabled);
 /* Number of SMs / persistent CTAs used by the decode kernel. */

@@ -98,7 +98,7 @@ EXPORTS = (
     "sinkr_routed_decode_batch", "sinkr_routed_decode_async", "sinkr_fetch_step_info",
     "sinkr_rank_partial_floats", "sinkr_decode_rank_partial_async",
     "sinkr_merge_rank_partials_async", "sinkr_last_step_stats", "sinkr_set_timing",
-    "sinkr_decode_grid", "sinkr_step_io_bytes", "sinkr_engine_config",
+    "sinkr_decode_grid", "sinkr_step_io_bytes", "sinkr_step_io_buffers", "sinkr_engine_config",
     # calibration (f1)
     "sinkr_profile_default", "sinkr_profile_constant", "sinkr_sweep", "sinkr_skip_ratio_at",
     "sinkr_solve_threshold", "sinkr_fit_cubic", "sinkr_calibrate", "sinkr_save_profile",
@@ -166,6 +166,7 @@ def lib():
             "sinkr_load_snapshot_into": [vp, sz, C.c_char_p],
             "sinkr_kv_append_device_f32": [vp, sz, sz, sz, vp, vp, sz],
             "sinkr_engine_config": [vp, vp],
+            "sinkr_step_io_buffers": [vp, vp, vp],
             "sinkr_attention_bos_mass": [vp, vp, sz, vp],
             "sinkr_attention_weights": [vp, vp, sz, sz, sz, vp],
             "sinkr_attention_last_kernel_seconds": [vp, vp],

@@ -1152,8 +1152,10 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
         stage_params(e, layer, config, options, true);  // validates before touching q
         const size_t qbytes = e->B * e->cfg.num_q_heads * e->D * 4;
         // params were written into h_in by stage_params; append the queries
-        // and upload the whole input block in one H2D copy.
-        std::memcpy(e->h_in + e->off_q, queries, qbytes);
+        // (unless the caller filled the pinned query area itself) and upload
+        // the whole input block in one H2D copy.
+        if (queries != reinterpret_cast<const float*>(e->h_in + e->off_q))
+            std::memcpy(e->h_in + e->off_q, queries, qbytes);
         if (e->fused && !e->timing && io_mode() != 0) {
             run_io_graph(e);  // H2D + step kernel, results land in mapped h_res
         } else {
@@ -1169,7 +1171,7 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
             CK(cudaMemcpy(&ws, e->d_ws, sizeof(ws), cudaMemcpyDeviceToHost));
             if (ws.error) fail(SINKR_RUNTIME_ERROR, "decode partial-slot overflow");
         }
-        if (outputs) std::memcpy(outputs, e->h_res, qbytes);
+        if (outputs && outputs != reinterpret_cast<float*>(e->h_res)) std::memcpy(outputs, e->h_res, qbytes);
         fill_info(e, layer, config, groups, head_scores, counters, options);
     });
 }
@@ -1591,6 +1593,14 @@ sinkr_status sinkr_last_step_stats(sinkr_engine* e, uint32_t* kernel_launches, f
             if (e->timing || e->step_events)
                 CK(cudaEventElapsedTime(step_ms, e->ev[0], e->ev[3]));
         }
+    });
+}
+
+sinkr_status sinkr_step_io_buffers(sinkr_engine* e, float** queries, const float** outputs) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        if (queries) *queries = reinterpret_cast<float*>(e->h_in + e->off_q);
+        if (outputs) *outputs = reinterpret_cast<const float*>(e->h_res);
     });
 }
 

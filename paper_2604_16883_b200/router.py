@@ -515,10 +515,20 @@ class StepRunner:
     LayerStepResult of the last call on demand."""
 
     def __init__(self, cache: KvCache, config: RoutingConfig, options: Optional[EngineOptions] = None,
-                 layer: int = 0):
+                 layer: int = 0, pinned_io: bool = False):
         self.cache = cache
         self.layer = layer
         self.out, self.groups, self.hs, self.ctr = _step_buffers(cache)
+        self.queries = None
+        if pinned_io:
+            # the engine's own pinned buffers (sinkr_step_io_buffers): fill
+            # `self.queries`, call with no argument, read the returned outputs;
+            # no host copy on either side
+            qp, op = C.c_void_p(), C.c_void_p()
+            check(lib().sinkr_step_io_buffers(cache.handle, C.byref(qp), C.byref(op)))
+            shape, n = self.out.shape, self.out.size
+            self.queries = np.ctypeslib.as_array((C.c_float * n).from_address(qp.value)).reshape(shape)
+            self.out = np.ctypeslib.as_array((C.c_float * n).from_address(op.value)).reshape(shape)
         self._cfg, self._keep = config._c()
         self._opt = (options or EngineOptions())._c()
         L = lib()
@@ -531,7 +541,11 @@ class StepRunner:
                       C.addressof(self.ctr))
         self._qsize = self.out.size
 
-    def __call__(self, queries: np.ndarray) -> np.ndarray:
+    def __call__(self, queries: Optional[np.ndarray] = None) -> np.ndarray:
+        if queries is None:
+            if self.queries is None:
+                raise ValueError("no queries: pass them, or build the runner with pinned_io=True")
+            queries = self.queries
         if queries.dtype != np.float32 or not queries.flags.c_contiguous or \
                 queries.size != self._qsize:
             queries = np.ascontiguousarray(queries, dtype=np.float32)

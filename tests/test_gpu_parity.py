@@ -462,3 +462,23 @@ def test_randomized_batched_parity(oracle_libs, seed):
             ref = orc.routed_decode_step(kb, vb, k0, k0n, q[b], 0, oracle_profile(prof), excluded=(),
                                          sink_on_tie=cfg.sink_on_tie, observe_only=False, threads=8)
             assert_parity(res.outputs[b], ref, r, D, res.groups[b * hkv:(b + 1) * hkv])
+
+
+def test_step_runner_pinned_io_matches(oracle_libs):
+    """StepRunner over the engine's pinned step buffers (sinkr_step_io_buffers,
+    no host copies) returns what the copying form returns."""
+    spec = WorkloadSpec(length=9000, sink_fraction=0.5, seed=21)
+    q = spec.queries()[0]
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    with make_cache(spec) as cache:
+        plain = P.StepRunner(cache, cfg)
+        want = plain(q).copy()
+        info = plain.result()
+        pin = P.StepRunner(cache, cfg, pinned_io=True)
+        pin.queries[...] = q.reshape(pin.queries.shape)
+        for _ in range(3):
+            got = pin()
+            assert np.abs(got - want).max() <= 1e-6
+        res = pin.result()
+        assert [g.decision.sink for g in res.groups] == [g.decision.sink for g in info.groups]
+        assert res.counters.kv_floats_loaded == info.counters.kv_floats_loaded
