@@ -4,6 +4,8 @@ decisions, unit-affine / global-token scheduling, queue / per-unit merge,
 modes 0 / 1 / 3), interleaved, each compared with a fresh single step and with
 the previous replay of the same configuration.  Counters and locks must be
 restored by every step; no step may report a kernel error."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -48,7 +50,7 @@ def test_interleaved_paths_stay_consistent():
                 refs[(name, k)] = (outs[name].clone(), P.fetch_step_info(c))
             caches[name]._cfgs = cfgs_local
         (pm,) = sharding.peer_merge_in_process(P, [caches["lean"]])
-        for it in range(60):
+        for it in range(int(os.environ.get("SINKR_STRESS_STEPS", 60))):
             name = list(specs)[rng.integers(len(specs))]
             c = caches[name]
             k = list(c._cfgs)[rng.integers(3)]
