@@ -1412,6 +1412,20 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     a.n_units = n_units;
     a.G = G;
     a.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
+    // from here the counter sets are in flight: if anything fails before the
+    // finish kernel has zeroed the next set, the scratch is dropped (the next
+    // call reallocates and zeroes it)
+    struct DropScratchOnError {
+        sinkr_engine* e;
+        bool armed = true;
+        ~DropScratchOnError() {
+            if (!armed) return;
+            cudaStreamSynchronize(e->stream);
+            cudaFree(e->d_bos);
+            e->d_bos = nullptr;
+            e->bos_bytes = 0;
+        }
+    } guard_scratch{e};
     CK(cudaEventRecord(e->ev_bos[0], e->stream));
     static_assert(dev::kBosHeads >= dev::kMaxR, "one stream pass covers a GQA group");
     launch_bos(e, a);
@@ -1428,6 +1442,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     if (weights)
         CK(cudaMemcpyAsync(weights, scratch + off_w, wbytes, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
+    guard_scratch.armed = false;
     std::memcpy(alpha0, e->h_bos + h_a0, (size_t)nh * 8);
     CK(cudaEventElapsedTime(&e->bos_ms, e->ev_bos[0], e->ev_bos[1]));
 }
