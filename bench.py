@@ -418,7 +418,7 @@ def next_rows(P, torch, args, spec_cls, peak):
         "context": spec.length, "gpu_us_per_sample": round(gpu_us, 1),
         "reference_observe_only_step_us": round(statistics.median(ts) * 1e6, 1),
         "reference_threads": threads,
-        "note": "collect_scores (blocking C-ABI call: H2D q, probe kernel, D2H scores) vs the "
+        "note": "collect_scores (blocking C-ABI call: H2D q, probe kernel writing the scores into mapped host memory) vs the "
                 "reference's observe-only routed_decode_step, which its calibration runs per sample"}
     # f2: snapshot replay, reference-written snapshot of the same cache
     with tempfile.TemporaryDirectory() as d:

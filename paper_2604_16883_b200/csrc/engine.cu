@@ -1302,7 +1302,16 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
         std::memcpy(e->h_in + e->off_q, queries, NH * e->D * 4);
         CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
         CK(cudaEventRecord(e->ev_in, e->stream));
-        const dev::DevTables t = e->tables(reinterpret_cast<const float*>(e->d_in + e->off_q));
+        dev::DevTables t = e->tables(reinterpret_cast<const float*>(e->d_in + e->off_q));
+        // scores and flags straight into the mapped result block (as the step
+        // path does): no D2H copy in the call
+        const bool zc = io_mode() == 1 && e->h_res_dev;
+        if (zc) {
+            t.head_scores = reinterpret_cast<double*>(e->h_res_dev + e->off_hs);
+            t.group_scores = reinterpret_cast<double*>(e->h_res_dev + e->off_gs);
+            t.unit_flags = reinterpret_cast<uint32_t*>(e->h_res_dev + e->off_fl);
+            t.tokens = reinterpret_cast<unsigned long long*>(e->h_res_dev + e->off_tok);
+        }
         switch (e->D) {
             case 32: dev::probe_kernel<32><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
             case 64: dev::probe_kernel<64><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
@@ -1310,8 +1319,9 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
         }
         CK(cudaGetLastError());
         // head scores, group scores and flags are contiguous in the result block
-        CK(cudaMemcpyAsync(e->h_res + e->off_hs, e->d_res + e->off_hs, e->off_status - e->off_hs,
-                           cudaMemcpyDeviceToHost, e->stream));
+        if (!zc)
+            CK(cudaMemcpyAsync(e->h_res + e->off_hs, e->d_res + e->off_hs, e->off_status - e->off_hs,
+                               cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));
         const auto* hs = reinterpret_cast<const double*>(e->h_res + e->off_hs);
         const auto* gs = reinterpret_cast<const double*>(e->h_res + e->off_gs);
