@@ -131,7 +131,8 @@ struct sinkr_engine {
     uint32_t* d_route_flags = nullptr;  // distributed routing decisions [U]
     uint8_t* d_bos = nullptr;            // analysis scratch (run_bos), grown on demand
     size_t bos_bytes = 0;
-    uint8_t* h_bos = nullptr;            // pinned staging for run_bos (prefix up, alpha0 down)
+    uint8_t* h_bos = nullptr;            // pinned + mapped staging for run_bos (prefix up, alpha0 down)
+    uint8_t* h_bos_dev = nullptr;        // device address of h_bos
     cudaEvent_t ev_bos[2] = {};          // around run_bos's kernels (device time)
     uint32_t bos_parity = 0;             // which counter set the next run_bos uses
     float bos_ms = -1.f;
@@ -1365,13 +1366,12 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     const uint32_t G = std::max<uint32_t>(
         1, std::min<uint32_t>((uint32_t)e->num_sms, (T + dev::kBosTok - 1) / dev::kBosTok));
     // scratch: ctr[2][1+U] (zeroed at allocation; each call's finish zeroes the other set) | pre[n+1] |
-    //          part[n][G][r][2] | z0[U*r] | stats[U*r][2] | alpha0[U*r] f64 | logits | weights
+    //          part[n][G][r][2] | z0[U*r] | stats[U*r][2] | logits | weights (alpha0: mapped h_bos)
     const size_t off_pre = align_up(2 * (1 + U) * 4, 256);
     const size_t off_part = align_up(off_pre + (n_units + 1) * 4, 256);
     const size_t off_z0 = align_up(off_part + (size_t)n_units * G * r * 2 * 4, 256);
     const size_t off_st = align_up(off_z0 + U * r * 4, 256);
-    const size_t off_a0 = align_up(off_st + U * r * 2 * 4, 256);
-    const size_t off_z = align_up(off_a0 + U * r * 8, 256);
+    const size_t off_z = align_up(off_st + U * r * 2 * 4, 256);
     const size_t wbytes = weights ? r * (size_t)T * 4 : 0;
     const size_t off_w = align_up(off_z + wbytes, 256);
     const size_t need = off_w + wbytes;
@@ -1387,13 +1387,16 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     }
     uint8_t* scratch = e->d_bos;
     const uint32_t nh = n_units * (uint32_t)r;
-    const size_t h_a0 = align_up((n_units + 1) * 4, 64), h_need = h_a0 + (size_t)nh * 8;
+    // pinned + mapped: prefix up by copy, alpha0 [U*r] written by the finish
+    // kernel straight into host memory
+    const size_t h_a0 = align_up((n_units + 1) * 4, 64), h_need = h_a0 + U * r * 8;
     if (e->h_bos_bytes < h_need) {
         CK(cudaStreamSynchronize(e->stream));
         if (e->h_bos) cudaFreeHost(e->h_bos);
         e->h_bos = nullptr;
         e->h_bos_bytes = 0;
-        CK(cudaMallocHost(&e->h_bos, h_need));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&e->h_bos), h_need, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_bos_dev), e->h_bos, 0));
         e->h_bos_bytes = h_need;
     }
     CK(cudaEventSynchronize(e->ev_in));  // the input block is free
@@ -1412,7 +1415,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     e->bos_parity ^= 1u;
     a.z0 = reinterpret_cast<float*>(scratch + off_z0);
     a.stats = reinterpret_cast<float*>(scratch + off_st);
-    a.alpha0 = reinterpret_cast<double*>(scratch + off_a0);
+    a.alpha0 = reinterpret_cast<double*>(e->h_bos_dev + h_a0);
     a.zout = weights ? reinterpret_cast<float*>(scratch + off_z) : nullptr;
     a.weights = reinterpret_cast<float*>(scratch + off_w);
     a.r = (uint32_t)r;
@@ -1447,13 +1450,11 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(e->ev_bos[1], e->stream));
-    CK(cudaMemcpyAsync(e->h_bos + h_a0, scratch + off_a0 + (size_t)u_first * r * 8, (size_t)nh * 8,
-                       cudaMemcpyDeviceToHost, e->stream));
     if (weights)
         CK(cudaMemcpyAsync(weights, scratch + off_w, wbytes, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     guard_scratch.armed = false;
-    std::memcpy(alpha0, e->h_bos + h_a0, (size_t)nh * 8);
+    std::memcpy(alpha0, e->h_bos + h_a0 + (size_t)u_first * r * 8, (size_t)nh * 8);
     CK(cudaEventElapsedTime(&e->bos_ms, e->ev_bos[0], e->ev_bos[1]));
 }
 
