@@ -79,16 +79,51 @@ def peak_hbm():
 # ----------------------------------------------------------------------------
 # clocks during the timed region
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML
+    thread in this process (~every 0.2 ms, so a few-ms region still gets tens
+    of samples); `nvidia-smi -lms 50` when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.sm, self.mx, self.reasons = [], None, set()
+        self._stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx))
+            P_, h = self.nvml
+            self.mx = float(P_.nvmlDeviceGetMaxClockInfo(h, P_.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": P_.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": P_.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": P_.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": P_.nvmlClocksEventReasonSwPowerCap}
+
+            def run():
+                while not self._stop.is_set():
+                    self.sm.append(float(P_.nvmlDeviceGetClockInfo(h, P_.NVML_CLOCK_SM)))
+                    r = P_.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for n, bit in bits.items():
+                        if r & bit:
+                            self.reasons.add(n)
+                    time.sleep(0.0002)
+
+            self.t = threading.Thread(target=run, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
@@ -106,6 +141,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nvml:
+            self._stop.set()
+            self.t.join(timeout=2)
         if self.proc:
             time.sleep(0.06)
             self.proc.terminate()
@@ -115,8 +153,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = list(self.sm), self.mx, set(self.reasons)
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
@@ -126,13 +163,13 @@ class ClockSampler:
                 mx = float(f[1])
             except ValueError:
                 continue
-            for n, v in zip(names, f[4:8]):
+            for n, v in zip(self.NAMES, f[4:8]):
                 if v.lower() == "active":
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------
