@@ -21,6 +21,9 @@ for B, L in ((1, 4096), (4, 3000), (40, 600)):
         assert np.isfinite(res.outputs).all()
         g = P.splitk_attention(cache, q.reshape(B, 32, 128)[B - 1, 4:8], 0, 1, 1, seq=B - 1)
         assert np.isfinite(g.out).all()
+        from paper_2604_16883_b200 import calibration as cal
+        hs, gs, _ = cal.collect_scores(cache, q, 0)
+        assert np.isfinite(hs).all() and np.isfinite(gs).all()
         a0 = A.attention_bos_mass(cache, q, 0)
         w = A.attention_weights(cache, q[0, :4], 0, 1)
         assert np.isfinite(a0).all() and np.isfinite(w).all()
