@@ -1301,8 +1301,6 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
         stage_params(e, layer, config ? config : &none, nullptr, true);
         const size_t NH = e->B * e->cfg.num_q_heads;
         std::memcpy(e->h_in + e->off_q, queries, NH * e->D * 4);
-        CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
-        CK(cudaEventRecord(e->ev_in, e->stream));
         dev::DevTables t = e->tables(reinterpret_cast<const float*>(e->d_in + e->off_q));
         // scores and flags straight into the mapped result block (as the step
         // path does): no D2H copy in the call
@@ -1313,12 +1311,62 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
             t.unit_flags = reinterpret_cast<uint32_t*>(e->h_res_dev + e->off_fl);
             t.tokens = reinterpret_cast<unsigned long long*>(e->h_res_dev + e->off_tok);
         }
-        switch (e->D) {
-            case 32: dev::probe_kernel<32><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
-            case 64: dev::probe_kernel<64><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
-            default: dev::probe_kernel<128><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+        auto enqueue = [&] {
+            CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
+            switch (e->D) {
+                case 32: dev::probe_kernel<32><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+                case 64: dev::probe_kernel<64><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+                default: dev::probe_kernel<128><<<e->probe_grid, dev::kProbeThreads, probe_smem(e), e->stream>>>(t, e->pp); break;
+            }
+            CK(cudaGetLastError());
+        };
+        if (zc) {
+            // one graph (upload + probe), captured once per engine; the probe's
+            // by-value parameters are patched when they change
+            const auto key = std::make_tuple((const void*)e->h_in, (void*)e->h_res, 4);
+            auto it = e->graphs.find(key);
+            if (it == e->graphs.end()) {
+                sinkr_engine::GraphEntry ge;
+                CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    enqueue();
+                } catch (...) {
+                    cudaStreamEndCapture(e->stream, &ge.graph);
+                    if (ge.graph) cudaGraphDestroy(ge.graph);
+                    throw;
+                }
+                CK(cudaStreamEndCapture(e->stream, &ge.graph));
+                CK(cudaGraphInstantiate(&ge.exec, ge.graph, 0));
+                size_t n = 0;
+                CK(cudaGraphGetNodes(ge.graph, nullptr, &n));
+                std::vector<cudaGraphNode_t> nodes(n);
+                CK(cudaGraphGetNodes(ge.graph, nodes.data(), &n));
+                for (auto nd : nodes) {
+                    cudaGraphNodeType ty;
+                    CK(cudaGraphNodeGetType(nd, &ty));
+                    if (ty != cudaGraphNodeTypeKernel) continue;
+                    CK(cudaGraphKernelNodeGetParams(nd, &ge.probe_kp));
+                    ge.probe = nd;
+                }
+                if (!ge.probe) fail(SINKR_CUDA_ERROR, "probe node not found in the captured graph");
+                ge.probe_t = t;
+                ge.pp = e->pp;
+                it = e->graphs.emplace(key, ge).first;
+            }
+            auto& ge = it->second;
+            if (std::memcmp(&ge.pp, &e->pp, sizeof(e->pp)) != 0) {
+                ge.pp = e->pp;
+                void* args[2] = {&ge.probe_t, &ge.pp};
+                cudaKernelNodeParams kp = ge.probe_kp;
+                kp.kernelParams = args;
+                kp.extra = nullptr;
+                CK(cudaGraphExecKernelNodeSetParams(ge.exec, ge.probe, &kp));
+            }
+            CK(cudaGraphLaunch(ge.exec, e->stream));
+        } else {
+            enqueue();
         }
-        CK(cudaGetLastError());
+        CK(cudaEventRecord(e->ev_in, e->stream));
         // head scores, group scores and flags are contiguous in the result block
         if (!zc)
             CK(cudaMemcpyAsync(e->h_res + e->off_hs, e->d_res + e->off_hs, e->off_status - e->off_hs,
