@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -134,6 +135,13 @@ struct sinkr_engine {
     uint8_t* h_bos = nullptr;            // pinned + mapped staging for run_bos (prefix up, alpha0 down)
     uint8_t* h_bos_dev = nullptr;        // device address of h_bos
     cudaEvent_t ev_bos[2] = {};          // around run_bos's kernels (device time)
+    // run_bos as captured graphs, keyed by (layer, u_first, n_units, G, weights,
+    // parity); dropped when the scratch or the pinned staging is reallocated
+    std::map<std::array<uint64_t, 6>, cudaGraphExec_t> bos_graphs;
+    void drop_bos_graphs() {
+        for (auto& kv : bos_graphs) cudaGraphExecDestroy(kv.second);
+        bos_graphs.clear();
+    }
     uint32_t bos_parity = 0;             // which counter set the next run_bos uses
     float bos_ms = -1.f;
     size_t h_bos_bytes = 0;
@@ -847,6 +855,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
         cudaGraphExecDestroy(kv.second.exec);
         cudaGraphDestroy(kv.second.graph);
     }
+    e->drop_bos_graphs();
     for (auto& ev : e->ev)
         if (ev) cudaEventDestroy(ev);
     if (e->ev_in) cudaEventDestroy(e->ev_in);
@@ -1425,6 +1434,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     const size_t need = off_w + wbytes;
     if (e->bos_bytes < need) {
         CK(cudaStreamSynchronize(e->stream));
+        e->drop_bos_graphs();
         cudaFree(e->d_bos);
         e->d_bos = nullptr;
         e->bos_bytes = 0;
@@ -1440,6 +1450,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     const size_t h_a0 = align_up((n_units + 1) * 4, 64), h_need = h_a0 + U * r * 8;
     if (e->h_bos_bytes < h_need) {
         CK(cudaStreamSynchronize(e->stream));
+        e->drop_bos_graphs();
         if (e->h_bos) cudaFreeHost(e->h_bos);
         e->h_bos = nullptr;
         e->h_bos_bytes = 0;
@@ -1450,9 +1461,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
     CK(cudaEventSynchronize(e->ev_in));  // the input block is free
     std::memcpy(e->h_in + e->off_q + q_offset * 4, queries, q_floats * 4);
     std::memcpy(e->h_bos, pre.data(), (n_units + 1) * 4);
-    CK(cudaMemcpyAsync(e->d_in + e->off_q + q_offset * 4, e->h_in + e->off_q + q_offset * 4,
-                       q_floats * 4, cudaMemcpyHostToDevice, e->stream));
-    CK(cudaMemcpyAsync(scratch + off_pre, e->h_bos, (n_units + 1) * 4, cudaMemcpyHostToDevice, e->stream));
+    const uint32_t parity = e->bos_parity;
     dev::BosArgs a{};
     a.pre = reinterpret_cast<const uint32_t*>(scratch + off_pre);
     a.q = reinterpret_cast<const float*>(e->d_in + e->off_q);
@@ -1482,22 +1491,51 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
         ~DropScratchOnError() {
             if (!armed) return;
             cudaStreamSynchronize(e->stream);
+            e->drop_bos_graphs();
             cudaFree(e->d_bos);
             e->d_bos = nullptr;
             e->bos_bytes = 0;
         }
     } guard_scratch{e};
-    CK(cudaEventRecord(e->ev_bos[0], e->stream));
     static_assert(dev::kBosHeads >= dev::kMaxR, "one stream pass covers a GQA group");
-    launch_bos(e, a);
-    dev::bos_finish_kernel<<<std::max<uint32_t>(1, (nh + 7) / 8), 256, 0, e->stream>>>(a);
-    if (weights) {
-        const uint32_t blocks = std::min<uint32_t>((uint32_t)((r * (size_t)T + 255) / 256),
-                                                   8u * (uint32_t)e->num_sms);
-        dev::weights_kernel<<<blocks, 256, 0, e->stream>>>(a);
+    // uploads (query rows, token prefix) + stream + finish [+ weights]: one graph
+    auto enqueue = [&] {
+        CK(cudaMemcpyAsync(e->d_in + e->off_q + q_offset * 4, e->h_in + e->off_q + q_offset * 4,
+                           q_floats * 4, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(scratch + off_pre, e->h_bos, (n_units + 1) * 4, cudaMemcpyHostToDevice,
+                           e->stream));
+        // event-record nodes inside the graph: device time of the kernels alone
+        CK(cudaEventRecordWithFlags(e->ev_bos[0], e->stream, cudaEventRecordExternal));
+        launch_bos(e, a);
+        dev::bos_finish_kernel<<<std::max<uint32_t>(1, (nh + 7) / 8), 256, 0, e->stream>>>(a);
+        if (weights) {
+            const uint32_t blocks = std::min<uint32_t>((uint32_t)((r * (size_t)T + 255) / 256),
+                                                       8u * (uint32_t)e->num_sms);
+            dev::weights_kernel<<<blocks, 256, 0, e->stream>>>(a);
+        }
+        CK(cudaGetLastError());
+        CK(cudaEventRecordWithFlags(e->ev_bos[1], e->stream, cudaEventRecordExternal));
+    };
+    const std::array<uint64_t, 6> key = {layer, u_first, n_units, G, weights ? 1u : 0u, parity};
+    auto it = e->bos_graphs.find(key);
+    if (it == e->bos_graphs.end()) {
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue();
+        } catch (...) {
+            cudaStreamEndCapture(e->stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        CK(cudaStreamEndCapture(e->stream, &g));
+        cudaGraphExec_t x = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&x, g, 0);
+        cudaGraphDestroy(g);
+        CK(ie);
+        it = e->bos_graphs.emplace(key, x).first;
     }
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(e->ev_bos[1], e->stream));
+    CK(cudaGraphLaunch(it->second, e->stream));
     if (weights)
         CK(cudaMemcpyAsync(weights, scratch + off_w, wbytes, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
