@@ -262,6 +262,14 @@ def run_reference_arm(args, world, rank):
 
 
 # ----------------------------------------------------------------------------
+def gate(torch, stream, ms: float = 2.0):
+    """Hold the stream in a short spin kernel while the host enqueues a timed
+    sequence, so host launch latency never lands between a start event and
+    its step (the GPU then runs the sequence back to back)."""
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(ms * 2.0e6))  # ~ms at ~2 GHz
+
+
 def time_async(P, torch, cache, cfg, dq, dout, steps):
     """K back-to-back graph replays, CUDA events on the engine stream.  One
     more untimed replay of THIS config first: switching configs re-patches the
@@ -272,6 +280,7 @@ def time_async(P, torch, cache, cfg, dq, dout, steps):
     e1 = torch.cuda.Event(enable_timing=True)
     P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
     torch.cuda.synchronize()
+    gate(torch, stream)
     e0.record(stream)
     for _ in range(steps):
         P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
@@ -329,6 +338,7 @@ def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
                     P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
                 torch.cuda.synchronize()
                 evs = []
+                gate(torch, stream, 5.0)
                 with torch.cuda.stream(stream):
                     for _ in range(10):
                         flush.sum()  # read-only flush: evicts L2 without dirty write-backs
@@ -375,6 +385,7 @@ def time_flushed(P, torch, cache, cfg, dq, dout, flush, reps=10):
         P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
     torch.cuda.synchronize()
     evs = []
+    gate(torch, stream, 0.5 * reps)
     with torch.cuda.stream(stream):
         for _ in range(reps):
             flush.sum()
