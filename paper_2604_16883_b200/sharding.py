@@ -139,6 +139,13 @@ def sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, dout, 
     P.merge_rank_partials_async(cache, gathered.data_ptr(), world, dout.data_ptr())
 
 
+def _gate(torch, stream, ms: float = 2.0):
+    """Hold the stream in a short spin kernel while the host enqueues a timed
+    sequence (host launch latency then never lands inside a timed step)."""
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(ms * 2.0e6))
+
+
 def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev,
                            peak_gbs=None, peak_src="", clock_sampler=None):
     """bench.py's N>1 path (and --force-sharded at N=1): strong scaling of the
@@ -193,6 +200,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         sampler = clock_sampler(dev) if (clock_sampler and name == "routed") else None
         if sampler:
             sampler.__enter__()
+        _gate(torch, stream)
         e0.record(stream)
         for _ in range(args.steps):
             step(cfg)
@@ -215,6 +223,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        _gate(torch, stream)
         e0.record(stream)
         for _ in range(args.steps):
             sharded_step(P, torch, dist, cache, routed_cfg, opts, dq, partial, gathered, dout, world)
@@ -315,6 +324,7 @@ def bench_unit_sharded(P, torch, dist, spec_cls, args, rank, world, dev, routed_
         dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        _gate(torch, stream)
         e0.record(stream)
         for _ in range(args.steps):
             P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
