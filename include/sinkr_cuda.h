@@ -242,6 +242,14 @@ sinkr_status sinkr_routed_decode_peer_async(sinkr_engine* e, const float* d_quer
                                             const sinkr_routing_config* config,
                                             const sinkr_engine_options* options,
                                             float* d_outputs);
+/* The peer-merged step with host buffers, like sinkr_routed_decode_batch: one
+ * graph per call (H2D of the staged input block + the mode-3 step kernel,
+ * outputs and routing record zero-copy into pinned host memory), blocking. */
+sinkr_status sinkr_routed_decode_peer(sinkr_engine* e, const float* queries, size_t layer,
+                                      const sinkr_routing_config* config,
+                                      const sinkr_engine_options* options, float* outputs,
+                                      sinkr_group_info* groups, double* head_scores,
+                                      sinkr_load_counters* counters);
 
 /* ---- instrumentation ------------------------------------------------------- */
 /* Launch count of the last step (kernels of this library) and the device

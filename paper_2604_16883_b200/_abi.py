@@ -108,7 +108,7 @@ EXPORTS = (
     "sinkr_load_snapshot", "sinkr_load_snapshot_into", "sinkr_kv_append_device_f32",
     # analysis (f4)
     "sinkr_attention_bos_mass", "sinkr_attention_weights", "sinkr_attention_last_kernel_seconds",
-    "sinkr_group_attention", "sinkr_oracle_labels",
+    "sinkr_group_attention", "sinkr_routed_decode_peer", "sinkr_oracle_labels",
     "sinkr_pr_curve",
     # fused sequence-sharded peer merge
     "sinkr_peer_setup", "sinkr_peer_ipc_handle", "sinkr_peer_open", "sinkr_peer_set_blocks",
@@ -171,6 +171,7 @@ def lib():
             "sinkr_attention_weights": [vp, vp, sz, sz, sz, vp],
             "sinkr_attention_last_kernel_seconds": [vp, vp],
             "sinkr_group_attention": [vp, vp, sz, sz, sz, sz, vp, vp],
+            "sinkr_routed_decode_peer": [vp, vp, sz, vp, vp, vp, vp, vp, vp],
             "sinkr_pr_curve": [vp, vp, sz, vp, vp, vp],
             "sinkr_peer_setup": [vp, C.c_uint32, C.c_uint32, vp],
             "sinkr_peer_ipc_handle": [vp, vp],

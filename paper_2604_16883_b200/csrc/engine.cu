@@ -463,10 +463,10 @@ static int io_mode() {
     return m;
 }
 
-void run_io_graph(sinkr_engine* e) {
+void run_io_graph(sinkr_engine* e, int mode = 0) {
     e->last_launches = 1;
-    e->last_mode = 0;
-    const auto key = std::make_tuple((const void*)e->h_in, (void*)e->h_res, 2);
+    e->last_mode = mode;
+    const auto key = std::make_tuple((const void*)e->h_in, (void*)e->h_res, mode == 3 ? 6 : 2);
     auto it = e->graphs.find(key);
     const float* d_q = reinterpret_cast<const float*>(e->d_in + e->off_q);
     const bool zc = io_mode() == 1;
@@ -479,7 +479,7 @@ void run_io_graph(sinkr_engine* e) {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
             const bool timing = e->timing;
             e->timing = false;
-            enqueue_step(e, d_q, out, 0, res);
+            enqueue_step(e, d_q, out, mode, res);
             e->timing = timing;
             if (!zc)
                 CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
@@ -502,7 +502,7 @@ void run_io_graph(sinkr_engine* e) {
             ge.probe = nd;
         }
         if (!ge.probe) fail(SINKR_CUDA_ERROR, "step node not found in the captured graph");
-        ge.step_t = e->step_tables(d_q, out, 0, res);
+        ge.step_t = e->step_tables(d_q, out, mode, res);
         ge.fused = true;
         ge.pp = e->pp;
         it = e->graphs.emplace(key, ge).first;
@@ -1150,12 +1150,37 @@ sinkr_status sinkr_split_ranges(size_t len, size_t num_splits, size_t* from_to) 
 }
 
 // ---- hot path ------------------------------------------------------------------
+static void decode_host(sinkr_engine* e, const float* queries, size_t layer,
+                        const sinkr_routing_config* config, const sinkr_engine_options* options,
+                        float* outputs, sinkr_group_info* groups, double* head_scores,
+                        sinkr_load_counters* counters, int mode);
+
 sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, size_t layer,
                                        const sinkr_routing_config* config,
                                        const sinkr_engine_options* options, float* outputs,
                                        sinkr_group_info* groups, double* head_scores,
                                        sinkr_load_counters* counters) {
     return guard([&] {
+        decode_host(e, queries, layer, config, options, outputs, groups, head_scores, counters, 0);
+    });
+}
+
+sinkr_status sinkr_routed_decode_peer(sinkr_engine* e, const float* queries, size_t layer,
+                                      const sinkr_routing_config* config,
+                                      const sinkr_engine_options* options, float* outputs,
+                                      sinkr_group_info* groups, double* head_scores,
+                                      sinkr_load_counters* counters) {
+    return guard([&] {
+        if (e && !e->d_peer_xchg) fail(SINKR_INVALID_ARGUMENT, "peer merge not set up (sinkr_peer_open)");
+        decode_host(e, queries, layer, config, options, outputs, groups, head_scores, counters, 3);
+    });
+}
+
+static void decode_host(sinkr_engine* e, const float* queries, size_t layer,
+                        const sinkr_routing_config* config, const sinkr_engine_options* options,
+                        float* outputs, sinkr_group_info* groups, double* head_scores,
+                        sinkr_load_counters* counters, int mode) {
+    {
         if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
         if (!queries) fail(SINKR_INVALID_ARGUMENT, "queries span must be H_q x D for one layer");
         CK(cudaSetDevice(e->device));
@@ -1167,12 +1192,12 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
         if (queries != reinterpret_cast<const float*>(e->h_in + e->off_q))
             std::memcpy(e->h_in + e->off_q, queries, qbytes);
         if (e->fused && !e->timing && io_mode() != 0) {
-            run_io_graph(e);  // H2D + step kernel, results land in mapped h_res
+            run_io_graph(e, mode);  // H2D + step kernel, results land in mapped h_res
         } else {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
             CK(cudaEventRecord(e->ev_in, e->stream));
             float* d_out = reinterpret_cast<float*>(e->d_res);
-            run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, 0);
+            run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, mode);
             CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
         }
         CK(cudaStreamSynchronize(e->stream));
@@ -1183,7 +1208,7 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
         }
         if (outputs && outputs != reinterpret_cast<float*>(e->h_res)) std::memcpy(outputs, e->h_res, qbytes);
         fill_info(e, layer, config, groups, head_scores, counters, options);
-    });
+    }
 }
 
 // splitk_attention (attention.cpp:204-235) of ONE cached group on the GPU:

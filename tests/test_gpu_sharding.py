@@ -157,3 +157,23 @@ def test_peer_merge_across_processes_ipc():
                          capture_output=True, text=True, timeout=240, env=env, cwd=root)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
     assert "rank 0 ok" in res.stdout and "rank 1 ok" in res.stdout
+
+
+def test_peer_host_buffer_step_world1():
+    """sinkr_routed_decode_peer (host buffers, one graph, zero-copy outputs) at
+    world 1 returns the plain step's outputs and routing record, repeatedly."""
+    spec = WorkloadSpec(length=30000, sink_fraction=0.5, seed=8)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as cache:
+        spec.fill(cache)
+        q = spec.queries()[0]
+        ref = P.routed_decode_step(q, 0, cache, cfg)
+        (pm,) = _one_gpu_peer_setup(P, [cache])
+        hr = pm.host_runner(cfg, P.EngineOptions())
+        hr.queries[...] = q.reshape(hr.queries.shape)
+        for _ in range(4):
+            out = hr.call()
+            assert np.abs(out.reshape(ref.outputs.shape) - ref.outputs).max() <= 1e-6
+        res = hr.result()
+        assert [g.decision.sink for g in res.groups] == [g.decision.sink for g in ref.groups]
+        assert res.counters.kv_floats_loaded == ref.counters.kv_floats_loaded
