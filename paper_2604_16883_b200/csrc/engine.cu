@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -116,6 +117,11 @@ struct sinkr_engine {
     uint8_t* d_res = nullptr;
     uint8_t* h_res = nullptr;      // pinned + mapped
     uint8_t* h_res_dev = nullptr;  // device address of h_res (zero-copy results)
+    // completion word of a host-buffer step (pinned + mapped): the host
+    // clears it, the step kernel's last CTA sets it after a system fence, and
+    // the blocking call spins on it instead of synchronising the stream
+    uint32_t* h_done = nullptr;
+    uint32_t* h_done_dev = nullptr;
 
     dev::WorkState* d_ws = nullptr;
     uint32_t* d_active = nullptr;
@@ -136,8 +142,8 @@ struct sinkr_engine {
     uint8_t* h_bos_dev = nullptr;        // device address of h_bos
     cudaEvent_t ev_bos[2] = {};          // around run_bos's kernels (device time)
     // run_bos as captured graphs, keyed by (layer, u_first, n_units, G, weights,
-    // parity); dropped when the scratch or the pinned staging is reallocated
-    std::map<std::array<uint64_t, 6>, cudaGraphExec_t> bos_graphs;
+    // parity, T); dropped when the scratch or the pinned staging is reallocated
+    std::map<std::array<uint64_t, 7>, cudaGraphExec_t> bos_graphs;
     void drop_bos_graphs() {
         for (auto& kv : bos_graphs) cudaGraphExecDestroy(kv.second);
         bos_graphs.clear();
@@ -155,6 +161,10 @@ struct sinkr_engine {
     float** d_peer_xchg = nullptr;          // device array [world]
     unsigned int** d_peer_arrive = nullptr;  // device array [world]
     std::vector<void*> ipc_opened;           // peer blocks opened through CUDA IPC
+    // a peer-merge watchdog timeout leaves arrivals of the late rank in
+    // flight (they would count toward a later step): the exchange is unusable
+    // until it is set up again
+    bool peer_poisoned = false;
 
     CUtensorMap tmk{}, tmv{};
     CUtensorMap* d_tmap = nullptr;  // device copies of tmk, tmv (fused kernel)
@@ -345,9 +355,10 @@ void launch_step(sinkr_engine* e, const dev::StepTables& st) {
 }
 
 void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode,
-                  uint8_t* res = nullptr) {
+                  uint8_t* res = nullptr, uint32_t* done = nullptr) {
     if (e->fused) {
-        const dev::StepTables st = e->step_tables(d_q, d_out, mode, res);
+        dev::StepTables st = e->step_tables(d_q, d_out, mode, res);
+        st.done = done;
         if (e->timing) CK(cudaEventRecord(e->ev[0], e->stream));
         switch (e->D) {
             case 32: launch_step<32>(e, st); break;
@@ -479,7 +490,7 @@ void run_io_graph(sinkr_engine* e, int mode = 0) {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
             const bool timing = e->timing;
             e->timing = false;
-            enqueue_step(e, d_q, out, mode, res);
+            enqueue_step(e, d_q, out, mode, res, zc ? e->h_done_dev : nullptr);
             e->timing = timing;
             if (!zc)
                 CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
@@ -503,6 +514,7 @@ void run_io_graph(sinkr_engine* e, int mode = 0) {
         }
         if (!ge.probe) fail(SINKR_CUDA_ERROR, "step node not found in the captured graph");
         ge.step_t = e->step_tables(d_q, out, mode, res);
+        ge.step_t.done = zc ? e->h_done_dev : nullptr;
         ge.fused = true;
         ge.pp = e->pp;
         it = e->graphs.emplace(key, ge).first;
@@ -516,7 +528,33 @@ void run_io_graph(sinkr_engine* e, int mode = 0) {
         kp.extra = nullptr;
         CK(cudaGraphExecKernelNodeSetParams(ge.exec, ge.probe, &kp));
     }
+    if (zc) *reinterpret_cast<volatile uint32_t*>(e->h_done) = 0u;
     CK(cudaGraphLaunch(ge.exec, e->stream));
+}
+
+// Waits for a step launched by run_io_graph.  With zero-copy results the
+// step kernel's last CTA sets the completion word after a system-scope
+// fence, so the host spins on that word (it sees the results as soon as the
+// last CTA has written them, without the kernel-retire -> stream-sync round
+// trip); the stream is polled now and then so a failed launch cannot hang.
+void finish_io(sinkr_engine* e) {
+    if (io_mode() != 1) {
+        CK(cudaStreamSynchronize(e->stream));
+        return;
+    }
+    const volatile uint32_t* w = e->h_done;
+    for (uint32_t i = 1;; ++i) {
+        if (*w) break;
+        if ((i & 0x3FFFu) == 0) {
+            const cudaError_t q = cudaStreamQuery(e->stream);
+            if (q == cudaSuccess) {
+                if (*w) break;
+                fail(SINKR_CUDA_ERROR, "step finished without setting its completion word");
+            }
+            if (q != cudaErrorNotReady) CK(q);
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
 }
 
 size_t token_count(const sinkr_engine* e, size_t seq) {
@@ -614,6 +652,7 @@ void fill_info(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg,
         const auto* st = reinterpret_cast<const uint32_t*>(e->h_res + e->off_status);
         const auto* clk = reinterpret_cast<const unsigned long long*>(st + 4);
         if (st[0]) {
+            if (st[0] == 5) e->peer_poisoned = true;
             static const char* what[] = {"", "partial spill-slot lock timeout",
                                          "merge watchdog: a group never completed",
                                          "routing grid-barrier watchdog",
@@ -754,6 +793,9 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_res_dev), e->h_res, 0));
             std::memset(e->h_res, 0, e->res_bytes);
             CK(cudaMemsetAsync(e->d_res, 0, e->res_bytes, e->stream));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&e->h_done), 64, cudaHostAllocMapped));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_done_dev), e->h_done, 0));
+            *e->h_done = 0u;
 
             CK(cudaMalloc(&e->d_head_degen, e->B * Hq * 4));
             e->probe_grid = (int)((e->B * Hq + dev::kProbeHeads - 1) / dev::kProbeHeads);
@@ -885,6 +927,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_partials);
     if (e->h_in) cudaFreeHost(e->h_in);
     if (e->h_res) cudaFreeHost(e->h_res);
+    if (e->h_done) cudaFreeHost(e->h_done);
     if (e->h_bos) cudaFreeHost(e->h_bos);
     for (auto ev : e->ev_bos)
         if (ev) cudaEventDestroy(ev);
@@ -1172,6 +1215,8 @@ sinkr_status sinkr_routed_decode_peer(sinkr_engine* e, const float* queries, siz
                                       sinkr_load_counters* counters) {
     return guard([&] {
         if (e && !e->d_peer_xchg) fail(SINKR_INVALID_ARGUMENT, "peer merge not set up (sinkr_peer_open)");
+        if (e && e->peer_poisoned)
+            fail(SINKR_LOGIC_ERROR, "peer merge disabled after a watchdog timeout (set it up again)");
         decode_host(e, queries, layer, config, options, outputs, groups, head_scores, counters, 3);
     });
 }
@@ -1193,14 +1238,15 @@ static void decode_host(sinkr_engine* e, const float* queries, size_t layer,
             std::memcpy(e->h_in + e->off_q, queries, qbytes);
         if (e->fused && !e->timing && io_mode() != 0) {
             run_io_graph(e, mode);  // H2D + step kernel, results land in mapped h_res
+            finish_io(e);
         } else {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
             CK(cudaEventRecord(e->ev_in, e->stream));
             float* d_out = reinterpret_cast<float*>(e->d_res);
             run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, mode);
             CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+            CK(cudaStreamSynchronize(e->stream));
         }
-        CK(cudaStreamSynchronize(e->stream));
         if (!e->fused) {
             dev::WorkState ws;
             CK(cudaMemcpy(&ws, e->d_ws, sizeof(ws), cudaMemcpyDeviceToHost));
@@ -1257,14 +1303,15 @@ sinkr_status sinkr_group_attention(sinkr_engine* e, const float* group_queries, 
         std::memcpy(q + row0, group_queries, r * D * 4);
         if (e->fused && !e->timing && io_mode() != 0) {
             run_io_graph(e);
+            finish_io(e);
         } else {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
             CK(cudaEventRecord(e->ev_in, e->stream));
             run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q),
                       reinterpret_cast<float*>(e->d_res), 0);
             CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+            CK(cudaStreamSynchronize(e->stream));
         }
-        CK(cudaStreamSynchronize(e->stream));
         e->pp.only_unit = 0;
         const auto* fl = reinterpret_cast<const uint32_t*>(e->h_res + e->off_fl);
         const auto* tok = reinterpret_cast<const unsigned long long*>(e->h_res + e->off_tok);
@@ -1541,7 +1588,10 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
         CK(cudaGetLastError());
         CK(cudaEventRecordWithFlags(e->ev_bos[1], e->stream, cudaEventRecordExternal));
     };
-    const std::array<uint64_t, 6> key = {layer, u_first, n_units, G, weights ? 1u : 0u, parity};
+    // T is part of the key: the captured kernel arguments (a.weights =
+    // scratch + off_w, the weights grid) move with the token count even when
+    // the scratch is not reallocated
+    const std::array<uint64_t, 7> key = {layer, u_first, n_units, G, weights ? 1u : 0u, parity, T};
     auto it = e->bos_graphs.find(key);
     if (it == e->bos_graphs.end()) {
         cudaGraph_t g = nullptr;
@@ -1647,7 +1697,27 @@ sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, si
             fail(SINKR_INVALID_ARGUMENT, "peer merge needs 1 <= world <= 8 and rank < world");
         if (!e->fused) fail(SINKR_INVALID_ARGUMENT, "peer merge needs the fused step kernel");
         CK(cudaSetDevice(e->device));
-        if (e->d_xchg) fail(SINKR_LOGIC_ERROR, "peer merge already set up");
+        if (e->d_xchg && !e->peer_poisoned) fail(SINKR_LOGIC_ERROR, "peer merge already set up");
+        if (e->d_xchg) {
+            // after a watchdog timeout: a fresh exchange block, fresh device
+            // epoch / arrival base; every rank sets up and connects again
+            CK(cudaStreamSynchronize(e->stream));
+            for (auto& kv : e->graphs) {
+                cudaGraphExecDestroy(kv.second.exec);
+                cudaGraphDestroy(kv.second.graph);
+            }
+            e->graphs.clear();
+            for (void* pb : e->ipc_opened) cudaIpcCloseMemHandle(pb);
+            e->ipc_opened.clear();
+            cudaFree(e->d_xchg);
+            cudaFree(e->d_peer_xchg);
+            cudaFree(e->d_peer_arrive);
+            e->d_xchg = nullptr;
+            e->d_peer_xchg = nullptr;
+            e->d_peer_arrive = nullptr;
+            CK(cudaMemset(e->d_ss, 0, sizeof(dev::StepState)));
+            e->peer_poisoned = false;
+        }
         e->world = world;
         e->rank = rank;
         e->xchg_floats = 2ull * world * e->U * e->PS;
@@ -1708,6 +1778,8 @@ sinkr_status sinkr_routed_decode_peer_async(sinkr_engine* e, const float* d_quer
     return guard([&] {
         if (!e || !d_queries || !d_outputs) fail(SINKR_INVALID_ARGUMENT, "null argument");
         if (!e->d_peer_xchg) fail(SINKR_INVALID_ARGUMENT, "peer merge not set up (sinkr_peer_open)");
+        if (e->peer_poisoned)
+            fail(SINKR_LOGIC_ERROR, "peer merge disabled after a watchdog timeout (set it up again)");
         CK(cudaSetDevice(e->device));
         stage_params(e, layer, config, options, false);
         run_graph(e, d_queries, d_outputs, 3);

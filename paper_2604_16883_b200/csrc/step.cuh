@@ -85,6 +85,7 @@ struct StepTables {
     uint32_t world, rank;
     float qscale;                  // (1/sqrt(D)) * log2(e)
     unsigned long long* trace;     // optional [grid][4] per-CTA globaltimer stamps
+    uint32_t* done;                // optional completion word in mapped host memory (set to 1 last)
 };
 
 template <int D>
@@ -112,7 +113,7 @@ struct StepCfg {
 };
 
 // misc smem words
-enum : int { kMiscNact = 0, kMiscChunk, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast };
+enum : int { kMiscNact = 0, kMiscChunk, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast, kMiscPeerLate };
 
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -1376,37 +1377,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
-    // ======================= exit: last CTA restores the counters ================
+    // ======================= mode 3: merge every rank's partials ===============
+    // Every merge task signalled every rank once (warp_merge), so this step's
+    // partials are all here when the arrivals reach base + world * tasks (a
+    // rank a step ahead only adds arrivals that causally follow every partial
+    // of this step).  The CTAs that own output elements wait, then merge them
+    // -- BEFORE they count out below, so the status the last CTA publishes
+    // covers their waits.  A rank that never delivers is a watchdog error:
+    // the owners then write NaN rather than a merge of incomplete partials.
+    const uint32_t peer_want = peer_base + t.world * (nact * r * (D / 32));
     __syncthreads();
     STAMP(10);
-    if (t.trace && tid == 0) t.trace[bid * 8 + 2] = globaltimer();
-    if (tid == 0) {
-        // gpu-scope acq_rel count: releases this CTA's writes (ordered before
-        // tid 0 by the barrier) and, for the last CTA, acquires everyone's
-        misc[kMiscLast] = (ptx::atom_add_acq_rel(&t.ss->exit_count, 1u) == G - 1) ? 1u : 0u;
-    }
-    __syncthreads();
-    // mode 3: every merge task signalled every rank once (warp_merge), so this
-    // step's partials are all here when the arrivals reach base + world *
-    // tasks (a rank a step ahead only adds arrivals that causally follow every
-    // partial of this step); the CTAs that own output elements wait, then
-    // merge them (the others leave at once)
-    const uint32_t peer_want = peer_base + t.world * (nact * r * (D / 32));
     if (t.mode == 3 && bid * kThreads < nact * r * D) {
         if (tid == 0) {
             const unsigned int want = peer_want;
             const unsigned long long t_spin = globaltimer();
+            uint32_t late = 0;
             for (;;) {
                 unsigned int v;
                 asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(t.arrive_local) : "memory");
                 if ((int)(v - want) >= 0) break;
                 if (globaltimer() - t_spin > 2000000000ull) {
                     atomicExch(&t.ss->error, 5u);
+                    late = 1;
                     break;
                 }
             }
+            misc[kMiscPeerLate] = late;
         }
         __syncthreads();
+        const bool late = misc[kMiscPeerLate] != 0;
         const uint32_t PSx = r * (D + 2);
         const float* X = t.xchg_local + size_t((epoch & 1u) * t.world) * U * PSx;
         for (uint32_t e = bid * kThreads + tid; e < nact * r * D; e += G * kThreads) {
@@ -1431,9 +1431,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc += aq[q] * w;
                 lsum += lq[q] * w;
             }
-            t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
+            t.out[(size_t(u) * r + h) * D + d] = late ? __int_as_float(0x7fc00000) : acc / lsum;
         }
     }
+
+    // ======================= exit: last CTA restores the counters ================
+    __syncthreads();
+    if (t.trace && tid == 0) t.trace[bid * 8 + 2] = globaltimer();
+    if (tid == 0) {
+        // acq_rel count: releases this CTA's writes (ordered before tid 0 by
+        // the barrier) and, for the last CTA, acquires everyone's.  System
+        // scope when results go to mapped host memory and a host thread waits
+        // on the completion word instead of the stream.
+        const uint32_t prev = t.done ? ptx::atom_add_acq_rel_sys(&t.ss->exit_count, 1u)
+                                     : ptx::atom_add_acq_rel(&t.ss->exit_count, 1u);
+        misc[kMiscLast] = prev == G - 1 ? 1u : 0u;
+    }
+    __syncthreads();
     STAMP(11);
     if (misc[kMiscLast]) {
         for (uint32_t a = tid; a < nact; a += kThreads) {
@@ -1456,6 +1470,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (t.mode == 3) {
                 t.ss->peer_epoch = epoch + 1u;
                 t.ss->peer_base = peer_want;
+            }
+            if (t.done) {
+                // every CTA's results (outputs, routing record, status) are
+                // visible system-wide before the host sees the word
+                __threadfence_system();
+                ptx::st_release_sys(t.done, 1u);
             }
         }
     }

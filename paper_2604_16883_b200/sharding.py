@@ -166,11 +166,39 @@ def _gate(torch, stream, ms: float = 2.0):
         torch.cuda._sleep(int(ms * 2.0e6))
 
 
-def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev,
-                           peak_gbs=None, peak_src="", clock_sampler=None):
-    """bench.py's N>1 path (and --force-sharded at N=1): strong scaling of the
-    headline workload, every number the max over ranks."""
-    import json
+def _peer_self_check(P, torch, dist, pm, cache, cfg, opts, dq, partial, gathered, world):
+    """One fused peer-merge step against one all-gather + combine step on the
+    same inputs, on every rank: the fused path is used only if every rank
+    agrees (outputs within 1e-5, no step-kernel error such as the peer
+    watchdog).  Returns None when it passed, else the reason."""
+    why = None
+    try:
+        a = torch.empty_like(dq)
+        b = torch.empty_like(dq)
+        a.fill_(float("nan"))
+        pm.step(dq, a, cfg, opts)
+        torch.cuda.synchronize()
+        P.fetch_step_info(cache)  # raises on a step-kernel error (peer watchdog)
+        sharded_step(P, torch, dist, cache, cfg, opts, dq, partial, gathered, b, world)
+        torch.cuda.synchronize()
+        err = (a - b).abs().max().item()
+        if not err <= 1e-5:  # NaN fails too
+            why = f"self-check: fused peer merge differs from all-gather + combine by {err:.3e}"
+    except Exception as ex:  # noqa: BLE001 -- reported in the bench line
+        why = f"self-check: {type(ex).__name__}: {ex}"
+    ok = torch.tensor([0 if why else 1], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if why is None and int(ok.item()) == 0:
+        why = "self-check failed on another rank"
+    return why
+
+
+def time_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev,
+                          clock_sampler=None, e2e=True):
+    """Strong-scaling timing of one sequence-sharded workload: routed and dense
+    back-to-back steps on the product path (fused peer merge when every rank
+    passes the self-check, else NCCL all-gather + combine), the all-gather path
+    beside it, and the host-buffer e2e.  Every number is the max over ranks."""
     import statistics
     import time
 
@@ -186,7 +214,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
     gathered = torch.empty(world * nf, dtype=torch.float32, device="cuda")
     stream = torch.cuda.ExternalStream(cache.stream)
     # the merge fused into the step kernel over peer memory; NCCL all-gather +
-    # combine kernel when peer mappings are unavailable (both timed below)
+    # combine kernel when peer mappings are unavailable or the self-check fails
     pm, peer_err = None, None
     try:
         pm = PeerMerge(P, cache, world, rank, dist, torch)
@@ -196,6 +224,12 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if int(ok.item()) == 0:
         pm = None
+        peer_err = peer_err or "peer mapping failed on another rank"
+    if pm is not None:
+        peer_err = _peer_self_check(P, torch, dist, pm, cache, routed_cfg, opts, dq, partial,
+                                    gathered, world)
+        if peer_err:
+            pm = None
 
     def step(cfg):
         if pm is not None:
@@ -210,6 +244,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
 
     res = {}
     clocks = None
+    n_act = 0
     for name, cfg in (("routed", routed_cfg), ("dense", dense_cfg)):
         for _ in range(max(3, args.warmup)):
             step(cfg)
@@ -252,97 +287,149 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         torch.cuda.synchronize()
         nccl_us = maxed(e0.elapsed_time(e1) / args.steps) * 1e3
 
-    # e2e: host queries in (pinned H2D), sharded step, host outputs out, per step;
-    # with the fused peer merge, the blocking host-buffer call over the engine's
-    # pinned step buffers (one graph: upload + step, outputs zero-copy)
-    if pm is not None:
-        hr = pm.host_runner(routed_cfg, opts)
-        hr.queries[...] = q_host.numpy().reshape(hr.queries.shape)
-        for _ in range(3):
-            hr.call()
+    out = {"routed_ms": res["routed"], "dense_ms": res["dense"], "groups_active": n_act,
+           "lo": lo, "hi": hi, "peer": pm is not None, "peer_err": peer_err, "clocks": clocks,
+           "allgather_us": nccl_us, "partial_bytes_per_rank": nf * 4}
+    if e2e:
+        # e2e: host queries in (pinned H2D), sharded step, host outputs out, per
+        # step; with the fused peer merge, the blocking host-buffer call over the
+        # engine's pinned step buffers (one graph: upload + step, outputs
+        # zero-copy, completion word)
+        e2e_peer_us = None
+        if pm is not None:
+            hr = pm.host_runner(routed_cfg, opts)
+            hr.queries[...] = q_host.numpy().reshape(hr.queries.shape)
+            for _ in range(3):
+                hr.call()
+            dist.barrier()
+            ts = []
+            for _ in range(max(args.steps, 50)):
+                t0 = time.perf_counter()
+                hr.call()
+                ts.append((time.perf_counter() - t0) * 1e6)
+            e2e_peer_us = maxed(statistics.median(ts))
+        for _ in range(2):
+            with torch.cuda.stream(stream):
+                dq.copy_(q_host, non_blocking=True)
+            step(routed_cfg)
+            with torch.cuda.stream(stream):
+                out_host.copy_(dout, non_blocking=True)
+            stream.synchronize()
         dist.barrier()
         ts = []
-        for _ in range(max(args.steps, 50)):
+        for _ in range(max(args.steps, 50)):  # each step timed alone, median
             t0 = time.perf_counter()
-            hr.call()
+            with torch.cuda.stream(stream):
+                dq.copy_(q_host, non_blocking=True)
+            step(routed_cfg)
+            with torch.cuda.stream(stream):
+                out_host.copy_(dout, non_blocking=True)
+            stream.synchronize()
             ts.append((time.perf_counter() - t0) * 1e6)
-        e2e_peer_us = maxed(statistics.median(ts))
-    for _ in range(2):
-        with torch.cuda.stream(stream):
-            dq.copy_(q_host, non_blocking=True)
-        step(routed_cfg)
-        with torch.cuda.stream(stream):
-            out_host.copy_(dout, non_blocking=True)
-        stream.synchronize()
-    dist.barrier()
-    ts = []
-    for _ in range(max(args.steps, 50)):  # each step timed alone, median (robust to host hiccups)
-        t0 = time.perf_counter()
-        with torch.cuda.stream(stream):
-            dq.copy_(q_host, non_blocking=True)
-        step(routed_cfg)
-        with torch.cuda.stream(stream):
-            out_host.copy_(dout, non_blocking=True)
-        stream.synchronize()
-        ts.append((time.perf_counter() - t0) * 1e6)
-    e2e_copy_us = maxed(statistics.median(ts))
-    # the product path's e2e: the blocking peer call when peer mappings exist
-    e2e_us = e2e_peer_us if pm is not None else e2e_copy_us
-    h2d_bytes, d2h_bytes = int(q_host.numel() * 4), int(out_host.numel() * 4)
-    if pm is not None:  # the peer call moves the staged input block and the result block
-        h2d_bytes, d2h_bytes = cache.step_io_bytes()
+        e2e_copy_us = maxed(statistics.median(ts))
+        h2d_bytes, d2h_bytes = int(q_host.numel() * 4), int(out_host.numel() * 4)
+        if pm is not None:  # the peer call moves the staged input block and the result block
+            h2d_bytes, d2h_bytes = cache.step_io_bytes()
+        out.update(e2e_us=e2e_peer_us if pm is not None else e2e_copy_us, e2e_copy_us=e2e_copy_us,
+                   h2d_bytes=h2d_bytes, d2h_bytes=d2h_bytes)
     # pinned host blocks record an event on the engine stream when freed: free
     # them while the engine (and its stream) is alive
     stream.synchronize()
     del q_host, out_host
+    cache.close()
+    return out
 
+
+def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev,
+                           peak_gbs=None, peak_src="", clock_sampler=None, config=None):
+    """bench.py's N>1 path (and --force-sharded at N=1): strong scaling of the
+    headline workload, every number the max over ranks; other_configs adds
+    BASELINE configs[3] (Llama-3.1-70B shape, 512K, sequence-sharded -- the
+    north star's 8-way case) and configs[2] (Yi-9B, B=16, unit-sharded)."""
+    import json
+
+    t = time_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev,
+                              clock_sampler=clock_sampler)
+    pm = t["peer"]
+    n_act, lo, hi = t["groups_active"], t["lo"], t["hi"]
     kv_total = n_act * 2 * spec.length * spec.head_dim * 2          # all ranks
     kv_rank = n_act * 2 * (hi - lo) * spec.head_dim * 2             # this rank
-    per_gpu_gbs = kv_rank / (res["routed"] * 1e-3) / 1e9  # the step time is already max-over-ranks
+    routed_ms, dense_ms = t["routed_ms"], t["dense_ms"]
+    per_gpu_gbs = kv_rank / (routed_ms * 1e-3) / 1e9  # the step time is already max-over-ranks
+    cfg_dict = dict(config or {})
+    cfg_dict.update({
+        "workload": f"llama3.1-8b-attn L={spec.length} B=1 routed={spec.sink_fraction}",
+        "parallelism": (f"sequence-shard x{world} + LSE merge fused into the step kernel "
+                        "over peer memory (NVLink)") if pm else
+                       f"sequence-shard x{world} + NCCL all-gather + combine kernel",
+        "tokens_per_rank": hi - lo,
+        "l2": "per-rank KV larger than L2 at N <= 4; L2 not flushed between back-to-back steps"})
     line = {
         "metric": ("decode-attn \u00b5s/step & KV GB/s (% HBM peak) at 512K; "
                    "speedup vs own dense path"),
-        "value": round(res["routed"] * 1e3, 2), "unit": "us/step", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["routed"], 5),
+        "value": round(routed_ms * 1e3, 2), "unit": "us/step", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(routed_ms, 5),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic planted-sink KV (device generator, seeded); fp32 queries",
-        "config": {"workload": f"llama3.1-8b-attn L={spec.length} B=1 "
-                               f"routed={spec.sink_fraction} sequence-sharded",
-                   "parallelism": (f"sequence-shard x{world} + LSE merge fused into the step kernel "
-                                   "over peer memory (NVLink)") if pm is not None else
-                                  f"sequence-shard x{world} + NCCL all-gather + combine kernel",
-                   "context": spec.length, "tokens_per_rank": hi - lo,
-                   "l2": "per-rank KV larger than L2 at N <= 8"},
-        "dense_us_per_step": round(res["dense"] * 1e3, 2),
-        "speedup_vs_dense": round(res["dense"] / res["routed"], 3),
-        "kv_gbs_routed_step": round(kv_total / (res["routed"] * 1e-3) / 1e9, 1),
+        "config": cfg_dict,
+        "dense_us_per_step": round(dense_ms * 1e3, 2),
+        "speedup_vs_dense": round(dense_ms / routed_ms, 3),
+        "kv_gbs_routed_step": round(kv_total / (routed_ms * 1e-3) / 1e9, 1),
         "roofline": {"bound": "hbm", "achieved": round(per_gpu_gbs, 1),
                      "peak": peak_gbs, "unit": "GB/s",
                      "frac": round(per_gpu_gbs / peak_gbs, 4) if peak_gbs else None,
                      "traffic": None,
                      "kernel": ("step_kernel<128> with the rank merge fused over peer memory (mode 3)"
-                                if pm is not None else
+                                if pm else
                                 "step_kernel<128> rank partial (per GPU) + NCCL all-gather + combine_kernel"),
+                     "achieved_def": "this rank's Active K+V bytes / max-over-ranks step time",
                      "peak_source": peak_src},
-        "e2e": {"value": round(e2e_us, 2), "unit": "us/step",
-                "h2d_bytes_per_step": h2d_bytes,
-                "d2h_bytes_per_step": d2h_bytes,
+        "e2e": {"value": round(t["e2e_us"], 2), "unit": "us/step",
+                "h2d_bytes_per_step": t["h2d_bytes"],
+                "d2h_bytes_per_step": t["d2h_bytes"],
                 "method": ("blocking sinkr_routed_decode_peer over the engine's pinned step "
-                           "buffers, per-step median, max over ranks" if pm is not None else
+                           "buffers, per-step median, max over ranks" if pm else
                            "torch pinned copies around the all-gather step, per-step median, "
                            "max over ranks"),
-                "torch_copies_us": round(e2e_copy_us, 2)},
-        "gpu_launches": (1 if pm is not None else 2) * args.steps,  # ours only (NCCL's not counted)
-        "allgather_combine_us_per_step": round(nccl_us, 2) if nccl_us is not None else None,
-        "peer_merge_unavailable": peer_err,
-        "clocks": clocks,
-        "note": json.dumps({"partial_bytes_per_rank": nf * 4}),
+                "torch_copies_us": round(t["e2e_copy_us"], 2)},
+        "gpu_launches": (1 if pm else 2) * args.steps,  # ours only (NCCL's not counted)
+        "allgather_combine_us_per_step": (round(t["allgather_us"], 2)
+                                          if t["allgather_us"] is not None else None),
+        "peer_merge_unavailable": t["peer_err"],
+        "clocks": t["clocks"],
+        "note": json.dumps({"partial_bytes_per_rank": t["partial_bytes_per_rank"]}),
     }
-    cache.close()
-    line["other_configs"] = [bench_unit_sharded(P, torch, dist, spec_cls=type(spec), args=args,
-                                                rank=rank, world=world, dev=dev,
-                                                routed_cfg=routed_cfg, dense_cfg=dense_cfg)]
+    line["other_configs"] = [
+        bench_c4_sequence_sharded(P, torch, dist, spec_cls=type(spec), args=args, rank=rank,
+                                  world=world, dev=dev, routed_cfg=routed_cfg, dense_cfg=dense_cfg,
+                                  peak_gbs=peak_gbs),
+        bench_unit_sharded(P, torch, dist, spec_cls=type(spec), args=args, rank=rank, world=world,
+                           dev=dev, routed_cfg=routed_cfg, dense_cfg=dense_cfg)]
     return line
+
+
+def bench_c4_sequence_sharded(P, torch, dist, spec_cls, args, rank, world, dev, routed_cfg,
+                              dense_cfg, peak_gbs=None):
+    """BASELINE configs[3]: Llama-3.1-70B attention shape (64 q / 8 KV heads,
+    r = 8) at L = 524,288, sequence-sharded over the ranks with the product
+    merge path; per-GPU roofline fraction of this rank's Active K+V stream."""
+    spec = spec_cls(num_q_heads=64, num_kv_heads=8, head_dim=128, length=524288,
+                    sink_fraction=args.sink_fraction, seed=args.seed + 70)
+    t = time_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, rank, world, dev,
+                              e2e=False)
+    n_act, lo, hi = t["groups_active"], t["lo"], t["hi"]
+    kv_rank = n_act * 2 * (hi - lo) * 128 * 2
+    gbs = kv_rank / (t["routed_ms"] * 1e-3) / 1e9
+    return {"config": f"C4 llama3.1-70b-attn L=524288 B=1, sequence-sharded x{world}",
+            "merge": "fused peer merge (mode 3)" if t["peer"] else "NCCL all-gather + combine",
+            "peer_merge_unavailable": t["peer_err"],
+            "groups_active": n_act, "groups_total": 8, "tokens_per_rank": hi - lo,
+            "routed_us": round(t["routed_ms"] * 1e3, 2), "dense_us": round(t["dense_ms"] * 1e3, 2),
+            "speedup_vs_dense": round(t["dense_ms"] / t["routed_ms"], 3),
+            "per_gpu_kv_gbs_routed": round(gbs, 1),
+            "per_gpu_roofline_frac": round(gbs / peak_gbs, 4) if peak_gbs else None,
+            "allgather_combine_us": (round(t["allgather_us"], 2)
+                                     if t["allgather_us"] is not None else None)}
 
 
 def bench_unit_sharded(P, torch, dist, spec_cls, args, rank, world, dev, routed_cfg, dense_cfg):

@@ -244,6 +244,34 @@ def test_bos_mass_ragged_shapes(ref, B, hq, hkv, D):
             assert np.abs(w - rw).max() <= 1e-6, (s, g, np.abs(w - rw).max())
 
 
+def test_attention_weights_after_length_change(ref):
+    """attention_weights twice on one unit whose length changed in between,
+    after a longer unit sized the scratch (no reallocation): the captured
+    graph must follow the new token count (its weights offset moves with T)."""
+    rng = np.random.default_rng(77)
+    D, cap = 128, 12000
+    with P.KvCache(P.CacheConfig(1, 32, 8, D, cap)) as cache:
+        ks = {}
+        for g, n in ((1, 11000), (0, 2000)):
+            k = round_bf16((rng.standard_normal((n, D)) * 1.5).astype(np.float32))
+            k[0] *= 6.0
+            v = round_bf16(rng.standard_normal((n, D)).astype(np.float32))
+            cache.append(0, g, k, v)
+            ks[g] = k
+        q = (rng.standard_normal((4, D)) * 3.0).astype(np.float32)
+        A.attention_weights(cache, q, 0, 1)  # the scratch covers 11,000 tokens
+        for extra in (0, 37, 1500, 16):
+            if extra:
+                k = round_bf16((rng.standard_normal((extra, D)) * 1.5).astype(np.float32))
+                v = round_bf16(rng.standard_normal((extra, D)).astype(np.float32))
+                cache.append(0, 0, k, v)
+                ks[0] = np.concatenate([ks[0], k])
+            w = A.attention_weights(cache, q, 0, 0)
+            rw = ref.attention_weights(q, ks[0])
+            assert w.shape == rw.shape
+            assert np.abs(w - rw).max() <= 1e-6, (extra, np.abs(w - rw).max())
+
+
 def test_route_eval_planted_workload():
     """SPEC.md analysis invariant: on the planted workload the proxy at tau 0.5
     gives precision = recall = 1 against oracle labels with gamma 0.65, and the

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+import oracle
 import paper_2604_16883_b200 as P
 from paper_2604_16883_b200 import sharding
 from paper_2604_16883_b200.workload import WorkloadSpec
@@ -137,6 +138,87 @@ def test_peer_merge_two_ranks_on_one_gpu(world, monkeypatch):
         s_.close()
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_merge_world_n_vs_reference(world, monkeypatch, oracle_libs):
+    """The DEFAULT multi-GPU product path -- the rank merge fused into the step
+    kernel over peer memory (mode 3) -- at world 2/4/8, against the COMPILED
+    REFERENCE's unsharded routed_decode_step.  BASELINE configs[3] shape
+    (Llama-3.1-70B: 64 q / 8 KV heads, r = 8), 65,536 tokens per rank (world 8
+    = the 512K config); the ranks are `world` engines on one GPU, each with
+    floor(#SMs / world) CTAs, so their cooperative step kernels run side by
+    side and exchange partials through each other's blocks.  Three steps
+    (both parities of the exchange slots).  Bar: bitmap and group-score bytes
+    equal, per-group rows summed over ranks equal to the reference's
+    kv_floats, max-abs <= 2e-3 AND rel-L2 <= 1e-3 on every rank, Sink rows
+    bitwise zero."""
+    ref_lib, orc = oracle_libs
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    monkeypatch.setenv("SINKR_DEBUG_GRID", str(sms // world))
+    per_rank = 65536
+    L = per_rank * world
+    spec = WorkloadSpec(num_q_heads=64, num_kv_heads=8, head_dim=128, length=L,
+                        sink_fraction=0.625, seed=300 + world)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    q = spec.queries()[0]
+    dq = torch.from_numpy(q).cuda()
+    shards = [sharding.build_sequence_shard(P, spec, k, world, 0) for k in range(world)]
+    caches = [c for c, _ in shards]
+    pms = _one_gpu_peer_setup(P, caches)
+    opts = P.EngineOptions(global_context_len=L)
+    outs = [torch.empty_like(dq) for _ in range(world)]
+    got = []
+    for _ in range(3):
+        for pm, o in zip(pms, outs):
+            o.fill_(float("nan"))
+            pm.step(dq, o, cfg, opts)
+        torch.cuda.synchronize()
+        got.append([o.cpu().numpy() for o in outs])
+    infos = [P.fetch_step_info(c) for c in caches]
+    kv_sum = np.zeros(spec.num_kv_heads, dtype=np.uint64)
+    for info, (_, (lo, hi)) in zip(infos, shards):
+        assert np.array_equal(info.route_bitmap, infos[0].route_bitmap)
+        kv_sum += np.array([g.kv_floats_loaded for g in info.groups], dtype=np.uint64)
+        for g in info.groups:
+            assert g.tokens_loaded == (0 if g.decision.sink else hi - lo)
+    # the unsharded reference over exactly the tokens the shards hold
+    r = spec.r
+    if ref_lib is not None:
+        rc = oracle.RefCache(ref_lib, 1, 64, 8, 128, L)
+        for g in range(spec.num_kv_heads):
+            ks, vs = [], []
+            for c, (lo, hi) in shards:
+                k, v = c.historical(0, g, 0, hi - lo)
+                ks.append(k)
+                vs.append(v)
+            rc.append_rows(0, g, np.concatenate(ks), np.concatenate(vs))
+            del ks, vs
+        ref = rc.routed_decode_step(q, 0, oracle.Profile.constant(0.5), excluded=(), workers=16)
+        rc.close()
+    else:  # no compiled reference on this host: the pinned C restatement
+        k = np.stack([np.concatenate([c.historical(0, g, 0, hi - lo)[0] for c, (lo, hi) in shards])
+                      for g in range(8)])
+        v = np.stack([np.concatenate([c.historical(0, g, 0, hi - lo)[1] for c, (lo, hi) in shards])
+                      for g in range(8)])
+        k0 = np.ascontiguousarray(k[:, 0])
+        ref = orc.routed_decode_step(k, v, k0, [orc.anchor_norm(x) for x in k0], q, 0,
+                                     oracle.Profile.constant(0.5), excluded=(), threads=16)
+        del k, v
+    assert np.array_equal(infos[0].route_bitmap.astype(np.int32), ref.sink.astype(np.int32))
+    gs = np.array([g.decision.group_score for g in infos[0].groups])
+    assert gs.tobytes() == np.asarray(ref.group_scores).tobytes()
+    assert list(kv_sum) == [int(x) for x in ref.group_kv_floats]
+    ro = np.asarray(ref.outputs).reshape(64, 128)
+    for step_outs in got:
+        for o in step_outs:
+            assert np.abs(o - ro).max() <= 2e-3
+            assert np.linalg.norm(o - ro) <= 1e-3 * np.linalg.norm(ro)
+            for gi in range(8):
+                if ref.sink[gi]:
+                    assert not np.any(o[gi * r:(gi + 1) * r].view(np.uint32))
+    for c in caches:
+        c.close()
+
+
 def test_peer_merge_across_processes_ipc():
     """The fused peer merge between two PROCESSES (one engine each, CUDA IPC
     mappings of each other's exchange blocks, gloo for the handle exchange), on
@@ -159,21 +241,38 @@ def test_peer_merge_across_processes_ipc():
     assert "rank 0 ok" in res.stdout and "rank 1 ok" in res.stdout
 
 
-def test_peer_host_buffer_step_world1():
-    """sinkr_routed_decode_peer (host buffers, one graph, zero-copy outputs) at
-    world 1 returns the plain step's outputs and routing record, repeatedly."""
+@pytest.mark.parametrize("timing", [False, True])
+def test_peer_host_buffer_step_world1(timing):
+    """sinkr_routed_decode_peer (host buffers, zero-copy outputs) at world 1
+    returns the plain step's outputs and routing record, repeatedly.  With
+    timing off the call is the single captured graph (H2D + mode-3 step,
+    outputs into mapped host memory) that the sharded bench's e2e measures;
+    plain steps and device-buffer peer steps are interleaved between host
+    calls, so graph keying and the device-side peer epoch / arrival base are
+    exercised across all three entry points."""
     spec = WorkloadSpec(length=30000, sink_fraction=0.5, seed=8)
     cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
     with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as cache:
         spec.fill(cache)
+        P.set_timing(cache, timing)
         q = spec.queries()[0]
         ref = P.routed_decode_step(q, 0, cache, cfg)
         (pm,) = _one_gpu_peer_setup(P, [cache])
         hr = pm.host_runner(cfg, P.EngineOptions())
         hr.queries[...] = q.reshape(hr.queries.shape)
-        for _ in range(4):
+        dq = torch.from_numpy(q).cuda()
+        dout = torch.empty_like(dq)
+        for it in range(6):
             out = hr.call()
-            assert np.abs(out.reshape(ref.outputs.shape) - ref.outputs).max() <= 1e-6
-        res = hr.result()
-        assert [g.decision.sink for g in res.groups] == [g.decision.sink for g in ref.groups]
-        assert res.counters.kv_floats_loaded == ref.counters.kv_floats_loaded
+            assert np.abs(out.reshape(ref.outputs.shape) - ref.outputs).max() <= 1e-6, it
+            res = hr.result()
+            assert [g.decision.sink for g in res.groups] == [g.decision.sink for g in ref.groups]
+            assert res.counters.kv_floats_loaded == ref.counters.kv_floats_loaded
+            if it % 2 == 0:  # a plain host step between peer calls
+                again = P.routed_decode_step(q, 0, cache, cfg)
+                assert np.abs(again.outputs - ref.outputs).max() <= 1e-6
+            else:  # a device-buffer peer step between host peer calls
+                dout.fill_(float("nan"))
+                pm.step(dq, dout, cfg, P.EngineOptions())
+                torch.cuda.synchronize()
+                assert (dout.cpu().numpy() - ref.outputs).__abs__().max() <= 1e-6
