@@ -14,6 +14,11 @@
 //   threshold_for_length, route,    router.hpp:47-54,78   same
 //   auto_num_splits
 //   split_ranges                    attention.hpp:82-85   same
+//   QueryGroup, SplitPartial        attention.hpp:14-33   same names, same fields
+//   attend_chunk, merge_partials,   attention.hpp:38-85   same signatures over host spans
+//   splitk_attention, dense_/       (span overloads)      (GPU span kernels, fp64 state);
+//   online_attention                                      + overloads over a cached group
+//   ThreadPool                      parallel.hpp:20-44    accepted and unused (the GPU splits)
 //   routed_decode_step              router.hpp:84-86      same signature
 //   KvCache::save/load_snapshot     kv_cache.hpp:72-80    same (SNKT + manifest.json)
 //   calibration / analysis APIs     calibration.hpp, analysis.hpp -> sinkr/cuda/calibration.hpp,
@@ -25,7 +30,9 @@
 // by replacing `sinkr::` with `sinkr::cuda::` and linking libsinkr_cuda.so.
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstddef>
 #include <filesystem>
 #include <cstdint>
@@ -310,6 +317,154 @@ inline std::vector<float> online_attention(const KvCache& cache, std::span<const
                                            std::size_t seq = 0) {
     if (block_size == 0) throw std::invalid_argument("block_size must be positive");
     return splitk_attention(cache, group_q, layer, kv_head, 1, seq).out;
+}
+
+// ---- span-level operators (attention.hpp:14-85) ------------------------------
+// QueryGroup / SplitPartial with the reference's fields; the operators run on
+// the GPU of the calling thread (include/sinkr_cuda.h, span section).
+
+struct QueryGroup {  // attention.hpp:14-21
+    std::span<const float> q;
+    std::size_t heads = 0;
+    std::size_t dim = 0;
+    float scale = 0.0f;
+
+    static QueryGroup over(std::span<const float> q, std::size_t heads, std::size_t dim) {
+        QueryGroup qg{q, heads, dim, 0.0f};  // attention.cpp:33-40
+        if (dim == 0) throw std::invalid_argument("head_dim must be positive");
+        qg.scale = 1.0f / std::sqrt(static_cast<float>(dim));
+        if (q.size() != heads * dim)
+            throw std::invalid_argument("query span size does not match heads x dim");
+        return qg;
+    }
+};
+
+struct SplitPartial {  // attention.hpp:26-33
+    std::vector<double> m;    // heads
+    std::vector<double> l;    // heads
+    std::vector<double> acc;  // heads x dim
+    std::size_t tokens = 0;
+
+    bool empty() const { return tokens == 0; }
+};
+
+// The reference's CPU pool (parallel.hpp).  Accepted where the reference takes
+// a ThreadPool*, so callers compile unchanged; the split itself runs on the GPU.
+class ThreadPool {
+public:
+    explicit ThreadPool(std::size_t threads = 0) : n_(threads ? threads : 1) {}
+    std::size_t size() const { return n_; }
+
+private:
+    std::size_t n_;
+};
+
+namespace detail {
+// attention.cpp:13-23 (span sizes are only known on this side of the C-ABI)
+inline void check_shapes(const QueryGroup& qg, std::span<const float> keys,
+                         std::span<const float> values, std::size_t len, bool with_values) {
+    if (qg.heads == 0 || qg.dim == 0) throw std::invalid_argument("empty query group");
+    if (qg.q.size() != qg.heads * qg.dim)
+        throw std::invalid_argument("query span size does not match heads x dim");
+    if (len == 0) throw std::invalid_argument("attention needs at least one token");
+    if (keys.size() != len * qg.dim)
+        throw std::invalid_argument("key span size does not match len x dim");
+    if (with_values && values.size() != len * qg.dim)
+        throw std::invalid_argument("value span size does not match len x dim");
+}
+}  // namespace detail
+
+// attend_chunk (attention.hpp:55-60): the chunk's fp64 online-softmax state.
+inline SplitPartial attend_chunk(const QueryGroup& qg, std::span<const float> keys,
+                                 std::span<const float> values, std::size_t len,
+                                 std::size_t block_size = kDefaultBlockSize) {
+    detail::check_shapes(qg, keys, values, len, true);
+    SplitPartial p;
+    p.m.resize(qg.heads);
+    p.l.resize(qg.heads);
+    p.acc.resize(qg.heads * qg.dim);
+    std::uint64_t tok = 0;
+    check(sinkr_attend_chunk(qg.q.data(), qg.heads, qg.dim, keys.data(), values.data(), len,
+                             block_size, p.m.data(), p.l.data(), p.acc.data(), &tok));
+    p.tokens = tok;
+    return p;
+}
+
+// attend_chunk over the cached rows [from, to) of one group (historical +
+// attend_chunk, router.cpp:149-160), read in place from HBM.
+inline SplitPartial attend_chunk(const KvCache& cache, std::span<const float> group_q,
+                                 std::size_t layer, std::size_t kv_head, std::size_t from,
+                                 std::size_t to, std::size_t seq = 0,
+                                 std::size_t block_size = kDefaultBlockSize) {
+    const CacheConfig& cc = cache.config();
+    const std::size_t r = cc.group_width(), d = cc.head_dim;
+    if (group_q.size() != r * d) throw std::invalid_argument("query span size does not match heads x dim");
+    SplitPartial p;
+    p.m.resize(r);
+    p.l.resize(r);
+    p.acc.resize(r * d);
+    std::uint64_t tok = 0;
+    check(sinkr_attend_chunk_cached(cache.handle(), group_q.data(), seq, layer, kv_head, from, to,
+                                    block_size, p.m.data(), p.l.data(), p.acc.data(), &tok));
+    p.tokens = tok;
+    return p;
+}
+
+// merge_partials (attention.hpp:62-64): LSE combine on the GPU.
+inline std::vector<float> merge_partials(std::span<const SplitPartial> parts, std::size_t heads,
+                                         std::size_t dim) {
+    std::vector<double> m(parts.size() * heads), l(m.size()), acc(m.size() * dim);
+    std::vector<std::uint64_t> tok(parts.size());
+    for (std::size_t i = 0; i < parts.size(); ++i) {
+        const SplitPartial& p = parts[i];
+        tok[i] = p.tokens;
+        if (p.empty()) continue;
+        if (p.m.size() != heads || p.l.size() != heads || p.acc.size() != heads * dim)
+            throw std::invalid_argument("partial shape does not match heads x dim");
+        std::copy(p.m.begin(), p.m.end(), m.begin() + i * heads);
+        std::copy(p.l.begin(), p.l.end(), l.begin() + i * heads);
+        std::copy(p.acc.begin(), p.acc.end(), acc.begin() + i * heads * dim);
+    }
+    std::vector<float> out(heads * dim);
+    check(sinkr_merge_partials(parts.size(), m.data(), l.data(), acc.data(), tok.data(), heads,
+                               dim, out.data()));
+    return out;
+}
+
+// splitk_attention (attention.hpp:76-85) over host spans.
+inline SplitkResult splitk_attention(const QueryGroup& qg, std::span<const float> keys,
+                                     std::span<const float> values, std::size_t len,
+                                     std::size_t num_splits, ThreadPool* pool = nullptr,
+                                     std::size_t block_size = kDefaultBlockSize) {
+    (void)pool;
+    detail::check_shapes(qg, keys, values, len, true);
+    SplitkResult res;
+    res.out.resize(qg.heads * qg.dim);
+    sinkr_load_counters ctr{};
+    check(sinkr_splitk_attention(qg.q.data(), qg.heads, qg.dim, keys.data(), values.data(), len,
+                                 num_splits, block_size, res.out.data(), &ctr));
+    res.counters.kv_floats_loaded = ctr.kv_floats_loaded;
+    return res;
+}
+
+// dense_attention / online_attention (attention.hpp:38-53) over host spans.
+inline std::vector<float> dense_attention(const QueryGroup& qg, std::span<const float> keys,
+                                          std::span<const float> values, std::size_t len) {
+    detail::check_shapes(qg, keys, values, len, true);
+    std::vector<float> out(qg.heads * qg.dim);
+    check(sinkr_dense_attention(qg.q.data(), qg.heads, qg.dim, keys.data(), values.data(), len,
+                                out.data()));
+    return out;
+}
+
+inline std::vector<float> online_attention(const QueryGroup& qg, std::span<const float> keys,
+                                           std::span<const float> values, std::size_t len,
+                                           std::size_t block_size = kDefaultBlockSize) {
+    detail::check_shapes(qg, keys, values, len, true);
+    std::vector<float> out(qg.heads * qg.dim);
+    check(sinkr_online_attention(qg.q.data(), qg.heads, qg.dim, keys.data(), values.data(), len,
+                                 block_size, out.data()));
+    return out;
 }
 
 // router.hpp:84-86 — one decode step for one layer (all B sequences).

@@ -358,6 +358,62 @@ sinkr_status sinkr_group_attention(sinkr_engine* e, const float* group_queries, 
                                    size_t layer, size_t kv_head, size_t num_splits, float* out,
                                    sinkr_load_counters* counters);
 
+/* ---- span-level attention operators (attention.hpp:14-85) -------------------
+ * The reference's free functions over host spans, on the GPU of the calling
+ * thread (current device; a per-device context serialised by a mutex; each
+ * call blocks until its results are in host memory).  q is [heads][dim] f32,
+ * keys / values [len][dim] f32; the logit scale is QueryGroup::over's
+ * 1/sqrt(dim) (attention.cpp:33-40).  Arithmetic is the reference's: logits
+ * are fp64 sequential dots of exact f32 products (bit-identical), the softmax
+ * state m, l, acc is fp64 (SplitPartial, attention.hpp:26-33).  Errors follow
+ * check_shapes (attention.cpp:13-23): INVALID_ARGUMENT for heads/dim 0, len 0,
+ * block_size 0, num_splits outside [1, len]; head_dim is limited to 8192.
+ * Spans are transfer-bound (uploaded per call); the decode hot path streams
+ * the engine's cache instead (sinkr_routed_decode_*). */
+/* attend_chunk (attention.hpp:55-60, attention.cpp:101-142): the chunk's
+ * SplitPartial: m[heads], l[heads], acc[heads][dim] (fp64, caller-owned),
+ * *tokens = len (may be NULL).  block_size is validated (> 0); the GPU tiles
+ * the chunk itself (state equal up to fp64 rounding). */
+sinkr_status sinkr_attend_chunk(const float* q, size_t heads, size_t dim, const float* keys,
+                                const float* values, size_t len, size_t block_size, double* m,
+                                double* l, double* acc, uint64_t* tokens);
+/* attend_chunk over the cached rows [from, to) of (seq, layer, kv_head) of an
+ * engine (KvCache::historical + attend_chunk, router.cpp:149-160) with the
+ * group's r query heads: OUT_OF_RANGE past the slot's length
+ * (kv_cache.cpp:110-113), INVALID_ARGUMENT for an empty range. */
+sinkr_status sinkr_attend_chunk_cached(sinkr_engine* e, const float* group_queries, size_t seq,
+                                       size_t layer, size_t kv_head, size_t from, size_t to,
+                                       size_t block_size, double* m, double* l, double* acc,
+                                       uint64_t* tokens);
+/* merge_partials (attention.hpp:62-64, attention.cpp:159-183) of n host
+ * SplitPartials packed as m[n][heads], l[n][heads], acc[n][heads][dim],
+ * tokens[n]: partials with tokens == 0 are skipped; INVALID_ARGUMENT ("merge
+ * needs at least one non-empty partial") when all are empty.  out [heads][dim]. */
+sinkr_status sinkr_merge_partials(size_t n, const double* m, const double* l, const double* acc,
+                                  const uint64_t* tokens, size_t heads, size_t dim, float* out);
+/* The same merge as a device kernel on `stream` (cudaStream_t) over device
+ * buffers of that layout (d_tokens may be NULL: all live); does not check for
+ * the all-empty case (the host entry does). */
+sinkr_status sinkr_merge_partials_async(size_t n, const double* d_m, const double* d_l,
+                                        const double* d_acc, const uint64_t* d_tokens, size_t heads,
+                                        size_t dim, float* d_out, void* stream);
+/* splitk_attention (attention.hpp:76-85, attention.cpp:204-235): split_ranges
+ * chunks, one attend_chunk partial each, one merge; counters->kv_floats_loaded
+ * = 2 * len * dim (other fields 0; may be NULL). */
+sinkr_status sinkr_splitk_attention(const float* q, size_t heads, size_t dim, const float* keys,
+                                    const float* values, size_t len, size_t num_splits,
+                                    size_t block_size, float* out, sinkr_load_counters* counters);
+/* online_attention (attention.hpp:48-53, attention.cpp:144-157): acc / l of
+ * one attend_chunk over the whole span. */
+sinkr_status sinkr_online_attention(const float* q, size_t heads, size_t dim, const float* keys,
+                                    const float* values, size_t len, size_t block_size, float* out);
+/* dense_attention (attention.hpp:38-42, attention.cpp:42-73): the reference's
+ * two-pass exact softmax; computed here as one fp64 online pass, which equals
+ * it up to fp64 rounding (the reference's own online-vs-dense bar is 1e-5,
+ * SPEC.md:231). */
+sinkr_status sinkr_dense_attention(const float* q, size_t heads, size_t dim, const float* keys,
+                                   const float* values, size_t len, float* out);
+
 /* ---- analysis (attention.cpp:75-99, analysis.hpp:12-39) ---
  * Full-attention BOS mass on the GPU for oracle sink labels: for every query
  * head, alpha0 = softmax(scale * q.K^T)[0] over the whole cached context of

@@ -36,6 +36,13 @@ from .router import (  # noqa: F401
     SplitkResult,
     threshold_for_length,
 )
+from .attention import (  # noqa: F401
+    QueryGroup,
+    SplitPartial,
+    attend_chunk,
+    attend_chunk_cached,
+    merge_partials,
+)
 from .workload import WorkloadSpec  # noqa: F401
 
 __version__ = "0.1.0"

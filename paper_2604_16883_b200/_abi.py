@@ -113,6 +113,10 @@ EXPORTS = (
     # fused sequence-sharded peer merge
     "sinkr_peer_setup", "sinkr_peer_ipc_handle", "sinkr_peer_open", "sinkr_peer_set_blocks",
     "sinkr_peer_block", "sinkr_routed_decode_peer_async",
+    # span-level attention operators (attention.hpp:14-85)
+    "sinkr_attend_chunk", "sinkr_attend_chunk_cached", "sinkr_merge_partials",
+    "sinkr_merge_partials_async", "sinkr_splitk_attention", "sinkr_online_attention",
+    "sinkr_dense_attention",
 )
 
 _lib = None
@@ -178,6 +182,13 @@ def lib():
             "sinkr_peer_open": [vp, vp],
             "sinkr_peer_set_blocks": [vp, vp],
             "sinkr_routed_decode_peer_async": [vp, vp, sz, vp, vp, vp],
+            "sinkr_attend_chunk": [vp, sz, sz, vp, vp, sz, sz, vp, vp, vp, vp],
+            "sinkr_attend_chunk_cached": [vp, vp, sz, sz, sz, sz, sz, sz, vp, vp, vp, vp],
+            "sinkr_merge_partials": [sz, vp, vp, vp, vp, sz, sz, vp],
+            "sinkr_merge_partials_async": [sz, vp, vp, vp, vp, sz, sz, vp, vp],
+            "sinkr_splitk_attention": [vp, sz, sz, vp, vp, sz, sz, sz, vp, vp],
+            "sinkr_online_attention": [vp, sz, sz, vp, vp, sz, sz, vp],
+            "sinkr_dense_attention": [vp, sz, sz, vp, vp, sz, vp],
         }.items():
             getattr(L, name).argtypes = at
             getattr(L, name).restype = C.c_int if name != "sinkr_profile_default" else None

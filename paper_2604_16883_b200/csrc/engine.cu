@@ -24,6 +24,7 @@
 #include "host_util.hpp"
 #include "step.cuh"
 #include "analysis.cuh"
+#include "span.hpp"
 
 namespace {
 
@@ -136,6 +137,8 @@ struct sinkr_engine {
     uint32_t* d_cursor = nullptr;
     uint32_t* d_tokens_done = nullptr;
     uint32_t* d_route_flags = nullptr;  // distributed routing decisions [U]
+    uint8_t* d_span = nullptr;           // attend_chunk over a cached range: q | partial | scratch
+    size_t span_bytes = 0;
     uint8_t* d_bos = nullptr;            // analysis scratch (run_bos), grown on demand
     size_t bos_bytes = 0;
     uint8_t* h_bos = nullptr;            // pinned + mapped staging for run_bos (prefix up, alpha0 down)
@@ -915,6 +918,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_tokens_done);
     cudaFree(e->d_route_flags);
     cudaFree(e->d_bos);
+    cudaFree(e->d_span);
     for (void* pb : e->ipc_opened) cudaIpcCloseMemHandle(pb);
     cudaFree(e->d_xchg);
     cudaFree(e->d_peer_xchg);
@@ -1322,6 +1326,54 @@ sinkr_status sinkr_group_attention(sinkr_engine* e, const float* group_queries, 
             *counters = sinkr_load_counters{};
             counters->kv_floats_loaded = 2ull * L * D;  // attention.cpp:219
         }
+    });
+}
+
+// attend_chunk (attention.cpp:101-142) of one group's r query heads over the
+// cached rows [from, to) of (seq, layer, kv_head) -- the reference's
+// run_task pairing of KvCache::historical (kv_cache.cpp:106-121) with
+// attend_chunk (router.cpp:149-160) -- returning the chunk's SplitPartial
+// (fp64 m[r], l[r], acc[r][D]; tokens = to - from).  The span kernel
+// (span.cuh) reads the bf16 rows in place on the engine stream.
+sinkr_status sinkr_attend_chunk_cached(sinkr_engine* e, const float* group_queries, size_t seq,
+                                       size_t layer, size_t kv_head, size_t from, size_t to,
+                                       size_t block_size, double* m, double* l, double* acc,
+                                       uint64_t* tokens) {
+    return guard([&] {
+        if (!e || !group_queries || !m || !l || !acc) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        check_slot(e, seq, layer, kv_head);
+        const size_t idx = e->slot_index(layer, seq, kv_head), D = e->D, r = e->r;
+        if (from > to || to > e->len[idx])
+            fail(SINKR_OUT_OF_RANGE, "historical range [" + std::to_string(from) + ", " +
+                                         std::to_string(to) + ") exceeds length " +
+                                         std::to_string(e->len[idx]));
+        if (to == from) fail(SINKR_INVALID_ARGUMENT, "attention needs at least one token");
+        if (block_size == 0) fail(SINKR_INVALID_ARGUMENT, "block_size must be positive");
+        const size_t len = to - from;
+        const size_t qb = align_up(r * D * 4, 256), pb = align_up(r * (D + 2) * 8, 256);
+        const size_t need = qb + pb + span::attend_scratch_bytes(r, D, len, e->num_sms);
+        if (e->span_bytes < need) {
+            CK(cudaStreamSynchronize(e->stream));
+            cudaFree(e->d_span);
+            e->d_span = nullptr;
+            e->span_bytes = 0;
+            CK(cudaMalloc(&e->d_span, need));
+            e->span_bytes = need;
+        }
+        float* d_q = reinterpret_cast<float*>(e->d_span);
+        double* d_m = reinterpret_cast<double*>(e->d_span + qb);
+        double* d_l = d_m + r;
+        double* d_acc = d_l + r;
+        CK(cudaMemcpyAsync(d_q, group_queries, r * D * 4, cudaMemcpyHostToDevice, e->stream));
+        const size_t off = (e->row_base(layer, seq, kv_head) + from) * D;
+        span::attend_device(e->stream, d_q, r, D, e->d_k + off, e->d_v + off, len, e->d_span + qb + pb,
+                            d_m, d_l, d_acc, e->num_sms);
+        CK(cudaMemcpyAsync(m, d_m, r * 8, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaMemcpyAsync(l, d_l, r * 8, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaMemcpyAsync(acc, d_acc, r * D * 8, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        if (tokens) *tokens = len;
     });
 }
 

@@ -404,12 +404,23 @@ class SplitkResult:
     counters: LoadCounters
 
 
-def splitk_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
-                     num_splits: int, seq: int = 0) -> SplitkResult:
+def splitk_attention(cache, group_queries, layer=None, kv_head=None,
+                     num_splits=1, seq=0, **kw) -> SplitkResult:
     """splitk_attention (attention.cpp:204-235) of one cached group on the GPU:
     the group's r query heads over all of its cached rows.  num_splits is
     validated like split_ranges; the kernel picks its own split.  Replaces the
-    engine's last routing record."""
+    engine's last routing record.
+
+    Called with a QueryGroup (or a [heads, dim] array) and host K/V spans
+    instead of a KvCache, this is the reference's span overload
+    (attention.hpp:76-85): see attention.splitk_attention."""
+    if not isinstance(cache, KvCache):
+        from . import attention as _A
+
+        # (qg, keys, values, len, num_splits, pool, block_size)
+        return _A.splitk_attention(cache, group_queries, layer, kv_head, num_splits, seq, **kw)
+    if layer is None or kv_head is None:
+        raise TypeError("splitk_attention(cache, group_queries, layer, kv_head, num_splits, ...)")
     cc = cache.config()
     r = cc.num_q_heads // cc.num_kv_heads
     q = np.ascontiguousarray(group_queries, dtype=np.float32)
@@ -424,18 +435,34 @@ def splitk_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
     return SplitkResult(out=out, counters=LoadCounters(int(ctr.kv_floats_loaded)))
 
 
-def dense_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
+def dense_attention(cache, group_queries, layer=None, kv_head=None,
                     seq: int = 0) -> np.ndarray:
     """dense_attention (attention.cpp:42-73) of one cached group: [r, D] f32
-    (the GPU group attention; exact softmax to fp32 accumulation)."""
+    (the GPU group attention; exact softmax to fp32 accumulation).  With a
+    QueryGroup / array and host spans (qg, keys, values[, len]): the span
+    overload (attention.dense_attention)."""
+    if not isinstance(cache, KvCache):
+        from . import attention as _A
+
+        return _A.dense_attention(cache, group_queries, layer, kv_head)
+    if layer is None or kv_head is None:
+        raise TypeError("dense_attention(cache, group_queries, layer, kv_head, ...)")
     return splitk_attention(cache, group_queries, layer, kv_head, 1, seq).out
 
 
-def online_attention(cache: KvCache, group_queries, layer: int, kv_head: int,
+def online_attention(cache, group_queries, layer=None, kv_head=None,
                      block_size: int = kDefaultBlockSize, seq: int = 0) -> np.ndarray:
     """online_attention (attention.cpp:144-157) of one cached group: [r, D] f32.
     block_size is validated like attend_chunk (attention.cpp:107); the GPU
-    streams in its own 64-token stages."""
+    streams in its own 64-token stages.  With a QueryGroup / array and host
+    spans (qg, keys, values[, len[, block_size]]): the span overload
+    (attention.online_attention)."""
+    if not isinstance(cache, KvCache):
+        from . import attention as _A
+
+        return _A.online_attention(cache, group_queries, layer, kv_head, block_size)
+    if layer is None or kv_head is None:
+        raise TypeError("online_attention(cache, group_queries, layer, kv_head, ...)")
     if block_size == 0:
         raise ValueError("block_size must be positive")
     return splitk_attention(cache, group_queries, layer, kv_head, 1, seq).out

@@ -116,6 +116,53 @@ int main() {
         sc::splitk_attention(cache, std::span<const float>(q.data(), 4 * D), 1, 0, 0);
     }));
 
+    // attention.hpp:14-85 over host spans, as a reference caller writes it
+    std::fprintf(stderr, "span operators\n");
+    {
+        const std::size_t n = 1500, d = 80, h = 3;
+        std::vector<float> kk(n * d), vv(n * d), qq(h * d);
+        for (auto& x : kk) x = n01(rng);
+        for (auto& x : vv) x = n01(rng);
+        for (auto& x : qq) x = 2.0f * n01(rng);
+        const auto qg = sc::QueryGroup::over(qq, h, d);
+        REQUIRE(qg.scale == 1.0f / std::sqrt(80.0f));
+        sc::ThreadPool pool(4);
+        const auto spk = sc::splitk_attention(qg, kk, vv, n, 3, &pool);
+        REQUIRE(spk.counters.kv_floats_loaded == 2 * n * d);
+        const auto on = sc::online_attention(qg, kk, vv, n);
+        const auto de = sc::dense_attention(qg, kk, vv, n);
+        std::vector<sc::SplitPartial> parts;
+        for (auto [a, b] : sc::split_ranges(n, 4))
+            parts.push_back(sc::attend_chunk(qg, std::span<const float>(kk).subspan(a * d, (b - a) * d),
+                                             std::span<const float>(vv).subspan(a * d, (b - a) * d), b - a));
+        parts.insert(parts.begin() + 1, sc::SplitPartial{});  // empty: skipped by the merge
+        REQUIRE(parts[0].tokens == 375 && parts[0].m.size() == h && parts[0].acc.size() == h * d);
+        const auto mg = sc::merge_partials(parts, h, d);
+        float dm = 0.0f;
+        for (std::size_t i = 0; i < h * d; ++i) {
+            dm = std::fmax(dm, std::fabs(mg[i] - spk.out[i]));
+            dm = std::fmax(dm, std::fabs(on[i] - de[i]));
+            dm = std::fmax(dm, std::fabs(on[i] - spk.out[i]));
+        }
+        REQUIRE(dm <= 1e-6f);
+        std::vector<sc::SplitPartial> none(2);
+        REQUIRE(throws<std::invalid_argument>([&] { sc::merge_partials(none, h, d); }));
+        REQUIRE(throws<std::invalid_argument>([&] { sc::attend_chunk(qg, kk, vv, n, 0); }));
+        REQUIRE(throws<std::invalid_argument>([&] { sc::splitk_attention(qg, kk, vv, n, 0); }));
+        REQUIRE(throws<std::invalid_argument>([&] {
+            sc::dense_attention(qg, std::span<const float>(kk).first(d * 3), vv, n);
+        }));
+        // attend_chunk over a cached range == over the same rows as a span
+        const auto [hk, hv] = cache.historical(1, 2, 100, 600);
+        const std::span<const float> gq(q.data() + 8 * D, 4 * D);
+        const auto pc = sc::attend_chunk(cache, gq, 1, 2, 100, 600);
+        const auto ps = sc::attend_chunk(sc::QueryGroup::over(gq, 4, D), hk, hv, 500);
+        REQUIRE(pc.tokens == 500 && pc.m == ps.m);  // logits are bit-exact: maxima equal
+        for (std::size_t i = 0; i < 4 * D; ++i)
+            REQUIRE(std::fabs(pc.acc[i] - ps.acc[i]) <= 1e-12 * (1.0 + std::fabs(ps.acc[i])));
+        REQUIRE(throws<std::out_of_range>([&] { sc::attend_chunk(cache, gq, 1, 2, 100, L + 1); }));
+    }
+
     // analysis.hpp: GPU BOS mass, oracle labels, PR curve
     const auto a0 = sc::attention_bos_mass(cache, q, 1);
     for (double a : a0) REQUIRE(a > 0.0 && a < 1.0);
