@@ -197,6 +197,27 @@ sinkr_status sinkr_routed_decode_batch(sinkr_engine* e, const float* queries, si
                                        sinkr_group_info* groups, double* head_scores,
                                        sinkr_load_counters* counters);
 
+/* The decode loop's append (KvCache::append, kv_cache.cpp:61-84):
+ * ONE new token's K/V row to every (seq, kv_head) slot of `layer`.
+ *   _async: d_k_new / d_v_new are device f32 [B][H_kv][D]; one kernel enqueued
+ *           on the engine stream, no host sync (a slot's FIRST row takes the
+ *           synchronous host path: anchor capture + degenerate check).
+ *   sinkr_decode_append_step: host rows k_new / v_new, then the routed step of
+ *           that layer over the grown cache -- one graph per call (H2D of
+ *           params + queries + rows, append kernel, step kernel, results
+ *           zero-copy), blocking like sinkr_routed_decode_batch.
+ * Overflow -> RUNTIME_ERROR ("kv cache overflow"); as token_count requires
+ * (kv_cache.cpp:90-96), a sequence's slots must be uniform after the append
+ * for the step (LOGIC_ERROR otherwise, nothing appended). */
+sinkr_status sinkr_kv_append_token_async(sinkr_engine* e, size_t layer, const float* d_k_new,
+                                         const float* d_v_new);
+sinkr_status sinkr_decode_append_step(sinkr_engine* e, const float* queries, const float* k_new,
+                                      const float* v_new, size_t layer,
+                                      const sinkr_routing_config* config,
+                                      const sinkr_engine_options* options, float* outputs,
+                                      sinkr_group_info* groups, double* head_scores,
+                                      sinkr_load_counters* counters);
+
 /* Device-resident variant: d_queries / d_outputs are device pointers; the
  * call only enqueues work on the engine stream (no host sync).  Routing
  * results stay on the device until sinkr_fetch_step_info (which syncs). */

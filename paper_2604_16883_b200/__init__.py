@@ -7,6 +7,7 @@ reference interface (``router.py``), the synthetic planted-sink workload
 (``workload.py``) and the multi-GPU plumbing (``sharding.py``).
 """
 from .router import (  # noqa: F401
+    AppendStepRunner,
     CacheConfig,
     EngineOptions,
     GroupStepInfo,

@@ -117,6 +117,8 @@ EXPORTS = (
     "sinkr_attend_chunk", "sinkr_attend_chunk_cached", "sinkr_merge_partials",
     "sinkr_merge_partials_async", "sinkr_splitk_attention", "sinkr_online_attention",
     "sinkr_dense_attention",
+    # per-token append (the decode loop's KvCache::append)
+    "sinkr_kv_append_token_async", "sinkr_decode_append_step",
 )
 
 _lib = None
@@ -189,6 +191,8 @@ def lib():
             "sinkr_splitk_attention": [vp, sz, sz, vp, vp, sz, sz, sz, vp, vp],
             "sinkr_online_attention": [vp, sz, sz, vp, vp, sz, sz, vp],
             "sinkr_dense_attention": [vp, sz, sz, vp, vp, sz, vp],
+            "sinkr_kv_append_token_async": [vp, sz, vp, vp],
+            "sinkr_decode_append_step": [vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, vp],
         }.items():
             getattr(L, name).argtypes = at
             getattr(L, name).restype = C.c_int if name != "sinkr_profile_default" else None

@@ -274,6 +274,18 @@ def cmd_selftest(args) -> int:
     from . import calibration as cal
 
     failures = []
+    # fault injection: the reference's tie-breaking test hook
+    # (RoutingConfig::sink_on_tie, router.hpp:20-22) forced on in every routing
+    # config the suite builds; the routing-semantics check must then fail
+    fault = bool(getattr(args, "inject_tie_fault", False)) or \
+        os.environ.get("SINKR_INJECT_TIE_FAULT", "") == "1"
+    if fault:
+        print("fault injection: sink_on_tie forced on (routing semantics must fail)")
+
+    def rc(**kw):
+        c = P.RoutingConfig(**kw)
+        c.sink_on_tie = c.sink_on_tie or fault
+        return c
 
     def expect(name, ok):
         print(f"{'PASS' if ok else 'FAIL'}  {name}")
@@ -287,9 +299,9 @@ def cmd_selftest(args) -> int:
             spec.fill(cache)
         spec.layer = 2
         q = spec.queries()[0]
-        cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5))
+        cfg = rc(profile=P.ThresholdProfile.constant(0.5))
         res = P.routed_decode_step(q, 2, cache, cfg)
-        dense = P.routed_decode_step(q, 2, cache, P.RoutingConfig(profile=P.ThresholdProfile.constant(2.0)))
+        dense = P.routed_decode_step(q, 2, cache, rc(profile=P.ThresholdProfile.constant(2.0)))
         r = args.hq // args.hkv
         sinks = [g.decision.sink for g in res.groups]
         expect("planted groups route Sink", sinks == spec.sink_groups(0).tolist())
@@ -307,19 +319,22 @@ def cmd_selftest(args) -> int:
         expect("skipped-block record (kv_floats 0 or 2LD)", ok_cnt)
         ex = P.routed_decode_step(q, 0, cache, cfg)
         expect("excluded layers never skip", ex.counters.groups_skipped == 0)
-        ties = P.RoutingConfig(profile=P.ThresholdProfile.constant(res.groups[0].decision.group_score),
-                               excluded_layers=())
+        # an exact tie S == tau (router.cpp:67-75): strict >, so Active
+        ties = rc(profile=P.ThresholdProfile.constant(res.groups[0].decision.group_score),
+                  excluded_layers=())
         t0 = P.routed_decode_step(q, 2, cache, ties).groups[0].decision.sink
-        ties.sink_on_tie = True
-        t1 = P.routed_decode_step(q, 2, cache, ties).groups[0].decision.sink
-        expect("tie routes Active; sink_on_tie fault hook flips it", (not t0) and t1)
+        expect("routing semantics: an exact tie routes Active (strict >)", not t0)
+        hook = rc(profile=P.ThresholdProfile.constant(res.groups[0].decision.group_score),
+                  excluded_layers=())
+        hook.sink_on_tie = True
+        t1 = P.routed_decode_step(q, 2, cache, hook).groups[0].decision.sink
+        expect("sink_on_tie test hook flips the tie to Sink", t1)
     outs = []
     for L in (1000, 3000):
         s2 = _spec(args, L, 0.0, args.seed)
         with P.KvCache(P.CacheConfig(1, args.hq, args.hkv, args.dim, L)) as c:
             s2.fill(c)
-            o = P.routed_decode_step(s2.queries()[0], 0, c,
-                                     P.RoutingConfig(profile=P.ThresholdProfile.constant(2.0)))
+            o = P.routed_decode_step(s2.queries()[0], 0, c, rc(profile=P.ThresholdProfile.constant(2.0)))
             outs.append(np.isfinite(o.outputs).all() and o.counters.groups_active == args.hkv)
     expect("dense steps finite at several lengths", all(outs))
     prof = P.ThresholdProfile(coeffs=(0.1, -0.2, 0.3, 0.5), length_normalizer=65536.0)
@@ -367,6 +382,9 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--samples", type=int, default=4)
     p = sub.add_parser("selftest")
     common(p)
+    p.add_argument("--inject-tie-fault", action="store_true",
+                   help="force the sink_on_tie hook on (SPEC.md:610): the suite must report a "
+                        "routing-semantics failure and exit 1")
     return ap
 
 

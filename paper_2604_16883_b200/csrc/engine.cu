@@ -109,8 +109,15 @@ struct sinkr_engine {
     std::vector<float> h_anchor, h_anchor_norm;
     std::vector<uint8_t> anchored;
 
-    // step input block: hdr | tau[B] | len[B] | q[B][Hq][D]
+    // step input block: hdr | tau[B] | len[B] | q[B][Hq][D] | k_new, v_new [B][Hkv][D]
+    // (the new-token rows only travel with sinkr_decode_append_step)
     size_t off_tau = 0, off_len = 0, off_q = 0, in_bytes = 0;
+    size_t off_kvn = 0, in_bytes_append = 0;
+    // device copy of the slot lengths, advanced by append_token_kernel; the
+    // host paths mark it stale and the next token append re-uploads it
+    uint32_t* d_len = nullptr;
+    uint32_t* h_len_stage = nullptr;  // pinned
+    bool dlen_dirty = true;
     uint8_t* d_in = nullptr;
     uint8_t* h_in = nullptr;
     // step result block: out | head_scores | group_scores | tokens | flags
@@ -477,10 +484,20 @@ static int io_mode() {
     return m;
 }
 
-void run_io_graph(sinkr_engine* e, int mode = 0) {
-    e->last_launches = 1;
+void launch_append(sinkr_engine* e, size_t layer, const float* dk, const float* dv) {
+    dev::append_token_kernel<<<(unsigned)e->U, (unsigned)std::min<size_t>(e->D, 128), 0, e->stream>>>(
+        dk, dv, e->d_k, e->d_v, e->d_len, (uint32_t)(layer * e->U), (uint32_t)e->D, (uint32_t)e->cap);
+    CK(cudaGetLastError());
+}
+
+// append_layer >= 0: the graph also carries the new token's K/V rows (staged
+// after the queries) and appends them to every slot of that layer before
+// the step (sinkr_decode_append_step)
+void run_io_graph(sinkr_engine* e, int mode = 0, long append_layer = -1) {
+    e->last_launches = append_layer >= 0 ? 2 : 1;
     e->last_mode = mode;
-    const auto key = std::make_tuple((const void*)e->h_in, (void*)e->h_res, mode == 3 ? 6 : 2);
+    const int code = (mode == 3 ? 6 : 2) + (append_layer >= 0 ? 1000 + 16 * (int)append_layer : 0);
+    const auto key = std::make_tuple((const void*)e->h_in, (void*)e->h_res, code);
     auto it = e->graphs.find(key);
     const float* d_q = reinterpret_cast<const float*>(e->d_in + e->off_q);
     const bool zc = io_mode() == 1;
@@ -490,7 +507,12 @@ void run_io_graph(sinkr_engine* e, int mode = 0) {
         sinkr_engine::GraphEntry ge;
         CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
         try {
-            CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
+            CK(cudaMemcpyAsync(e->d_in, e->h_in, append_layer >= 0 ? e->in_bytes_append : e->in_bytes,
+                               cudaMemcpyHostToDevice, e->stream));
+            if (append_layer >= 0) {
+                const float* kn = reinterpret_cast<const float*>(e->d_in + e->off_kvn);
+                launch_append(e, (size_t)append_layer, kn, kn + e->U * e->D);
+            }
             const bool timing = e->timing;
             e->timing = false;
             enqueue_step(e, d_q, out, mode, res, zc ? e->h_done_dev : nullptr);
@@ -508,11 +530,17 @@ void run_io_graph(sinkr_engine* e, int mode = 0) {
         CK(cudaGraphGetNodes(ge.graph, nullptr, &n));
         std::vector<cudaGraphNode_t> nodes(n);
         CK(cudaGraphGetNodes(ge.graph, nodes.data(), &n));
+        const void* step_fn = e->D == 32 ? (const void*)dev::step_kernel<32>
+                              : e->D == 64 ? (const void*)dev::step_kernel<64>
+                                           : (const void*)dev::step_kernel<128>;
         for (auto nd : nodes) {
             cudaGraphNodeType ty;
             CK(cudaGraphNodeGetType(nd, &ty));
             if (ty != cudaGraphNodeTypeKernel) continue;
-            CK(cudaGraphKernelNodeGetParams(nd, &ge.probe_kp));
+            cudaKernelNodeParams kp{};
+            CK(cudaGraphKernelNodeGetParams(nd, &kp));
+            if (kp.func != step_fn) continue;
+            ge.probe_kp = kp;
             ge.probe = nd;
         }
         if (!ge.probe) fail(SINKR_CUDA_ERROR, "step node not found in the captured graph");
@@ -568,6 +596,31 @@ size_t token_count(const sinkr_engine* e, size_t seq) {
             if (e->len[e->slot_index(l, seq, g)] != n)
                 fail(SINKR_LOGIC_ERROR, "kv cache lengths are ragged across slots");
     return n;
+}
+
+// Brings the device length table up to date after host-path appends (the
+// token-append kernel reads and advances it).  Host paths synchronise the
+// stream when they finish, so the pinned staging is free here.
+void sync_dlen(sinkr_engine* e) {
+    if (!e->dlen_dirty) return;
+    for (size_t i = 0; i < e->len.size(); ++i) e->h_len_stage[i] = (uint32_t)e->len[i];
+    CK(cudaMemcpyAsync(e->d_len, e->h_len_stage, e->len.size() * 4, cudaMemcpyHostToDevice, e->stream));
+    e->dlen_dirty = false;
+}
+
+// One new row for every (seq, kv_head) slot of `layer`: capacity checked
+// first (kv_cache.cpp:67-69); true when some slot is still empty (its first
+// row needs the host path: anchor capture + degenerate check).
+bool check_token_append(sinkr_engine* e, size_t layer) {
+    if (layer >= e->layers) fail(SINKR_OUT_OF_RANGE, "layer index out of range");
+    bool empty = false;
+    for (size_t u = 0; u < e->U; ++u) {
+        const size_t n = e->len[layer * e->U + u];
+        if (n + 1 > e->cap)
+            fail(SINKR_RUNTIME_ERROR, "kv cache overflow: slot at capacity " + std::to_string(e->cap));
+        empty |= n == 0;
+    }
+    return empty;
 }
 
 // Validates a step (router.cpp:85-90) and stages hdr / tau / len into the
@@ -781,9 +834,14 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->off_len = align_up(e->off_tau + 8 * e->B, 64);
             e->off_q = align_up(e->off_len + 4 * e->B, 128);
             e->in_bytes = e->off_q + e->B * Hq * e->D * 4;
-            CK(cudaMalloc(&e->d_in, e->in_bytes));
-            CK(cudaMallocHost(&e->h_in, e->in_bytes));
-            std::memset(e->h_in, 0, e->in_bytes);
+            e->off_kvn = align_up(e->in_bytes, 128);
+            e->in_bytes_append = e->off_kvn + 2 * e->U * e->D * 4;
+            CK(cudaMalloc(&e->d_in, e->in_bytes_append));
+            CK(cudaMallocHost(&e->h_in, e->in_bytes_append));
+            std::memset(e->h_in, 0, e->in_bytes_append);
+            CK(cudaMalloc(&e->d_len, slots * 4));
+            CK(cudaMemsetAsync(e->d_len, 0, slots * 4, e->stream));
+            CK(cudaMallocHost(&e->h_len_stage, slots * 4));
 
             e->off_hs = align_up(e->B * Hq * e->D * 4, 128);
             e->off_gs = align_up(e->off_hs + e->B * Hq * 8, 128);
@@ -932,6 +990,8 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     if (e->h_in) cudaFreeHost(e->h_in);
     if (e->h_res) cudaFreeHost(e->h_res);
     if (e->h_done) cudaFreeHost(e->h_done);
+    if (e->h_len_stage) cudaFreeHost(e->h_len_stage);
+    cudaFree(e->d_len);
     if (e->h_bos) cudaFreeHost(e->h_bos);
     for (auto ev : e->ev_bos)
         if (ev) cudaEventDestroy(ev);
@@ -981,6 +1041,7 @@ sinkr_status sinkr_kv_append(sinkr_engine* e, size_t seq, size_t layer, size_t k
                            e->stream));
         CK(cudaStreamSynchronize(e->stream));
         e->len[idx] += rows;
+        e->dlen_dirty = true;
     });
 }
 
@@ -1018,6 +1079,7 @@ sinkr_status sinkr_kv_append_device_bf16(sinkr_engine* e, size_t seq, size_t lay
         if (e->len[idx] == 0) capture_anchor_device(e, idx);
         CK(cudaStreamSynchronize(e->stream));
         e->len[idx] += rows;
+        e->dlen_dirty = true;
     });
 }
 
@@ -1044,6 +1106,7 @@ sinkr_status sinkr_kv_append_device_f32(sinkr_engine* e, size_t seq, size_t laye
         if (e->len[idx] == 0) capture_anchor_device(e, idx);
         CK(cudaStreamSynchronize(e->stream));
         e->len[idx] += rows;
+        e->dlen_dirty = true;
     });
 }
 
@@ -1078,6 +1141,7 @@ sinkr_status sinkr_kv_append_synthetic(sinkr_engine* e, size_t seq, size_t layer
         if (row0 == 0) capture_anchor_device(e, idx);
         CK(cudaStreamSynchronize(e->stream));
         e->len[idx] += rows;
+        e->dlen_dirty = true;
     });
 }
 
@@ -1259,6 +1323,92 @@ static void decode_host(sinkr_engine* e, const float* queries, size_t layer,
         if (outputs && outputs != reinterpret_cast<float*>(e->h_res)) std::memcpy(outputs, e->h_res, qbytes);
         fill_info(e, layer, config, groups, head_scores, counters, options);
     }
+}
+
+// ---- per-token KV append (kv_cache.cpp:61-84) ---------------------
+// The decode loop's append of the new token to every (seq, kv_head) slot of a
+// layer, stream-ordered on the engine stream: one small kernel, no host sync
+// (first rows of empty slots take the synchronous host path, which captures
+// the anchor and checks it like KvCache::append).
+sinkr_status sinkr_kv_append_token_async(sinkr_engine* e, size_t layer, const float* d_k_new,
+                                         const float* d_v_new) {
+    return guard([&] {
+        if (!e || !d_k_new || !d_v_new) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(e->device));
+        if (check_token_append(e, layer)) {
+            const size_t H = e->cfg.num_kv_heads;
+            for (size_t u = 0; u < e->U; ++u) {
+                const sinkr_status st = sinkr_kv_append_device_f32(e, u / H, layer, u % H, d_k_new + u * e->D,
+                                                                   d_v_new + u * e->D, 1);
+                if (st != SINKR_OK) fail(st, g_err);
+            }
+            return;
+        }
+        sync_dlen(e);
+        launch_append(e, layer, d_k_new, d_v_new);
+        for (size_t u = 0; u < e->U; ++u) ++e->len[layer * e->U + u];
+    });
+}
+
+// One decode step of `layer` that first appends the new token (host rows
+// k_new / v_new [B][H_kv][D] f32) to every slot of the layer and then runs the
+// routed step over the grown cache (the reference's append-then-step,
+// a Sink group skips the new row too).  One graph per call: H2D
+// of params + queries + new rows, the append kernel, the step kernel writing
+// zero-copy into pinned host memory.  As in the reference, the sequence's
+// slots must be uniform after the append (token_count, kv_cache.cpp:90-96).
+sinkr_status sinkr_decode_append_step(sinkr_engine* e, const float* queries, const float* k_new,
+                                      const float* v_new, size_t layer,
+                                      const sinkr_routing_config* config,
+                                      const sinkr_engine_options* options, float* outputs,
+                                      sinkr_group_info* groups, double* head_scores,
+                                      sinkr_load_counters* counters) {
+    return guard([&] {
+        if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+        if (!queries) fail(SINKR_INVALID_ARGUMENT, "queries span must be H_q x D for one layer");
+        if (!k_new || !v_new) fail(SINKR_INVALID_ARGUMENT, "k/v row size does not match head_dim");
+        if (!config) fail(SINKR_INVALID_ARGUMENT, "routing config is null");
+        CK(cudaSetDevice(e->device));
+        const size_t H = e->cfg.num_kv_heads, D = e->D;
+        if (check_token_append(e, layer)) {  // first rows: the host append path
+            for (size_t u = 0; u < e->U; ++u) {
+                const sinkr_status st = sinkr_kv_append(e, u / H, layer, u % H, k_new + u * D, v_new + u * D, 1);
+                if (st != SINKR_OK) fail(st, g_err);
+            }
+            decode_host(e, queries, layer, config, options, outputs, groups, head_scores, counters, 0);
+            return;
+        }
+        // every slot of each sequence must be uniform once this layer grows
+        for (size_t s = 0; s < e->B; ++s) {
+            const size_t n = e->len[e->slot_index(layer, s, 0)] + 1;
+            for (size_t l = 0; l < e->layers; ++l)
+                for (size_t g = 0; g < H; ++g)
+                    if (e->len[e->slot_index(l, s, g)] + (l == layer ? 1 : 0) != n)
+                        fail(SINKR_LOGIC_ERROR, "kv cache lengths are ragged across slots");
+        }
+        sync_dlen(e);  // the kernel appends at the device lengths (pre-append)
+        for (size_t u = 0; u < e->U; ++u) ++e->len[layer * e->U + u];
+        stage_params(e, layer, config, options, true);
+        const size_t qbytes = e->B * e->cfg.num_q_heads * D * 4;
+        std::memcpy(e->h_in + e->off_q, queries, qbytes);
+        std::memcpy(e->h_in + e->off_kvn, k_new, e->U * D * 4);
+        std::memcpy(e->h_in + e->off_kvn + e->U * D * 4, v_new, e->U * D * 4);
+        if (e->fused && !e->timing && io_mode() != 0) {
+            run_io_graph(e, 0, (long)layer);
+            finish_io(e);
+        } else {
+            CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes_append, cudaMemcpyHostToDevice, e->stream));
+            CK(cudaEventRecord(e->ev_in, e->stream));
+            const float* kn = reinterpret_cast<const float*>(e->d_in + e->off_kvn);
+            launch_append(e, layer, kn, kn + e->U * D);
+            run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), reinterpret_cast<float*>(e->d_res), 0);
+            e->last_launches += 1;
+            CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+            CK(cudaStreamSynchronize(e->stream));
+        }
+        if (outputs && outputs != reinterpret_cast<float*>(e->h_res)) std::memcpy(outputs, e->h_res, qbytes);
+        fill_info(e, layer, config, groups, head_scores, counters, options);
+    });
 }
 
 // splitk_attention (attention.cpp:204-235) of ONE cached group on the GPU:

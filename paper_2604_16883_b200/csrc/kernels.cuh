@@ -753,6 +753,27 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16*
         dst[i] = __float2bfloat16_rn(src[i]);
 }
 
+// One decode token appended to every (seq, kv_head) slot of a layer
+// (KvCache::append, kv_cache.cpp:61-84, for the step's new row), stream
+// ordered: CTA u writes the f32 rows knew/vnew [U][D] as bf16 (RNE) at row
+// len[slot] of slot layer*U + u and advances the device length table.  The
+// engine tracks the same lengths on the host (they feed the step's params)
+// and keeps first rows (anchor capture, degenerate check) on the host path.
+__global__ void append_token_kernel(const float* __restrict__ knew, const float* __restrict__ vnew,
+                                    __nv_bfloat16* __restrict__ K, __nv_bfloat16* __restrict__ V,
+                                    uint32_t* __restrict__ dlen, uint32_t slot0, uint32_t D,
+                                    uint32_t cap) {
+    const uint32_t u = blockIdx.x, slot = slot0 + u;
+    const uint32_t row = dlen[slot];
+    const size_t off = ((size_t)slot * cap + row) * D;
+    for (uint32_t j = threadIdx.x; j < D; j += blockDim.x) {
+        K[off + j] = __float2bfloat16_rn(knew[(size_t)u * D + j]);
+        V[off + j] = __float2bfloat16_rn(vnew[(size_t)u * D + j]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) dlen[slot] = row + 1;
+}
+
 // synthetic rows: value = bf16(scale * gauss12(key, row*D + j)), the exact
 // restatement of oracle/sinkr_oracle.c:orc_fill_rows (counter-based access to
 // the reference's SplitMix64 stream, tensor.hpp:15-25).

@@ -271,6 +271,13 @@ class KvCache:
             C.c_uint64(key_k), C.c_uint64(key_v), C.c_float(k_scale), C.c_float(v_scale),
             C.c_size_t(global_row0), C.c_size_t(rows)))
 
+    def append_token_async(self, layer: int, d_k_new: int, d_v_new: int) -> None:
+        """The decode loop's append: one new row to every (seq, kv_head) slot of
+        `layer` from device f32 [B][H_kv][D] buffers, enqueued on the engine
+        stream (no host sync after the first row)."""
+        check(lib().sinkr_kv_append_token_async(self.handle, layer, C.c_void_p(d_k_new),
+                                                C.c_void_p(d_v_new)))
+
     def step_io_bytes(self):
         h2d, d2h = C.c_size_t(), C.c_size_t()
         check(lib().sinkr_step_io_bytes(self._h, C.byref(h2d), C.byref(d2h)))
@@ -587,3 +594,35 @@ class StepRunner:
     def result(self) -> LayerStepResult:
         return _to_result(self.cache, self.out.copy(), self.groups, self.hs, self.ctr,
                           batched=self.cache.B > 1)
+
+
+class AppendStepRunner(StepRunner):
+    """StepRunner whose calls first append the new token's K/V rows (host f32
+    [B][H_kv][D]) to every slot of the layer, then step over the grown cache:
+    sinkr_decode_append_step, one graph per call."""
+
+    def __init__(self, cache: KvCache, config: RoutingConfig, options: Optional[EngineOptions] = None,
+                 layer: int = 0, pinned_io: bool = False):
+        super().__init__(cache, config, options, layer, pinned_io)
+        self._fa = lib().sinkr_decode_append_step
+        cc = cache.config()
+        self._kvsize = cache.B * cc.num_kv_heads * cc.head_dim
+
+    def __call__(self, k_new, v_new, queries: Optional[np.ndarray] = None) -> np.ndarray:
+        if queries is None:
+            if self.queries is None:
+                raise ValueError("no queries: pass them, or build the runner with pinned_io=True")
+            queries = self.queries
+        queries = np.ascontiguousarray(queries, dtype=np.float32)
+        k = np.ascontiguousarray(k_new, dtype=np.float32)
+        v = np.ascontiguousarray(v_new, dtype=np.float32)
+        if queries.size != self._qsize:
+            raise ValueError("queries span must be H_q x D for one layer")
+        if k.size != self._kvsize or v.size != self._kvsize:
+            raise ValueError("k/v row size does not match head_dim")
+        h, _, layer, cfg, opt, out, groups, hs, ctr = self._args
+        rc = self._fa(h, queries.ctypes.data, k.ctypes.data, v.ctypes.data, layer, cfg, opt, out,
+                      groups, hs, ctr)
+        if rc:
+            check(rc)
+        return self.out

@@ -45,3 +45,16 @@ def test_cli_end_to_end(tmp_path, capsys):
     assert r["auprc"] == 1.0 and "0.55" in r["operating_points"]
     assert cli.main(["selftest"]) == 0
     assert "selftest: ok" in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+def test_selftest_reports_injected_tie_fault(capsys, monkeypatch):
+    """with the tie-breaking test hook forced on, selftest
+    reports the routing-semantics failure and exits 1 (flag or env var)."""
+    assert cli.main(["selftest", "--inject-tie-fault"]) == 1
+    out = capsys.readouterr().out
+    assert "FAIL  routing semantics: an exact tie routes Active (strict >)" in out
+    assert "selftest: FAILED" in out
+    monkeypatch.setenv("SINKR_INJECT_TIE_FAULT", "1")
+    assert cli.main(["selftest"]) == 1
+    assert "routing semantics" in capsys.readouterr().out.split("FAILED:")[1]
