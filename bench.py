@@ -60,7 +60,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--cpu-steps", type=int, default=32,
+                    help="timed reference steps per CPU-baseline leg (median; BASELINE.md §3: >= 32)")
+    ap.add_argument("--cpu-warmup", type=int, default=4)
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the sequence-sharded N>1 path even at N=1 (validation)")
     return ap.parse_args()
@@ -172,6 +174,44 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+def bench_config(args, world=1):
+    """The workload dict BOTH arms print (`--impl ours` and `--impl reference`):
+    identical keys and values, so the driver's same-config check holds."""
+    L, D, hkv = args.length, SHAPE["head_dim"], SHAPE["num_kv_heads"]
+    n_act = hkv - int(args.sink_fraction * hkv)  # WorkloadSpec plants floor(p * H_kv) sinks
+    kv_routed, kv_dense = n_act * 2 * L * D * 2, hkv * 2 * L * D * 2
+    return {
+        "workload": f"llama3.1-8b-attn L={L} B=1 routed={args.sink_fraction}",
+        "shape": "32q/8kv/D128", "context": L, "batch": 1, "layers": 1,
+        "sink_fraction": args.sink_fraction, "tau": 0.5, "dense_tau": 2.0, "seed": args.seed,
+        "parallelism": "single GPU" if world == 1 and not args.force_sharded
+                       else f"sequence-shard x{world}",
+        "l2": (f"inputs larger than L2 ({kv_routed >> 20} MiB routed / "
+               f"{kv_dense >> 20} MiB dense bf16 KV vs 126 MB L2); sweep flushes L2"
+               if world == 1 else
+               f"{(kv_routed // world) >> 20} MiB routed bf16 KV per rank: steps timed alone "
+               f"behind a 256 MiB L2 flush when that fits in 2x the 126 MB L2"),
+    }
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ----------------------------------------------------------------------------
 # reference (CPU) side: the compiled reference on identical inputs
 def fill_ref_cache(spec, threads):
@@ -206,12 +246,13 @@ def fill_ref_cache(spec, threads):
     return rc
 
 
-def time_reference(spec, steps, warmup, threads):
+def time_reference(spec, steps, warmup, threads, tau=0.5, rc=None):
     import oracle
 
-    rc = fill_ref_cache(spec, threads)
+    if rc is None:
+        rc = fill_ref_cache(spec, threads)
     q = spec.queries()[0]
-    prof = oracle.Profile.constant(0.5)
+    prof = oracle.Profile.constant(tau)
     for _ in range(warmup):
         rc.routed_decode_step(q, 0, prof, excluded=(), workers=threads)
     ts = []
@@ -232,30 +273,36 @@ def run_reference_arm(args, world, rank):
     threads = os.cpu_count() or 1
     spec = WorkloadSpec(**SHAPE, length=args.length, sink_fraction=args.sink_fraction,
                         seed=args.seed)
-    # a routed step of the reference is ~70 ms on 16 host threads: honour K and
-    # W up to 50 / 10 (a few seconds); the cache fill dominates the run
-    steps = max(1, min(args.steps, 50))
-    warm = max(0, min(args.warmup, 10))
-    _, res, ts = time_reference(spec, steps, warm, threads)
-    us = sum(ts) / len(ts) * 1e6
+    # a routed step of the reference is ~50-70 ms on 16 host threads, a dense
+    # one ~3x that: median of >= 32 steps after >= 4 warm-ups,
+    # at most 64 (a few seconds); the cache fill dominates the run
+    steps = min(max(args.steps, 32), 64)
+    warm = min(max(args.warmup, 4), 10)
+    rc, res, ts = time_reference(spec, steps, warm, threads)
+    _, res_d, ts_d = time_reference(spec, steps, warm, threads, tau=2.0, rc=rc)
+    us = statistics.median(ts) * 1e6
+    us_d = statistics.median(ts_d) * 1e6
     n_act = int(res.counters["groups_active"])
     kv_bytes = n_act * 2 * args.length * SHAPE["head_dim"] * 4  # f32 as the reference stores
+    kv_dense = int(res_d.counters["groups_active"]) * 2 * args.length * SHAPE["head_dim"] * 4
     line = {
         "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
         "steps": steps, "warmup": warm, "ms_per_step": round(us / 1e3, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic planted-sink KV (seeded), host f32",
-        "config": {"workload": f"llama3.1-8b-attn L={args.length} B=1 routed={args.sink_fraction}",
-                   "shape": "32q/8kv/D128", "context": args.length,
-                   "sink_fraction": args.sink_fraction, "tau": 0.5},
+        "config": bench_config(args, world),
         "impl": "reference",
         "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{steps} routed_decode_step calls of the compiled reference "
-                                   f"(oracle/_ref, ThreadPool({threads})) at the full config"},
+                         "kind": "reference", "cpu_model": cpu_model(), "nproc": threads,
+                         "sample": f"median of {steps} routed_decode_step calls after {warm} "
+                                   f"warm-ups, compiled reference (oracle/_ref, "
+                                   f"ThreadPool({threads})) at the full config"},
         "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "dense_us_per_step": round(us_d, 1),
+        "speedup_vs_dense": round(us_d / us, 3),
         "kv_gbs_f32": round(kv_bytes / (us * 1e-6) / 1e9, 2),
+        "kv_gbs_f32_dense": round(kv_dense / (us_d * 1e-6) / 1e9, 2),
         "groups_active": n_act,
     }
     print(json.dumps(line), flush=True)
@@ -558,7 +605,8 @@ def run_ours(args, world, rank, local_rank):
 
         result = sharding.bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg,
                                                  args, rank, world, dev, peak_gbs=peak,
-                                                 peak_src=peak_src, clock_sampler=ClockSampler)
+                                                 peak_src=peak_src, clock_sampler=ClockSampler,
+                                                 config=bench_config(args, world))
         if rank == 0:
             print(json.dumps(result), flush=True)
         dist.barrier()
@@ -596,8 +644,15 @@ def run_ours(args, world, rank, local_rank):
     q_bytes = 32 * D * 4
     alg_r = kv_routed + n_act * 4 * D * 4
     alg_d = kv_dense + q_bytes
-    achieved = alg_r / (dec_mean_r * 1e-3) / 1e9
-    achieved_d = alg_d / (dec_mean_d * 1e-3) / 1e9
+    # roofline numerator: the step kernel is the ONLY launch of a timed step
+    # (gpu_launches = steps), so its average launch duration is bounded by the
+    # timed region itself -- CUDA events on the engine stream around K
+    # back-to-back launches, / K.  That includes the inter-launch gap, so the
+    # fraction is conservative (kernel_us == ms_per_step).  The single-launch
+    # event brackets (launch_event_us) carry launch latency and are reported
+    # only beside it.
+    achieved = alg_r / (routed_ms * 1e-3) / 1e9
+    achieved_d = alg_d / (dense_ms * 1e-3) / 1e9
 
     # ---- e2e through the public C-ABI call (sinkr_routed_decode_batch via
     # StepRunner), host queries in, host outputs + routing record out
@@ -621,13 +676,16 @@ def run_ours(args, world, rank, local_rank):
     res_host = runner.result()
     h2d, d2h = cache.step_io_bytes()
 
-    traffic = None
+    # DRAM bytes per launch of this kernel from the committed ncu capture of
+    # the same command (profiles/decode_traffic.json names the capture files)
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
     if os.path.exists(tp):
         try:
             with open(tp) as f:
                 tr = json.load(f)
             traffic = tr.get(f"routed_{L}_{args.sink_fraction}")
+            traffic_src = tr.get("source")
         except Exception:
             traffic = None
 
@@ -644,29 +702,28 @@ def run_ours(args, world, rank, local_rank):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic planted-sink KV (device generator, seeded); fp32 queries",
-        "config": {
-            "workload": f"llama3.1-8b-attn L={L} B=1 routed={args.sink_fraction}",
-            "shape": "32q/8kv/D128", "context": L, "batch": 1, "layers": 1,
-            "sink_fraction": args.sink_fraction, "tau": 0.5, "dense_tau": 2.0,
-            "parallelism": "single GPU",
-            "l2": f"inputs larger than L2 ({kv_routed >> 20} MiB routed / "
-                  f"{kv_dense >> 20} MiB dense KV vs 126 MB L2); sweep flushes L2",
-        },
+        "config": bench_config(args),
         "dense_us_per_step": round(dense_ms * 1e3, 2),
         "speedup_vs_dense": round(dense_ms / routed_ms, 3),
         "groups_active": n_act,
         "kv_gbs_routed_step": round(kv_routed / (routed_ms * 1e-3) / 1e9, 1),
         "kv_gbs_dense_step": round(kv_dense / (dense_ms * 1e-3) / 1e9, 1),
-        "dense_decode_kernel": {"us": round(dec_mean_d * 1e3, 2),
+        "dense_decode_kernel": {"us": round(dense_ms * 1e3, 2),
+                                "launch_event_us": round(dec_mean_d * 1e3, 2),
                                 "achieved_gbs": round(achieved_d, 1),
                                 "frac": round(achieved_d / peak, 4), "phases": phases_d},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": ("step_kernel<128> (fused probe + Split-K decode + merge), routed"
                                 if nlaunch == 1 else "decode_kernel<128> (routed)"),
                      "phases": phases_r,
                      "stream_phase_gbs": round(kv_routed / max(phases_r["stream_us"], 1e-9) / 1e3, 1),
-                     "kernel_us": round(dec_mean_r * 1e3, 2),
+                     "kernel_us": round(routed_ms * 1e3, 2),
+                     "kernel_us_method": "CUDA events on the engine stream around the K "
+                                         "back-to-back launches of the timed region / K "
+                                         "(one step_kernel launch per step)",
+                     "launch_event_us": round(dec_mean_r * 1e3, 2),
                      "alg_bytes_per_launch": alg_r, "peak_source": peak_src},
         "e2e": {"value": round(e2e_us, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "mean_us": round(e2e_mean, 2), "calls": len(e2e_ts),
@@ -681,12 +738,22 @@ def run_ours(args, world, rank, local_rank):
     if not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            _, ref, ts = time_reference(spec, args.cpu_steps, 0, threads)
+            rc, ref, ts = time_reference(spec, args.cpu_steps, args.cpu_warmup, threads)
+            _, ref_d, ts_d = time_reference(spec, args.cpu_steps, args.cpu_warmup, threads,
+                                            tau=2.0, rc=rc)
+            del rc
             cpu_us = statistics.median(ts) * 1e6
+            cpu_us_d = statistics.median(ts_d) * 1e6
             line["cpu_baseline"] = {
                 "value": round(cpu_us, 1), "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": f"{args.cpu_steps} routed_decode_step calls of the compiled reference "
-                          f"(oracle/_ref, ThreadPool({threads})) at the full config, median"}
+                "cpu_model": cpu_model(), "nproc": threads,
+                "dense_value": round(cpu_us_d, 1),
+                "kv_gbs_f32": round(n_act * 2 * L * D * 4 / (cpu_us * 1e-6) / 1e9, 2),
+                "kv_gbs_f32_dense": round(8 * 2 * L * D * 4 / (cpu_us_d * 1e-6) / 1e9, 2),
+                "sample": f"median of {args.cpu_steps} routed (value) and {args.cpu_steps} dense "
+                          f"(dense_value) routed_decode_step calls after {args.cpu_warmup} "
+                          f"warm-ups each, compiled reference (oracle/_ref, ThreadPool({threads})) "
+                          f"at the full config"}
             out = res_host.outputs
             sink = np.array([g.decision.sink for g in res_host.groups], dtype=np.int32)
             err = float(np.abs(out - ref.outputs).max())

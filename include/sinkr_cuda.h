@@ -265,7 +265,12 @@ sinkr_status sinkr_routed_decode_peer_async(sinkr_engine* e, const float* d_quer
                                             float* d_outputs);
 /* The peer-merged step with host buffers, like sinkr_routed_decode_batch: one
  * graph per call (H2D of the staged input block + the mode-3 step kernel,
- * outputs and routing record zero-copy into pinned host memory), blocking. */
+ * outputs and routing record zero-copy into pinned host memory), blocking.
+ * The outputs are the merge over ALL ranks; the routing record (decisions,
+ * scores) is identical on every rank; the load counters and each group's
+ * tokens_loaded / kv_floats_loaded cover THIS rank's shard only -- sum them
+ * over the ranks for the whole step's traffic (the reference's per-group
+ * count, router.cpp:181-182; tests/test_gpu_sharding.py sums them). */
 sinkr_status sinkr_routed_decode_peer(sinkr_engine* e, const float* queries, size_t layer,
                                       const sinkr_routing_config* config,
                                       const sinkr_engine_options* options, float* outputs,

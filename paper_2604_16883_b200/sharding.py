@@ -270,6 +270,35 @@ def time_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ran
         if name == "routed":
             n_act = P.fetch_step_info(cache).counters.groups_active
 
+    # a rank's Active KV fits in L2 at high N (8-way at 512K: 96 MiB of the
+    # 126 MB L2): then back-to-back steps could re-read it from L2, so each
+    # step is timed alone behind a 256 MiB L2 flush (median of per-step event
+    # pairs, max over ranks) and that is the reported value
+    kv_rank_routed = n_act * 2 * (hi - lo) * spec.head_dim * 2
+    flushed = None
+    if kv_rank_routed < 2 * 126 * 1024 * 1024:
+        flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+        flushed = {}
+        for name, cfg in (("routed", routed_cfg), ("dense", dense_cfg)):
+            step(cfg)
+            torch.cuda.synchronize()
+            dist.barrier()
+            evs = []
+            for _ in range(max(args.steps, 10)):
+                with torch.cuda.stream(stream):
+                    flush.add_(1)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                step(cfg)
+                e1.record(stream)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            flushed[name] = maxed(statistics.median(a.elapsed_time(b) for a, b in evs))
+        del flush
+        res["back_to_back_routed"], res["back_to_back_dense"] = res["routed"], res["dense"]
+        res["routed"], res["dense"] = flushed["routed"], flushed["dense"]
+
     # the all-gather + combine path beside it (same steps, same clock)
     nccl_us = None
     if pm is not None:
@@ -288,6 +317,9 @@ def time_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ran
         nccl_us = maxed(e0.elapsed_time(e1) / args.steps) * 1e3
 
     out = {"routed_ms": res["routed"], "dense_ms": res["dense"], "groups_active": n_act,
+           "l2_flushed": flushed is not None,
+           "back_to_back_ms": ({"routed": res["back_to_back_routed"],
+                                "dense": res["back_to_back_dense"]} if flushed else None),
            "lo": lo, "hi": hi, "peer": pm is not None, "peer_err": peer_err, "clocks": clocks,
            "allgather_us": nccl_us, "partial_bytes_per_rank": nf * 4}
     if e2e:
@@ -356,14 +388,21 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
     kv_rank = n_act * 2 * (hi - lo) * spec.head_dim * 2             # this rank
     routed_ms, dense_ms = t["routed_ms"], t["dense_ms"]
     per_gpu_gbs = kv_rank / (routed_ms * 1e-3) / 1e9  # the step time is already max-over-ranks
-    cfg_dict = dict(config or {})
-    cfg_dict.update({
+    # `config` is bench.py's workload dict, printed identically by the
+    # reference arm; how this arm shards it goes under "sharding"
+    cfg_dict = dict(config or {
         "workload": f"llama3.1-8b-attn L={spec.length} B=1 routed={spec.sink_fraction}",
-        "parallelism": (f"sequence-shard x{world} + LSE merge fused into the step kernel "
-                        "over peer memory (NVLink)") if pm else
-                       f"sequence-shard x{world} + NCCL all-gather + combine kernel",
+        "parallelism": f"sequence-shard x{world}"})
+    shard_info = {
+        "merge": ("LSE merge fused into the step kernel over peer memory (NVLink)" if pm else
+                  "NCCL all-gather + combine kernel"),
         "tokens_per_rank": hi - lo,
-        "l2": "per-rank KV larger than L2 at N <= 4; L2 not flushed between back-to-back steps"})
+        "l2": ("a rank's Active KV fits in 2x L2: every step timed alone behind a 256 MiB "
+               "L2 flush (median, max over ranks); back_to_back_us beside it"
+               if t["l2_flushed"] else
+               "a rank's Active KV is larger than 2x L2: back-to-back steps, no flush"),
+        "back_to_back_us": ({k: round(v * 1e3, 2) for k, v in t["back_to_back_ms"].items()}
+                            if t["back_to_back_ms"] else None)}
     line = {
         "metric": ("decode-attn \u00b5s/step & KV GB/s (% HBM peak) at 512K; "
                    "speedup vs own dense path"),
@@ -372,6 +411,7 @@ def bench_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ra
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic planted-sink KV (device generator, seeded); fp32 queries",
         "config": cfg_dict,
+        "sharding": shard_info,
         "dense_us_per_step": round(dense_ms * 1e3, 2),
         "speedup_vs_dense": round(dense_ms / routed_ms, 3),
         "kv_gbs_routed_step": round(kv_total / (routed_ms * 1e-3) / 1e9, 1),
