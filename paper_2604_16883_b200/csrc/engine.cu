@@ -93,6 +93,16 @@ int smem_bytes() {
 
 }  // namespace
 
+// Static share (percent of a CTA's fair share of the Active tokens) of the
+// step kernel's unit-affine schedule; SINKR_STATIC_PCT overrides (A/B runs).
+static uint32_t static_pct() {
+    static uint32_t v = [] {
+        const char* s = std::getenv("SINKR_STATIC_PCT");
+        return s ? (uint32_t)std::atoi(s) : 0u;
+    }();
+    return v;
+}
+
 struct sinkr_engine {
     sinkr_cache_config cfg{};
     size_t B = 1, U = 0, r = 0, D = 0, layers = 0, cap = 0;
@@ -161,7 +171,8 @@ struct sinkr_engine {
     uint32_t bos_parity = 0;             // which counter set the next run_bos uses
     float bos_ms = -1.f;
     size_t h_bos_bytes = 0;
-    uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [U]
+    uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [2][U]
+    uint32_t* d_cta_epoch = nullptr;    // step-kernel launches per CTA slot [grid]
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
     // sequence-sharded peer merge (mode 3): this rank's exchange block
     // [2][world][U][PS] f32 + arrival counter, and every rank's block mapped here
@@ -256,6 +267,7 @@ struct sinkr_engine {
         t.tokens_done = d_tokens_done;
         t.route_flags = d_route_flags;
         t.ovf = d_ovf;
+        t.cta_epoch = d_cta_epoch;
         t.partials = d_partials;
         t.out = out;
         t.B = (uint32_t)B;
@@ -266,6 +278,7 @@ struct sinkr_engine {
         t.S = (uint32_t)S;
         t.mode = (uint32_t)mode;
         t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
+        t.static_pct = static_pct();
         t.trace = d_trace;
         if (mode == 3) {
             t.peer_xchg = d_peer_xchg;
@@ -862,13 +875,17 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->probe_grid = (int)((e->B * Hq + dev::kProbeHeads - 1) / dev::kProbeHeads);
             CK(cudaMalloc(&e->d_ss, sizeof(dev::StepState)));
             CK(cudaMemsetAsync(e->d_ss, 0, sizeof(dev::StepState), e->stream));
-            CK(cudaMalloc(&e->d_cursor, e->U * 4));
-            CK(cudaMemsetAsync(e->d_cursor, 0, e->U * 4, e->stream));
-            CK(cudaMalloc(&e->d_tokens_done, e->U * 4));
+            // per-unit step counters: two sets, used by alternate launches
+            // (StepCounters, step.cuh); the per-CTA launch counts pick the set
+            CK(cudaMalloc(&e->d_cursor, 2 * e->U * 4));
+            CK(cudaMemsetAsync(e->d_cursor, 0, 2 * e->U * 4, e->stream));
+            CK(cudaMalloc(&e->d_tokens_done, 2 * e->U * 4));
             CK(cudaMalloc(&e->d_route_flags, e->U * 4));
-            CK(cudaMalloc(&e->d_ovf, e->U * 4));
-            CK(cudaMemsetAsync(e->d_ovf, 0, e->U * 4, e->stream));
-            CK(cudaMemsetAsync(e->d_tokens_done, 0, e->U * 4, e->stream));
+            CK(cudaMalloc(&e->d_ovf, 2 * e->U * 4));
+            CK(cudaMemsetAsync(e->d_ovf, 0, 2 * e->U * 4, e->stream));
+            CK(cudaMemsetAsync(e->d_tokens_done, 0, 2 * e->U * 4, e->stream));
+            CK(cudaMalloc(&e->d_cta_epoch, e->grid * 4));
+            CK(cudaMemsetAsync(e->d_cta_epoch, 0, e->grid * 4, e->stream));
             if (const char* tr = std::getenv("SINKR_TRACE"); tr && tr[0] == '1') {
                 CK(cudaMalloc(&e->d_trace, e->grid * 8 * 8));
                 CK(cudaMemsetAsync(e->d_trace, 0, e->grid * 8 * 8, e->stream));
@@ -882,8 +899,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMemsetAsync(e->d_ws, 0, sizeof(dev::WorkState), e->stream));
             CK(cudaMalloc(&e->d_active, e->U * 16));
             CK(cudaMalloc(&e->d_prefix, (e->U + 1) * 4));  // unit_next cursors
-            CK(cudaMalloc(&e->d_slot_count, e->U * 4));
-            CK(cudaMemsetAsync(e->d_slot_count, 0, e->U * 4, e->stream));
+            CK(cudaMalloc(&e->d_slot_count, 2 * e->U * 4));
+            CK(cudaMemsetAsync(e->d_slot_count, 0, 2 * e->U * 4, e->stream));
             // partial slots per unit: one per (CTA, unit) visit up to S-1; any
             // further partial of a unit is LSE-combined into slot S-1 under a
             // per-unit lock (step.cuh flush), so S only sizes the fast path.
@@ -891,6 +908,9 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->S = std::min<size_t>(e->grid, (e->cap + dev::kStageTok - 1) / dev::kStageTok) + 32;
             if (const char* ds = std::getenv("SINKR_DEBUG_SLOTS"); ds && std::atoi(ds) >= 2)
                 e->S = (size_t)std::atoi(ds);
+            // even: a unit's slot block then starts 16-byte aligned (PS is
+            // even), which the merge's bulk copies need
+            e->S = (e->S + 1) & ~size_t(1);
             e->PS = e->r * (e->D + 2);
             // + 64 slots: warp_merge loads groups of 64 slots unpredicated
             CK(cudaMalloc(&e->d_partials, (e->U * e->S + 64) * e->PS * 4));
@@ -982,6 +1002,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_peer_xchg);
     cudaFree(e->d_peer_arrive);
     cudaFree(e->d_ovf);
+    cudaFree(e->d_cta_epoch);
     cudaFree(e->d_head_degen);
     cudaFree(e->d_active);
     cudaFree(e->d_prefix);
@@ -2030,6 +2051,30 @@ extern "C" sinkr_status sinkr_debug_trace(sinkr_engine* e, unsigned long long* o
         CK(cudaStreamSynchronize(e->stream));
         CK(cudaMemcpy(out, e->d_trace, e->grid * 8 * 8, cudaMemcpyDeviceToHost));
         CK(cudaMemset(e->d_trace, 0, e->grid * 8 * 8));
+    });
+}
+
+// debug: touch the K and V regions of `layer` with one 4-byte load every
+// `stride` bytes on the engine stream (cold-start experiments: warms address
+// translation for the region without pulling it into L2 beyond a line/stride)
+__global__ void debug_touch_kernel(const uint8_t* k, const uint8_t* v, size_t bytes, size_t stride,
+                                   unsigned int* sink) {
+    unsigned int acc = 0;
+    for (size_t off = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * stride; off < bytes;
+         off += (size_t)gridDim.x * blockDim.x * stride)
+        acc += *reinterpret_cast<const volatile unsigned int*>(k + off) +
+               *reinterpret_cast<const volatile unsigned int*>(v + off);
+    if (acc == 0x9e3779b9u) *sink = acc;
+}
+
+extern "C" sinkr_status sinkr_debug_touch(sinkr_engine* e, size_t layer, size_t stride) {
+    return guard([&] {
+        const size_t bytes = e->U * e->cap * e->D * 2;
+        const uint8_t* k = reinterpret_cast<const uint8_t*>(e->d_k) + layer * bytes;
+        const uint8_t* v = reinterpret_cast<const uint8_t*>(e->d_v) + layer * bytes;
+        debug_touch_kernel<<<148, 128, 0, e->stream>>>(k, v, bytes, stride,
+                                                       reinterpret_cast<unsigned int*>(e->d_norm64));
+        CK(cudaGetLastError());
     });
 }
 

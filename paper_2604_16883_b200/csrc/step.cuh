@@ -39,15 +39,24 @@ constexpr uint32_t kFlatMinTok = 512;  // smallest claim of the global token-spa
 constexpr double kRouteMargin = 1e-4;
 constexpr uint32_t kMaxEstHeads = 2048;  // distributed form: per-CTA estimate slots (s_score overlay)
 
-struct StepState {
+// Cross-CTA counters of one step.  Two sets, used by alternate launches
+// (parity of the per-CTA launch count, StepTables.cta_epoch): a launch zeroes
+// the set its predecessor used, which the next launch will use, so no CTA has
+// to restore anything at exit (the per-unit arrays cursor / slot_count /
+// tokens_done / ovf are double-buffered the same way).
+struct StepCounters {
     unsigned int flat_counter;
     unsigned int merge_next;
-    unsigned int exit_count;
+    unsigned int exit_count;  // only counted when a last CTA has work (host completion word, mode 3)
     unsigned int error;
     unsigned int route_done;  // CTAs that published their units' decisions (distributed routing)
+    unsigned int pad[3];
+};
+struct StepState {
+    StepCounters c[2];
     unsigned int peer_epoch;  // mode 3: steps completed (advanced by the last CTA at exit)
     unsigned int peer_base;   // mode 3: arrivals counted on this rank before this step
-    unsigned int pad;
+    unsigned int pad[6];
 };
 
 struct StepTables {
@@ -68,10 +77,11 @@ struct StepTables {
     unsigned long long* tokens;    // result [U] rows streamed (the skipped-block record)
     uint32_t* status;              // result: nonzero = partial-slot overflow
     StepState* ss;
-    uint32_t* cursor;              // [U] chunk cursor per active-list entry
-    uint32_t* slot_count;          // [U]
-    uint32_t* tokens_done;         // [U]
-    uint32_t* ovf;                 // [U] spill-slot lock (bit0) + valid (bit1)
+    uint32_t* cursor;              // [2][U] chunk cursor per active-list entry (two sets: parity)
+    uint32_t* slot_count;          // [2][U]
+    uint32_t* tokens_done;         // [2][U]
+    uint32_t* ovf;                 // [2][U] spill-slot lock (bit0) + valid (bit1)
+    uint32_t* cta_epoch;           // [grid] launches seen by each CTA slot (counter-set parity)
     float* partials;               // [U][S][r*(D+2)]: m[r], l[r], acc[r][D]
     float* out;                    // mode 0: [B][Hq][D]; mode 1: [U][r][D+2]
     uint32_t B, Hq, Hkv, r, cap, S, mode;  // mode 0 outputs, 1 rank partial, 3 peer merge
@@ -84,6 +94,7 @@ struct StepTables {
     const unsigned int* arrive_local;     // this rank's arrival counter
     uint32_t world, rank;
     float qscale;                  // (1/sqrt(D)) * log2(e)
+    uint32_t static_pct;           // static share of the unit-affine schedule (0: one Ck chunk)
     unsigned long long* trace;     // optional [grid][4] per-CTA globaltimer stamps
     uint32_t* done;                // optional completion word in mapped host memory (set to 1 last)
 };
@@ -113,7 +124,19 @@ struct StepCfg {
 };
 
 // misc smem words
-enum : int { kMiscNact = 0, kMiscChunk, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast, kMiscPeerLate };
+enum : int { kMiscNact = 0, kMiscChunk, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast, kMiscPeerLate,
+             kMiscStatic };
+
+// Unit-affine scheduling: the static first range of a CTA is static_pct % of
+// its fair share T/G of the Active tokens (64-token multiple, at least one
+// stage); the rest is claimed from per-unit cursors (guided, capped at Ck).
+__device__ __forceinline__ uint32_t static_chunk(unsigned long long T, uint32_t G, uint32_t pct,
+                                                 uint32_t Ck) {
+    if (pct == 0) return Ck;
+    unsigned long long c = (T * pct + 100ull * G - 1) / (100ull * G);
+    c = (c + kStageTok - 1) / kStageTok * kStageTok;
+    return c < (unsigned long long)kStageTok ? (uint32_t)kStageTok : (uint32_t)c;
+}
 
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -223,9 +246,17 @@ __device__ __forceinline__ void warp_merge_r(const StepTables& t, uint32_t u, ui
     }
 }
 
+// A step-kernel error: kept in the launch's counter set and stored straight
+// into the result block's status word (zeroed by CTA 0 at launch; every error
+// source is a >= 2 s watchdog or CTA 0 itself, so the zeroing comes first).
+__device__ __forceinline__ void raise_error(const StepTables& t, StepCounters* sc, uint32_t code) {
+    atomicExch(&sc->error, code);
+    *reinterpret_cast<volatile uint32_t*>(t.status) = code;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
-    step_kernel(StepTables t, const ProbeParams p) {
+    step_kernel(const StepTables t_in, const ProbeParams p) {
     using C = Cfg<D>;
     using SC = StepCfg<D>;
     using Scan = cub::BlockScan<uint32_t, kThreads>;
@@ -257,7 +288,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t G = gridDim.x, bid = blockIdx.x;
-    const uint32_t U = t.B * t.Hkv, NH = t.B * t.Hq, r = t.r;
+    const uint32_t U = t_in.B * t_in.Hkv, NH = t_in.B * t_in.Hq, r = t_in.r;
+    // counter-set parity: every CTA of a launch reads the same count (the
+    // grid is fixed per engine and CTA b's count is written only by CTA b,
+    // after its final barrier); this launch uses set `par` and zeroes the
+    // other, which the previous launch used and the next one will use
+    const uint32_t cta_ep = ld_volatile(&t_in.cta_epoch[bid]), par = cta_ep & 1u;
+    StepTables t = t_in;
+    t.cursor += par * U;
+    t.slot_count += par * U;
+    t.tokens_done += par * U;
+    t.ovf += par * U;
+    StepCounters* const sc = &t_in.ss->c[par];
+    {
+        const uint32_t oth = (par ^ 1u) * U;
+        for (uint32_t i = bid * kThreads + tid; i < U; i += G * kThreads) {
+            t_in.cursor[oth + i] = 0u;
+            t_in.slot_count[oth + i] = 0u;
+            t_in.tokens_done[oth + i] = 0u;
+            t_in.ovf[oth + i] = 0u;
+        }
+        if (bid == 0 && tid == 0) {
+            StepCounters* o = &t_in.ss->c[par ^ 1u];
+            o->flat_counter = o->merge_next = o->exit_count = o->error = o->route_done = 0u;
+            *t.status = 0u;  // (errors are raised by watchdogs >= 2 s later, or by this CTA)
+        }
+    }
     const uint32_t layer = p.layer, flags = p.flags;
     const bool lead = bid == 0;
     unsigned long long* clk = reinterpret_cast<unsigned long long*>(t.status + 4);
@@ -457,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 cc = (cc + kStageTok - 1) / kStageTok * kStageTok;
                 misc[kMiscNact] = nact;
                 misc[kMiscChunk] = cc < kMinChunkTok ? kMinChunkTok : cc;
+                misc[kMiscStatic] = static_chunk(T, G, t.static_pct, misc[kMiscChunk]);
                 misc[kMiscFlat] = 0u;  // U <= 32 < #SMs: unit-affine scheduling
             }
             return true;
@@ -727,11 +784,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         if (tid == 0) {
             __threadfence();
-            atomicAdd(&t.ss->route_done, 1u);
+            atomicAdd(&sc->route_done, 1u);
             const unsigned long long t_spin = globaltimer();
-            while (ld_volatile(&t.ss->route_done) < G) {
+            while (ld_volatile(&sc->route_done) < G) {
                 if (globaltimer() - t_spin > 2000000000ull) {
-                    atomicExch(&t.ss->error, 3u);
+                    raise_error(t, sc, 3u);
                     break;
                 }
             }
@@ -809,6 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tid == 0) {
             misc[kMiscNact] = nact;
             misc[kMiscChunk] = Ck;
+            misc[kMiscStatic] = static_chunk(T, G, t.static_pct, Ck);
             misc[kMiscFlat] = flat ? 1u : 0u;
         }
     }
@@ -816,6 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     STAMP(7);
     const uint32_t nact = misc[kMiscNact];
     const uint32_t Ck = misc[kMiscChunk];
+    const uint32_t Cs = misc[kMiscStatic];
     const bool flat = misc[kMiscFlat] != 0;
     // up to ~4 merge tasks (unit, head, 32 dims) per consumer warp: the tasks
     // are spread over every warp once its stream ends; more: the CTA that
@@ -872,8 +931,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (nact > 0 && !flat) {
                 // Unit-affine guided self-scheduling over TOKEN cursors.  CTA c
                 // starts on Active entry c mod nact with the static range
-                // [k*Ck, (k+1)*Ck), k = c / nact.  Later claims take tokens past
-                // the statically covered prefix base(a)*Ck; their size shrinks
+                // [k*Cs, (k+1)*Cs), k = c / nact.  Later claims take tokens past
+                // the statically covered prefix base(a)*Cs; their size shrinks
                 // with the unit's remaining rows (guided), down to one 64-token
                 // stage, so all SMs finish within about one stage of each other.
                 // An exhausted unit hands the CTA on to the unit with the most
@@ -885,13 +944,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // CTAs nact, 2 nact, ... (chunk k - 1).
                 const uint32_t cpu = (G + nact - 1) / nact;  // CTAs per unit
                 auto static_end = [&](uint32_t e) {        // statically covered prefix of entry e
-                    return (((G - e + nact - 1) / nact) - (e == 0 ? 1u : 0u)) * Ck;
+                    return (((G - e + nact - 1) / nact) - (e == 0 ? 1u : 0u)) * Cs;
                 };
                 uint32_t a = bid % nact;
                 uint32_t u = act_unit[a], L = act_len[a];
                 uint32_t first = static_end(a);
                 const uint32_t k0 = bid / nact - (a == 0 ? 1u : 0u);  // bid 0: wraps, no static range
-                uint32_t t0 = bid == 0 ? L : k0 * Ck, t1 = min(t0 + Ck, L);
+                uint32_t t0 = bid == 0 ? L : k0 * Cs, t1 = min(t0 + Cs, L);
                 auto guided = [&](uint32_t hint) {
                     const uint32_t rem = L > hint ? L - hint : 0u;
                     uint32_t sz = rem / (3 * cpu);
@@ -966,8 +1025,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // prefetch the next claim, sized from the LIVE cursor: our own
                     // position lags it by about one claim per CTA, which would
                     // keep late claims large and leave a long tail
-                    const uint32_t sz = guided(base + ld_volatile(&t.ss->flat_counter));
-                    const uint32_t n0 = base + atomicAdd(&t.ss->flat_counter, sz);
+                    const uint32_t sz = guided(base + ld_volatile(&sc->flat_counter));
+                    const uint32_t n0 = base + atomicAdd(&sc->flat_counter, sz);
                     while (g0 < g1) {
                         // act_prefix is sorted and claims of one CTA increase
                         if (act_prefix[a + 1] <= g0) {
@@ -1115,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 const bool taken = lean ? act_prefix[u] != 0u : (t.route_flags[u] & kActive) != 0u;
-                if (active != taken) atomicExch(&t.ss->error, 4u);  // never: margin >> error
+                if (active != taken) raise_error(t, sc, 4u);  // never: margin >> error
             }
             ptx::named_bar_sync(1, kCWarps * 32);
         }
@@ -1190,7 +1249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const unsigned long long t_spin = globaltimer();
                     while ((old_v = atomicOr(&t.ovf[u], 1u)) & 1u) {
                         if (globaltimer() - t_spin > 2000000000ull) {
-                            atomicExch(&t.ss->error, 1u);
+                            raise_error(t, sc, 1u);
                             break;
                         }
                     }
@@ -1352,7 +1411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ntasks = nact * r * nd;
         for (;;) {
             uint32_t task = 0;
-            if (lane == 0) task = atomicAdd(&t.ss->merge_next, 1u);
+            if (lane == 0) task = atomicAdd(&sc->merge_next, 1u);
             task = __shfl_sync(0xffffffffu, task, 0);
             if (task >= ntasks) break;
             const uint32_t a = task / (r * nd), rem = task % (r * nd);
@@ -1365,7 +1424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const unsigned long long t_spin = globaltimer();
                 while (ptx::ld_acquire(&t.tokens_done[u]) < L) {
                     if (globaltimer() - t_spin > 2000000000ull) {
-                        atomicExch(&t.ss->error, 2u);
+                        raise_error(t, sc, 2u);
                         break;
                     }
                 }
@@ -1398,7 +1457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(t.arrive_local) : "memory");
                 if ((int)(v - want) >= 0) break;
                 if (globaltimer() - t_spin > 2000000000ull) {
-                    atomicExch(&t.ss->error, 5u);
+                    raise_error(t, sc, 5u);
                     late = 1;
                     break;
                 }
@@ -1435,49 +1494,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
-    // ======================= exit: last CTA restores the counters ================
+    // ======================= exit =============================================
+    // Nothing to restore (the next launch zeroes this launch's counter set).
+    // A last CTA is found only when it has work: the host completion word
+    // (zero-copy results) and the mode-3 step count.
     __syncthreads();
     if (t.trace && tid == 0) t.trace[bid * 8 + 2] = globaltimer();
-    if (tid == 0) {
-        // acq_rel count: releases this CTA's writes (ordered before tid 0 by
-        // the barrier) and, for the last CTA, acquires everyone's.  System
-        // scope when results go to mapped host memory and a host thread waits
-        // on the completion word instead of the stream.
-        const uint32_t prev = t.done ? ptx::atom_add_acq_rel_sys(&t.ss->exit_count, 1u)
-                                     : ptx::atom_add_acq_rel(&t.ss->exit_count, 1u);
-        misc[kMiscLast] = prev == G - 1 ? 1u : 0u;
-    }
-    __syncthreads();
-    STAMP(11);
-    if (misc[kMiscLast]) {
-        for (uint32_t a = tid; a < nact; a += kThreads) {
-            const uint32_t u = act_unit[a];
-            t.cursor[a] = 0;
-            t.slot_count[u] = 0;
-            t.tokens_done[u] = 0;
-            t.ovf[u] = 0;
-        }
-        if (tid == 0 && t.trace) t.trace[bid * 8 + 5] = globaltimer();
+    if (tid == 0) t_in.cta_epoch[bid] = cta_ep + 1u;  // after every thread of the CTA read it
+    if (t.done || t.mode == 3) {
         if (tid == 0) {
-            clk[2] = t_stream_end;
-            clk[3] = globaltimer();
-            *t.status = t.ss->error;
-            t.ss->error = 0;
-            t.ss->flat_counter = 0;
-            t.ss->merge_next = 0;
-            t.ss->exit_count = 0;
-            t.ss->route_done = 0;
-            if (t.mode == 3) {
-                t.ss->peer_epoch = epoch + 1u;
-                t.ss->peer_base = peer_want;
-            }
-            if (t.done) {
-                // every CTA's results (outputs, routing record, status) are
-                // visible system-wide before the host sees the word
-                __threadfence_system();
-                ptx::st_release_sys(t.done, 1u);
+            // acq_rel count: releases this CTA's writes (ordered before tid 0
+            // by the barrier) and, for the last CTA, acquires everyone's.
+            // System scope when results go to mapped host memory and a host
+            // thread waits on the completion word instead of the stream.
+            const uint32_t prev = t.done ? ptx::atom_add_acq_rel_sys(&sc->exit_count, 1u)
+                                         : ptx::atom_add_acq_rel(&sc->exit_count, 1u);
+            if (prev == G - 1) {
+                if (t.trace) t.trace[bid * 8 + 5] = globaltimer();
+                clk[2] = t_stream_end;
+                clk[3] = globaltimer();
+                if (t.mode == 3) {
+                    t.ss->peer_epoch = epoch + 1u;
+                    t.ss->peer_base = peer_want;
+                }
+                if (t.done) {
+                    // every CTA's results (outputs, routing record, status)
+                    // are visible system-wide before the host sees the word
+                    __threadfence_system();
+                    ptx::st_release_sys(t.done, 1u);
+                }
             }
         }
+    } else if (tid == 0) {
+        // phase stamps: the latest stream end and exit (globaltimer only grows,
+        // so a max over this launch's CTAs needs no reset)
+        atomicMax(&clk[2], t_stream_end);
+        atomicMax(&clk[3], globaltimer());
     }
 }
 

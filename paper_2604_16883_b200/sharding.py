@@ -286,7 +286,7 @@ def time_sequence_sharded(P, torch, dist, spec, routed_cfg, dense_cfg, args, ran
             evs = []
             for _ in range(max(args.steps, 10)):
                 with torch.cuda.stream(stream):
-                    flush.add_(1)
+                    flush.sum()  # read-only flush: evicts L2 without dirty write-backs
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)

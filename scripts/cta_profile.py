@@ -46,7 +46,7 @@ for cold in (False, True):
     for it in range(8):
         if cold:
             with torch.cuda.stream(st):
-                flush.add_(1)
+                flush.sum()  # read-only: evicts L2 without leaving dirty lines
         else:
             step()
         _abi.lib().sinkr_debug_trace(cache.handle, buf)  # clears
@@ -75,4 +75,8 @@ for cold in (False, True):
     dur = (a[:, 1] - a[:, 0]) / 1e3
     gbs = toks * 512 / np.maximum(dur, 1e-3) / 1e3
     print(f"  per-CTA stream GB/s quantiles {np.percentile(gbs, qs).round(1)}")
+    for b in list(np.argsort(-a[:, 2])[:3]) + [0]:
+        print(f"  cta {b:3d}: start {rel(4)[b]:6.2f} stream {rel(0)[b]:6.2f} prod_end {rel(7)[b]:6.2f} "
+              f"stream_end {rel(1)[b]:6.2f} merge {rel(3)[b] if a[b, 3] else float('nan'):6.2f} "
+              f"exit {rel(2)[b]:6.2f} claims {emits[b]} tokens {toks[b]} t6 {(a[b, 6] - t0) / 1e3:9.2f}")
 cache.close()
