@@ -41,6 +41,15 @@ constexpr uint32_t kSink = 1u, kDegenerate = 2u, kActive = 4u;
 // hdr flags
 constexpr uint32_t kObserveOnly = 1u, kSinkOnTie = 2u, kLayerExcluded = 4u;
 
+// Host -> device copy of the pinned (mapped) staging block by a small kernel.
+// As a graph node it is ~8 us shorter than a cudaMemcpy node of the same 16 KB
+// (copy-engine start latency; scripts/micro/e2e_floor.cu), which is most of
+// what separates a blocking step from its device time.
+__global__ void upload_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, uint32_t n16) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 struct StepHdr {
     uint32_t layer;
     uint32_t flags;
