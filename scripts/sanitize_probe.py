@@ -16,9 +16,11 @@ for B, L in ((1, 4096), (4, 3000), (40, 600)):
         spec.fill(cache)
         q = spec.queries()
         cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
-        for _ in range(2):
-            res = P.routed_decode_step(q[0] if B == 1 else q, 0, cache, cfg)
-        assert np.isfinite(res.outputs).all()
+        for timing in (True, False):  # eager path, then the one-graph path (upload kernel + step)
+            P.set_timing(cache, timing)
+            for _ in range(3):  # both counter-set parities, twice
+                res = P.routed_decode_step(q[0] if B == 1 else q, 0, cache, cfg)
+            assert np.isfinite(res.outputs).all()
         g = P.splitk_attention(cache, q.reshape(B, 32, 128)[B - 1, 4:8], 0, 1, 1, seq=B - 1)
         assert np.isfinite(g.out).all()
         from paper_2604_16883_b200 import calibration as cal
@@ -27,4 +29,25 @@ for B, L in ((1, 4096), (4, 3000), (40, 600)):
         a0 = A.attention_bos_mass(cache, q, 0)
         w = A.attention_weights(cache, q[0, :4], 0, 1)
         assert np.isfinite(a0).all() and np.isfinite(w).all()
+# span operators (csrc/span.cu) on host spans
+rng = np.random.default_rng(5)
+kk = rng.standard_normal((700, 64)).astype(np.float32)
+vv = rng.standard_normal((700, 64)).astype(np.float32)
+qq = rng.standard_normal((3, 64)).astype(np.float32)
+from paper_2604_16883_b200 import attention as SA
+r1 = SA.splitk_attention(qq, kk, vv, num_splits=3)
+parts = [SA.attend_chunk(qq, kk[a:b], vv[a:b]) for a, b in ((0, 300), (300, 700))]
+mo = SA.merge_partials(parts + [SA.SplitPartial()], 3, 64)
+assert np.isfinite(r1.out).all() and np.abs(mo - r1.out).max() < 1e-5
+# per-token append + step (one graph) and the stream-ordered token append
+spec = WorkloadSpec(length=1000, sink_fraction=0.5, seed=4)
+with P.KvCache(P.CacheConfig(1, 32, 8, 128, 1003)) as cache:
+    spec.fill(cache)
+    P.set_timing(cache, False)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    run = P.AppendStepRunner(cache, cfg)
+    for _ in range(3):
+        o = run(rng.standard_normal((8, 128)).astype(np.float32),
+                rng.standard_normal((8, 128)).astype(np.float32), spec.queries()[0])
+        assert np.isfinite(o).all()
 print("sanitize probe OK")
