@@ -151,6 +151,7 @@ struct sinkr_engine {
     // fused single-kernel step (step.cuh); the 3-kernel pipeline remains for
     // A/B profiling (SINKR_FUSED=0) and serves the multi-rank merge.
     bool fused = true;
+    bool lean = false;  // single-sequence step-kernel instantiation (step.cuh LEAN)
     dev::StepState* d_ss = nullptr;
     uint32_t* d_cursor = nullptr;
     uint32_t* d_tokens_done = nullptr;
@@ -362,6 +363,15 @@ static int debug_kernel_mask() {
     return m;
 }
 
+// the step-kernel instantiation of this engine (lean: single-sequence shapes)
+const void* step_fn(const sinkr_engine* e) {
+    switch (e->D) {
+        case 32: return e->lean ? (const void*)dev::step_kernel<32, true> : (const void*)dev::step_kernel<32, false>;
+        case 64: return e->lean ? (const void*)dev::step_kernel<64, true> : (const void*)dev::step_kernel<64, false>;
+        default: return e->lean ? (const void*)dev::step_kernel<128, true> : (const void*)dev::step_kernel<128, false>;
+    }
+}
+
 template <int D>
 void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     cudaLaunchConfig_t cfg{};
@@ -375,7 +385,7 @@ void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, dev::step_kernel<D>, st, e->pp));
+    CK(cudaLaunchKernelEx(&cfg, e->lean ? dev::step_kernel<D, true> : dev::step_kernel<D, false>, st, e->pp));
 }
 
 void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode,
@@ -443,9 +453,7 @@ void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
         std::vector<cudaGraphNode_t> nodes(n);
         CK(cudaGraphGetNodes(ge.graph, nodes.data(), &n));
         const void* probe_fn =
-            e->fused ? (e->D == 32 ? (const void*)dev::step_kernel<32>
-                        : e->D == 64 ? (const void*)dev::step_kernel<64>
-                                     : (const void*)dev::step_kernel<128>)
+            e->fused ? step_fn(e)
                      : (e->D == 32 ? (const void*)dev::probe_kernel<32>
                         : e->D == 64 ? (const void*)dev::probe_kernel<64>
                                      : (const void*)dev::probe_kernel<128>);
@@ -553,16 +561,14 @@ void run_io_graph(sinkr_engine* e, int mode = 0, long append_layer = -1) {
         CK(cudaGraphGetNodes(ge.graph, nullptr, &n));
         std::vector<cudaGraphNode_t> nodes(n);
         CK(cudaGraphGetNodes(ge.graph, nodes.data(), &n));
-        const void* step_fn = e->D == 32 ? (const void*)dev::step_kernel<32>
-                              : e->D == 64 ? (const void*)dev::step_kernel<64>
-                                           : (const void*)dev::step_kernel<128>;
+        const void* sfn = step_fn(e);
         for (auto nd : nodes) {
             cudaGraphNodeType ty;
             CK(cudaGraphNodeGetType(nd, &ty));
             if (ty != cudaGraphNodeTypeKernel) continue;
             cudaKernelNodeParams kp{};
             CK(cudaGraphKernelNodeGetParams(nd, &kp));
-            if (kp.func != step_fn) continue;
+            if (kp.func != sfn) continue;
             ge.probe_kp = kp;
             ge.probe = nd;
         }
@@ -884,6 +890,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
 
             CK(cudaMalloc(&e->d_head_degen, e->B * Hq * 4));
             e->probe_grid = (int)((e->B * Hq + dev::kProbeHeads - 1) / dev::kProbeHeads);
+            // the step kernel's lean routing form (step.cuh): every single-sequence shape
+            e->lean = e->B * Hq <= (size_t)dev::kRouteTile && e->U <= 32;
             CK(cudaMalloc(&e->d_ss, sizeof(dev::StepState)));
             CK(cudaMemsetAsync(e->d_ss, 0, sizeof(dev::StepState), e->stream));
             // per-unit step counters: two sets, used by alternate launches
@@ -946,13 +954,10 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
                                     dev::BosCfg<64>::kSmemBytes));
             CK(cudaFuncSetAttribute(dev::bos_stream_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     dev::BosCfg<128>::kSmemBytes));
-            CK(cudaFuncSetAttribute(dev::step_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dev::StepCfg<32>::kSmemBytes));
-            CK(cudaFuncSetAttribute(dev::step_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dev::StepCfg<64>::kSmemBytes));
-            CK(cudaFuncSetAttribute(dev::step_kernel<128>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dev::StepCfg<128>::kSmemBytes));
+            CK(cudaFuncSetAttribute(step_fn(e), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    e->D == 32 ? dev::StepCfg<32>::kSmemBytes
+                                    : e->D == 64 ? dev::StepCfg<64>::kSmemBytes
+                                                 : dev::StepCfg<128>::kSmemBytes));
             CK(cudaFuncSetAttribute(dev::probe_kernel<32>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
             CK(cudaFuncSetAttribute(dev::probe_kernel<64>,

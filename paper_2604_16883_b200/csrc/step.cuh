@@ -158,7 +158,7 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 // (mode 1), or that partial into every rank's exchange block (mode 3).
 template <int D, int R>
 __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
-                                           uint32_t lane, size_t xoff) {
+                                           uint32_t lane, size_t xoff, float* wsm) {
     // R = t.r at compile time: the partial stride is an immediate, so each of
     // the 64 acc loads is one LDG with an immediate offset.  This loop is cold
     // code at the end of every step, and instruction fetch from DRAM costs
@@ -200,8 +200,23 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
         lsum += lw;
+        // the 64 weights reach every lane through the warp's shared scratch
+        // (16 broadcast 16-byte loads instead of 64 shuffles: a shorter cold
+        // tail), into 4 independent FMA chains
+        wsm[lane] = w[0];
+        wsm[32 + lane] = w[1];
+        __syncwarp();
+        float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int k = 0; k < 64; ++k) acc += av[k] * __shfl_sync(0xffffffffu, w[k / 32], k % 32);
+        for (int k4 = 0; k4 < 16; ++k4) {
+            const float4 wv = reinterpret_cast<const float4*>(wsm)[k4];
+            a4[0] = fmaf(av[4 * k4], wv.x, a4[0]);
+            a4[1] = fmaf(av[4 * k4 + 1], wv.y, a4[1]);
+            a4[2] = fmaf(av[4 * k4 + 2], wv.z, a4[2]);
+            a4[3] = fmaf(av[4 * k4 + 3], wv.w, a4[3]);
+        }
+        acc += (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        __syncwarp();  // scratch reused by the next group / task
     }
     if (t.mode == 0) {
         t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
@@ -233,16 +248,16 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
 // warp_merge for the runtime GQA width
 template <int D>
 __device__ __forceinline__ void warp_merge_r(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
-                                             uint32_t lane, size_t xoff) {
+                                             uint32_t lane, size_t xoff, float* wsm) {
     switch (t.r) {
-        case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff); break;
-        case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff); break;
-        case 3: warp_merge<D, 3>(t, u, h, d0, lane, xoff); break;
-        case 4: warp_merge<D, 4>(t, u, h, d0, lane, xoff); break;
-        case 5: warp_merge<D, 5>(t, u, h, d0, lane, xoff); break;
-        case 6: warp_merge<D, 6>(t, u, h, d0, lane, xoff); break;
-        case 7: warp_merge<D, 7>(t, u, h, d0, lane, xoff); break;
-        default: warp_merge<D, 8>(t, u, h, d0, lane, xoff); break;
+        case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff, wsm); break;
+        case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff, wsm); break;
+        case 3: warp_merge<D, 3>(t, u, h, d0, lane, xoff, wsm); break;
+        case 4: warp_merge<D, 4>(t, u, h, d0, lane, xoff, wsm); break;
+        case 5: warp_merge<D, 5>(t, u, h, d0, lane, xoff, wsm); break;
+        case 6: warp_merge<D, 6>(t, u, h, d0, lane, xoff, wsm); break;
+        case 7: warp_merge<D, 7>(t, u, h, d0, lane, xoff, wsm); break;
+        default: warp_merge<D, 8>(t, u, h, d0, lane, xoff, wsm); break;
     }
 }
 
@@ -254,7 +269,13 @@ __device__ __forceinline__ void raise_error(const StepTables& t, StepCounters* s
     *reinterpret_cast<volatile uint32_t*>(t.status) = code;
 }
 
-template <int D>
+// LEAN: the single-sequence instantiation (B*H_q <= 64, B*H_kv <= 32: every
+// single-sequence shape of the configs) -- estimate-first routing in every CTA,
+// unit-affine scheduling; the distributed routing, the global-token-space
+// scheduler and their exact record are compiled out, so the binary a step
+// fetches (cold, from DRAM, at the start of every step in a model) is smaller.
+// The engine picks the instantiation once, from its shape (engine.cu step_fn).
+template <int D, bool LEAN>
 __global__ void __launch_bounds__(kThreads, 1)
     step_kernel(const StepTables t_in, const ProbeParams p) {
     using C = Cfg<D>;
@@ -363,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     //    in all, and a short code path (the phase is latency bound).
     //  * distributed (batched steps): each CTA scores its share of the units,
     //    one grid barrier, then every CTA scans the published decisions.
-    const bool lean = NH <= (uint32_t)kRouteTile && U <= 32u;
+    constexpr bool lean = LEAN;
     bool exact_later = false;  // distributed form: exact record after streaming starts
     if (lean) {
         // Fast decision first: an fp32 estimate of every head score (warp
@@ -875,13 +896,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t nact = misc[kMiscNact];
     const uint32_t Ck = misc[kMiscChunk];
     const uint32_t Cs = misc[kMiscStatic];
-    const bool flat = misc[kMiscFlat] != 0;
+    const bool flat = !LEAN && misc[kMiscFlat] != 0;
     // up to ~4 merge tasks (unit, head, 32 dims) per consumer warp: the tasks
     // are spread over every warp once its stream ends; more: the CTA that
     // streams a group's last rows merges it in line.  A/B (r01f, back to back):
     // queue mode for all takes C3-dense (2,048 tasks) 959 -> 941 us and
     // C5-routed (1,920) 309 -> 305 us, but C5-dense (5,120) 757 -> 761 us.
-    const bool queue_mode = nact * r * (D / 32) <= 16u * G;
+    const bool queue_mode = LEAN || nact * r * (D / 32) <= 16u * G;  // (LEAN: nact <= 32; correct either way)
     const bool lean_fast = lean && misc[kMiscFast] != 0;
     // mode 3: partial slots double-buffered by step parity (a rank one step
     // ahead never overwrites partials a slower rank is still merging).  The
@@ -1218,7 +1239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // merge every partial of unit u (consumers only; few partials)
         auto merge_unit = [&](uint32_t u, uint32_t L) {
             for (uint32_t task = cw; task < r * (D / 32); task += kCWarps)
-                warp_merge_r<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff);
+                warp_merge_r<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff, sm_o + warp * 64);
             if (ctid == 0) t.tokens[u] = L;
         };
         auto flush = [&](uint32_t u, uint32_t L) {
@@ -1431,7 +1452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
             }
             __syncwarp();
-            warp_merge_r<D>(t, u, h, d - lane, lane, xoff);
+            warp_merge_r<D>(t, u, h, d - lane, lane, xoff, sm_o + warp * 64);
             if (h == 0 && d == 0) t.tokens[u] = L;
         }
     }
