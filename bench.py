@@ -355,6 +355,19 @@ def decode_kernel_ms(P, cache, cfg, dq, dout, steps):
     return float(np.mean(ds)), float(np.median(ds)), phases, n
 
 
+FLUSHED_REPS = 30
+
+
+def trimmed_mean(xs, frac=0.1):
+    """Mean of the middle 80 % of single-step event times: CUDA event
+    timestamps tick in ~1 us steps on this GPU, so a median of a few
+    single-step brackets snaps to a tick; the trimmed mean resolves below it
+    and still drops host-hiccup outliers."""
+    xs = sorted(xs)
+    k = int(len(xs) * frac)
+    return statistics.fmean(xs[k:len(xs) - k])
+
+
 def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
     """Context x routed-fraction sweep (BASELINE.json configs[1]).  Each timed
     step follows an L2 flush (a 256 MiB write) on the same stream; CUDA events
@@ -385,9 +398,9 @@ def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
                     P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
                 torch.cuda.synchronize()
                 evs = []
-                gate(torch, stream, 5.0)
+                gate(torch, stream, 0.5 * FLUSHED_REPS)
                 with torch.cuda.stream(stream):
-                    for _ in range(10):
+                    for _ in range(FLUSHED_REPS):
                         flush.sum()  # read-only flush: evicts L2 without dirty write-backs
                         e0 = torch.cuda.Event(enable_timing=True)
                         e1 = torch.cuda.Event(enable_timing=True)
@@ -397,7 +410,7 @@ def sweep(P, torch, args, spec_cls, dense_cfg, routed_cfg, main_cache=None):
                         e1.record(stream)
                         evs.append((e0, e1))
                 torch.cuda.synchronize()
-                res[name] = statistics.median(a.elapsed_time(b) * 1e3 for a, b in evs)
+                res[name] = trimmed_mean([a.elapsed_time(b) * 1e3 for a, b in evs])
             info = P.fetch_step_info(cache)
             n_act = info.counters.groups_active
             if k == 0:
@@ -425,8 +438,9 @@ OTHER_CONFIGS = [
 ]
 
 
-def time_flushed(P, torch, cache, cfg, dq, dout, flush, reps=10):
-    """Median single-step time with a read-only L2 flush before each step."""
+def time_flushed(P, torch, cache, cfg, dq, dout, flush, reps=FLUSHED_REPS):
+    """Single-step time with a read-only L2 flush before each step (trimmed
+    mean of `reps`)."""
     stream = torch.cuda.ExternalStream(cache.stream)
     for _ in range(3):
         P.routed_decode_async(dq.data_ptr(), 0, cache, cfg, d_outputs=dout.data_ptr())
@@ -443,7 +457,7 @@ def time_flushed(P, torch, cache, cfg, dq, dout, flush, reps=10):
             e1.record(stream)
             evs.append((e0, e1))
     torch.cuda.synchronize()
-    return statistics.median(a.elapsed_time(b) * 1e3 for a, b in evs)
+    return trimmed_mean([a.elapsed_time(b) * 1e3 for a, b in evs])
 
 
 def other_configs(P, torch, args, spec_cls, dense_cfg, routed_cfg):

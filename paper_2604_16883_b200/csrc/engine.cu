@@ -102,6 +102,15 @@ static uint32_t static_pct() {
     }();
     return v;
 }
+// Merge-code prewarm of the single-sequence step (StepTables.prewarm);
+// SINKR_PREWARM=0/1 overrides (A/B runs).
+static uint32_t prewarm_default() {
+    static uint32_t v = [] {
+        const char* s = std::getenv("SINKR_PREWARM");
+        return s ? (uint32_t)std::atoi(s) : 8u;
+    }();
+    return v;
+}
 
 struct sinkr_engine {
     sinkr_cache_config cfg{};
@@ -281,6 +290,7 @@ struct sinkr_engine {
         t.mode = (uint32_t)mode;
         t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
         t.static_pct = static_pct();
+        t.prewarm = prewarm_default();
         t.trace = d_trace;
         if (mode == 3) {
             t.peer_xchg = d_peer_xchg;
@@ -372,6 +382,23 @@ const void* step_fn(const sinkr_engine* e) {
     }
 }
 
+static int step_launch_mode() {
+    static int m = [] {
+        const char* v = std::getenv("SINKR_STEP_LAUNCH");
+        return v ? std::atoi(v) : 0;
+    }();
+    return m;
+}
+// SINKR_STEP_GRAPH=0: device-buffer steps launch the kernel directly instead
+// of replaying a captured graph (A/B knob)
+static bool step_graph() {
+    static bool g = [] {
+        const char* v = std::getenv("SINKR_STEP_GRAPH");
+        return !(v && v[0] == '0');
+    }();
+    return g;
+}
+
 template <int D>
 void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     cudaLaunchConfig_t cfg{};
@@ -380,9 +407,16 @@ void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     cfg.dynamicSmemBytes = dev::StepCfg<D>::kSmemBytes;
     cfg.stream = e->stream;
     // cooperative: the merge phase waits on other CTAs, so all must be resident
+    // (SINKR_STEP_LAUNCH=1 plain, =2 programmatic serialization: A/B knobs)
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    const int lm = step_launch_mode();
+    if (lm == 2) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = lm == 0 ? 1 : 0;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CK(cudaLaunchKernelEx(&cfg, e->lean ? dev::step_kernel<D, true> : dev::step_kernel<D, false>, st, e->pp));
@@ -429,7 +463,7 @@ void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode,
 void run_graph(sinkr_engine* e, const float* d_q, float* d_out, int mode) {
     e->last_launches = e->fused ? 1 : 3;
     e->last_mode = mode;
-    if (e->timing) {
+    if (e->timing || (e->fused && !step_graph())) {
         enqueue_step(e, d_q, d_out, mode);
         return;
     }
@@ -1630,6 +1664,7 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
             t.group_scores = reinterpret_cast<double*>(e->h_res_dev + e->off_gs);
             t.unit_flags = reinterpret_cast<uint32_t*>(e->h_res_dev + e->off_fl);
             t.tokens = reinterpret_cast<unsigned long long*>(e->h_res_dev + e->off_tok);
+            t.done = e->h_done_dev;  // the probe's last CTA sets it after its writes
         }
         auto enqueue = [&] {
             if (zc)
@@ -1691,16 +1726,16 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
                 kp.extra = nullptr;
                 CK(cudaGraphExecKernelNodeSetParams(ge.exec, ge.probe, &kp));
             }
+            *reinterpret_cast<volatile uint32_t*>(e->h_done) = 0u;
             CK(cudaGraphLaunch(ge.exec, e->stream));
+            finish_io(e);  // spins on the completion word
         } else {
             enqueue();
-        }
-        CK(cudaEventRecord(e->ev_in, e->stream));
-        // head scores, group scores and flags are contiguous in the result block
-        if (!zc)
+            // head scores, group scores and flags are contiguous in the result block
             CK(cudaMemcpyAsync(e->h_res + e->off_hs, e->d_res + e->off_hs, e->off_status - e->off_hs,
                                cudaMemcpyDeviceToHost, e->stream));
-        CK(cudaStreamSynchronize(e->stream));
+            CK(cudaStreamSynchronize(e->stream));
+        }
         const auto* hs = reinterpret_cast<const double*>(e->h_res + e->off_hs);
         const auto* gs = reinterpret_cast<const double*>(e->h_res + e->off_gs);
         const auto* fl = reinterpret_cast<const uint32_t*>(e->h_res + e->off_fl);

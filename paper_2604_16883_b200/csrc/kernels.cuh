@@ -113,6 +113,7 @@ struct DevTables {
     float* partials;             // [U][S][r*(D+2)]
     uint32_t B, Hq, Hkv, r, D, cap, S, grid;
     float qscale;                // (1/sqrt(D)) * log2(e)
+    uint32_t* done;              // probe: optional completion word in mapped host memory (set last)
 };
 
 // ============================================================================
@@ -296,6 +297,16 @@ __global__ void __launch_bounds__(kProbeThreads, 1) probe_kernel(DevTables t, co
         t.ws->n_active = a_tot;
         t.ws->chunk_tokens = Ck;
         t.ws->error = 0;
+    }
+    if (t.done) {
+        // score collection: the scores went to mapped host memory; make the
+        // whole CTA's writes visible system-wide, then set the word the host
+        // spins on (no kernel-retire -> stream-sync round trip)
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            ptx::st_release_sys(t.done, 1u);
+        }
     }
 }
 

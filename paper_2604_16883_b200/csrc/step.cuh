@@ -95,6 +95,7 @@ struct StepTables {
     uint32_t world, rank;
     float qscale;                  // (1/sqrt(D)) * log2(e)
     uint32_t static_pct;           // static share of the unit-affine schedule (0: one Ck chunk)
+    uint32_t prewarm;              // single-sequence steps: the last CTAs dry-run code regions first
     unsigned long long* trace;     // optional [grid][4] per-CTA globaltimer stamps
     uint32_t* done;                // optional completion word in mapped host memory (set to 1 last)
 };
@@ -158,7 +159,7 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 // (mode 1), or that partial into every rank's exchange block (mode 3).
 template <int D, int R>
 __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
-                                           uint32_t lane, size_t xoff, float* wsm) {
+                                           uint32_t lane, size_t xoff, float* wsm, bool dry) {
     // R = t.r at compile time: the partial stride is an immediate, so each of
     // the 64 acc loads is one LDG with an immediate offset.  This loop is cold
     // code at the end of every step, and instruction fetch from DRAM costs
@@ -166,7 +167,9 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
     // block is padded by 64 slots and zero-initialised, every slot holds
     // finite values, and their weights are 0.
     constexpr uint32_t r = R, PS = R * (D + 2);
-    const uint32_t n = min(ld_volatile(&t.slot_count[u]), t.S);
+    // dry: one group over slot 0 (finite, stale) and no stores -- fetches this
+    // code into L2 before the real merge needs it
+    const uint32_t n = dry ? 1u : min(ld_volatile(&t.slot_count[u]), t.S);
     const float* base = t.partials + size_t(u) * t.S * PS;
     const uint32_t d = d0 + lane;
     float mx = -INFINITY, lsum = 0.f, acc = 0.f;
@@ -218,7 +221,9 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
         acc += (a4[0] + a4[1]) + (a4[2] + a4[3]);
         __syncwarp();  // scratch reused by the next group / task
     }
-    if (t.mode == 0) {
+    if (dry) {
+        return;
+    } else if (t.mode == 0) {
         t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
     } else if (t.mode == 1) {
         float* P = t.out + size_t(u) * PS;
@@ -248,16 +253,16 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
 // warp_merge for the runtime GQA width
 template <int D>
 __device__ __forceinline__ void warp_merge_r(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
-                                             uint32_t lane, size_t xoff, float* wsm) {
+                                             uint32_t lane, size_t xoff, float* wsm, bool dry = false) {
     switch (t.r) {
-        case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff, wsm); break;
-        case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff, wsm); break;
-        case 3: warp_merge<D, 3>(t, u, h, d0, lane, xoff, wsm); break;
-        case 4: warp_merge<D, 4>(t, u, h, d0, lane, xoff, wsm); break;
-        case 5: warp_merge<D, 5>(t, u, h, d0, lane, xoff, wsm); break;
-        case 6: warp_merge<D, 6>(t, u, h, d0, lane, xoff, wsm); break;
-        case 7: warp_merge<D, 7>(t, u, h, d0, lane, xoff, wsm); break;
-        default: warp_merge<D, 8>(t, u, h, d0, lane, xoff, wsm); break;
+        case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        case 3: warp_merge<D, 3>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        case 4: warp_merge<D, 4>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        case 5: warp_merge<D, 5>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        case 6: warp_merge<D, 6>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        case 7: warp_merge<D, 7>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        default: warp_merge<D, 8>(t, u, h, d0, lane, xoff, wsm, dry); break;
     }
 }
 
@@ -310,6 +315,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t G = gridDim.x, bid = blockIdx.x;
     const uint32_t U = t_in.B * t_in.Hkv, NH = t_in.B * t_in.Hq, r = t_in.r;
+    // prologue that touches no memory the previous kernel may write: with a
+    // programmatic (PDL) launch it runs while the previous step drains
+    if (tid == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], kCWarps);
+        }
+        ptx::fence_mbar_init();
+        ptx::tma_prefetch_desc(t_in.tmk);
+        ptx::tma_prefetch_desc(t_in.tmv);
+    }
+    pdl_wait();              // no-op unless launched with programmatic serialization
+    pdl_launch();  // the next step's CTAs may take SMs as this grid's CTAs exit
     // counter-set parity: every CTA of a launch reads the same count (the
     // grid is fixed per engine and CTA b's count is written only by CTA b,
     // after its final barrier); this launch uses set `par` and zeroes the
@@ -343,17 +361,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned long long* dbg = clk + 4;  // debug cycle stamps (lead CTA, thread 0)
 #define STAMP(i) do { if (lead && tid == 0) dbg[i] = clock64(); } while (0)
     STAMP(0);
-
-    if (tid == 0) {
-        for (int s = 0; s < C::kStages; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], kCWarps);
-        }
-        ptx::fence_mbar_init();
-        ptx::tma_prefetch_desc(t.tmk);
-        ptx::tma_prefetch_desc(t.tmv);
-    }
-
     STAMP(1);
     // per-sequence tau / length into smem once (no dynamic indexing of the
     // parameter block in the loops below)
@@ -371,6 +378,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             s_len[sq] = __ldg(&t.len_g[sq]);
         }
     }
+    // Code prewarm (single-sequence steps).  A decode step in a model runs
+    // with a cold L2, so every code region a step enters for the first time
+    // is fetched from DRAM -- by all 148 SMs at once, on the critical path
+    // (cold code).  The last kPrewarmCtas CTAs first run one
+    // region each DRY (no waits, no claims, no stores): CTA G-1 one consumer
+    // iteration over stale shared memory, CTA G-2 one flush, CTA G-3 one
+    // merge task per warp over slot 0.  That brings the regions' code into L2
+    // in parallel while the other CTAs route; the dry CTAs then route and
+    // stream on dynamic claims only (no static range), so their late start
+    // costs no tail.  The dry and the real pass are one loop over the same
+    // code, so they execute the same instructions.
+    // t.prewarm: bit mask of the regions (bit 0 consumer body, 1 flush, 2
+    // merge), the k-th set bit to CTA G-1-k; bit 3: all three in CTA G-1
+    const uint32_t pw_mask = (LEAN && G >= 64u) ? (t.prewarm & 15u) : 0u;
+    const uint32_t n_pw = (pw_mask & 8u) ? 1u : __popc(pw_mask);
+    const bool pw_on = n_pw != 0u;
+    const bool prewarm = pw_on && bid >= G - n_pw;
+    uint32_t dry_regions = 0;  // prewarm CTAs: bit 0 consumer body, 1 flush, 2 merge
+    if (prewarm) {
+        uint32_t m = pw_mask;
+        for (uint32_t k = G - 1u - bid; k > 0; --k) m &= m - 1u;
+        dry_regions = (pw_mask & 8u) ? 7u : 1u << (__ffs(m) - 1);
+    }
+    unsigned long long t_stream_end = 0;
+    constexpr bool lean = LEAN;
+    bool exact_later = false;  // distributed form: exact record after streaming starts
+    uint32_t nact = 0, Ck = 0, Cs = 0, epoch = 0, peer_base = 0;
+    bool flat = false, queue_mode = true, lean_fast = false;
+    size_t xoff = 0;
+#pragma unroll 1
+    for (uint32_t pass = prewarm ? 0u : 1u; pass < 2u; ++pass) {
+    const bool dry = pass == 0u;
+    if (!dry) {
     // ======================= phase R: routing ================================
     // proxy_score (router.cpp:36-48), group_score (50-57), route (67-75) and the
     // task build (131-145).  Two forms with identical results:
@@ -384,8 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     //    in all, and a short code path (the phase is latency bound).
     //  * distributed (batched steps): each CTA scores its share of the units,
     //    one grid barrier, then every CTA scans the published decisions.
-    constexpr bool lean = LEAN;
-    bool exact_later = false;  // distributed form: exact record after streaming starts
     if (lean) {
         // Fast decision first: an fp32 estimate of every head score (warp
         // dot products of the rows already in registers).  If every group's
@@ -893,32 +931,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();  // Active list, chunk plan and misc visible to all threads
     STAMP(7);
-    const uint32_t nact = misc[kMiscNact];
-    const uint32_t Ck = misc[kMiscChunk];
-    const uint32_t Cs = misc[kMiscStatic];
-    const bool flat = !LEAN && misc[kMiscFlat] != 0;
+    nact = misc[kMiscNact];
+    Ck = misc[kMiscChunk];
+    Cs = misc[kMiscStatic];
+    flat = !LEAN && misc[kMiscFlat] != 0;
     // up to ~4 merge tasks (unit, head, 32 dims) per consumer warp: the tasks
     // are spread over every warp once its stream ends; more: the CTA that
     // streams a group's last rows merges it in line.  A/B (r01f, back to back):
     // queue mode for all takes C3-dense (2,048 tasks) 959 -> 941 us and
     // C5-routed (1,920) 309 -> 305 us, but C5-dense (5,120) 757 -> 761 us.
-    const bool queue_mode = LEAN || nact * r * (D / 32) <= 16u * G;  // (LEAN: nact <= 32; correct either way)
-    const bool lean_fast = lean && misc[kMiscFast] != 0;
+    queue_mode = LEAN || nact * r * (D / 32) <= 16u * G;  // (LEAN: nact <= 32; correct either way)
+    lean_fast = lean && misc[kMiscFast] != 0;
     // mode 3: partial slots double-buffered by step parity (a rank one step
     // ahead never overwrites partials a slower rank is still merging).  The
     // step number lives on the device (advanced by the last CTA at exit, after
     // every CTA has read it), so the graph needs no per-step parameter patch.
-    const uint32_t epoch = t.mode == 3 ? ld_volatile(&t.ss->peer_epoch) : 0u;
-    const uint32_t peer_base = t.mode == 3 ? ld_volatile(&t.ss->peer_base) : 0u;
-    const size_t xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
+    epoch = t.mode == 3 ? ld_volatile(&t.ss->peer_epoch) : 0u;
+    peer_base = t.mode == 3 ? ld_volatile(&t.ss->peer_base) : 0u;
+    xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
     if (t.trace && tid == 0) t.trace[bid * 8 + 0] = globaltimer();
     if (lead && tid == 0) clk[1] = globaltimer();
+    } else {
+        // dry pass: one Active entry (unit 0), no routing
+        if (tid == 0) {
+            act_unit[0] = 0;
+            act_len[0] = 0;
+        }
+        nact = 1;
+        __syncthreads();
+    }
 
     // ======================= phase S: stream + attend ==========================
     if (warp == 0) {
-        if (lane == 0) {
+        if (lane == 0 && !dry) {
             const uint64_t pol = ptx::policy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
@@ -963,15 +1010,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // busy with the routing record for the first microseconds, so
                 // it starts on dynamic claims; entry 0's static ranges go to
                 // CTAs nact, 2 nact, ... (chunk k - 1).
+                // (the prewarm CTAs, the last ones, have no static range either)
                 const uint32_t cpu = (G + nact - 1) / nact;  // CTAs per unit
+                const uint32_t Gs = G - n_pw;  // CTAs [0, Gs) hold static ranges
                 auto static_end = [&](uint32_t e) {        // statically covered prefix of entry e
-                    return (((G - e + nact - 1) / nact) - (e == 0 ? 1u : 0u)) * Cs;
+                    return (e < Gs ? ((Gs - e + nact - 1) / nact) - (e == 0 ? 1u : 0u) : 0u) * Cs;
                 };
                 uint32_t a = bid % nact;
                 uint32_t u = act_unit[a], L = act_len[a];
                 uint32_t first = static_end(a);
                 const uint32_t k0 = bid / nact - (a == 0 ? 1u : 0u);  // bid 0: wraps, no static range
-                uint32_t t0 = bid == 0 ? L : k0 * Cs, t1 = min(t0 + Cs, L);
+                uint32_t t0 = (bid == 0 || prewarm) ? L : k0 * Cs, t1 = min(t0 + Cs, L);
                 auto guided = [&](uint32_t hint) {
                     const uint32_t rem = L > hint ? L - hint : 0u;
                     uint32_t sz = rem / (3 * cpu);
@@ -1084,7 +1133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // first stages are in flight: single-sequence steps, CTA u mod G for
         // unit u (binary search of the sorted Active list); batched steps, the
         // CTA that routed the unit
-        if (t.mode != 1 && nact < U) {
+        if (!dry && t.mode != 1 && nact < U) {
             uint32_t z_lo = bid, z_step = G, z_hi = U;
             if (!lean) {
                 const uint32_t up = (U + G - 1) / G;
@@ -1109,7 +1158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (uint32_t k = ctid; k < r * D / 4; k += kCWarps * 32) row[k] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        if ((lean_fast && lead) || exact_later) {
+        if (!dry && ((lean_fast && lead) || exact_later)) {
             // the routing record's exact fp64 scores (the decisions were taken
             // from fp32 estimates that cleared tau by kRouteMargin), computed
             // while the first stages are in flight: thread h streams q row h and
@@ -1263,7 +1312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // slots [0, S-1) take one partial each; every later partial of the
             // unit (only a long, many-handed tail gets there) is LSE-combined
             // into slot S-1 under a per-unit lock (ovf: bit0 lock, bit1 valid)
-            const bool spill = slot >= t.S - 1;
+            const bool spill = !dry && slot >= t.S - 1;
             if (spill) {
                 if (ctid == 0) {
                     uint32_t old_v;
@@ -1292,6 +1341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (uint32_t idx = ctid; idx < r * D; idx += kCWarps * 32) {
                 const uint32_t h = idx / D, d = idx % D;
                 float mx = -INFINITY;
+                // (dry: everything but the stores below)
 #pragma unroll
                 for (int w = 0; w < kCWarps; ++w) mx = fmaxf(mx, sm_ml[(w * kMaxR + h) * 2]);
                 float acc = 0.f, lsum = 0.f;
@@ -1309,10 +1359,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     lsum = old_ml[2 * h + 1] * so + lsum * sn;
                     mx = mn;
                 }
-                P[2 * r + h * D + d] = acc;
-                if (d == 0) {
-                    P[h] = mx;
-                    P[r + h] = lsum;
+                if (!dry) {
+                    P[2 * r + h * D + d] = acc;
+                    if (d == 0) {
+                        P[h] = mx;
+                        P[r + h] = lsum;
+                    }
                 }
             }
             if (spill) {
@@ -1324,10 +1376,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             // barrier orders the CTA's writes before ctid 0's gpu-scope release
             ptx::named_bar_sync(1, kCWarps * 32);
             if (ctid == 0) {
-                const uint32_t done = (queue_mode ? ptx::atom_add_release(&t.tokens_done[u], run_tokens)
-                                                  : ptx::atom_add_acq_rel(&t.tokens_done[u], run_tokens)) +
-                                      run_tokens;
-                misc[kMiscLast] = (done == L) ? 1u : 0u;
+                const uint32_t done =
+                    dry ? 0u
+                        : (queue_mode ? ptx::atom_add_release(&t.tokens_done[u], run_tokens)
+                                      : ptx::atom_add_acq_rel(&t.tokens_done[u], run_tokens)) +
+                              run_tokens;
+                misc[kMiscLast] = (!dry && done == L) ? 1u : 0u;
             }
             ptx::named_bar_sync(1, kCWarps * 32);
             if (misc[kMiscLast] && !queue_mode) merge_unit(u, L);
@@ -1336,20 +1390,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         int stage = 0;
         uint32_t phase = 0;
+        // dry pass: iteration 0 runs the body on unit 0 over stale shared
+        // memory, iteration 1 the flush (no stores), then out
+        uint32_t dry_it = 0;
         for (;;) {
-            ptx::mbar_wait(&full[stage], phase);
-            const uint32_t unit = meta[stage].unit;
+            if (dry && !(dry_regions & 3u)) break;  // merge only
+            if (!dry) ptx::mbar_wait(&full[stage], phase);
+            const uint32_t unit = dry ? (dry_it++ == 0 ? 0u : kEnd) : meta[stage].unit;
             if (unit != cur || unit == kEnd) {  // kEnd == cur when a CTA had no work
-                if (cur != kEnd) flush(cur, cur_len);  // the only flush site
+                if (cur != kEnd && !(dry && !(dry_regions & 2u))) flush(cur, cur_len);  // the only flush site
                 if (unit == kEnd) break;
                 cur = unit;
-                if (ctid == 0) my_slot = atomicAdd(&t.slot_count[unit], 1u);  // hidden by the stream
-                cur_len = meta[stage].pad;
+                if (ctid == 0 && !dry) my_slot = atomicAdd(&t.slot_count[unit], 1u);  // hidden by the stream
+                cur_len = dry ? 0u : meta[stage].pad;
                 run_tokens = 0;
                 load_q(unit);
                 reset_state();
             }
-            const uint32_t ntok = meta[stage].ntok;
+            const uint32_t ntok = dry ? ((dry_regions & 1u) ? (uint32_t)kStageTok : 0u) : meta[stage].ntok;
             run_tokens += ntok;
             const int n = (int)ntok - tb;
             if (n > 0) {
@@ -1409,7 +1467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+            if (lane == 0 && !dry) ptx::mbar_arrive(&empty[stage]);
             if (++stage == C::kStages) {
                 stage = 0;
                 phase ^= 1u;
@@ -1417,29 +1475,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     __syncthreads();
-    STAMP(9);
-    const unsigned long long t_stream_end = globaltimer();
-    if (t.trace && tid == 0) {
-        t.trace[bid * 8 + 1] = t_stream_end;
+    if (!dry) {
+        STAMP(9);
+        t_stream_end = globaltimer();
+        if (t.trace && tid == 0) t.trace[bid * 8 + 1] = t_stream_end;
     }
 
     // ======================= phase M: distributed merge ========================
     // Tasks (active entry, head, 32-dim slice) are claimed by WARPS: a warp
     // waits until its unit's last rows are counted, then merges the slice with
     // warp_merge (one L2 round trip per 64 partials, no block barrier).
-    if (queue_mode && nact > 0) {
+    if (queue_mode && nact > 0 && !(dry && !(dry_regions & 4u))) {
         constexpr uint32_t nd = D / 32;
         const uint32_t ntasks = nact * r * nd;
         for (;;) {
             uint32_t task = 0;
-            if (lane == 0) task = atomicAdd(&sc->merge_next, 1u);
+            if (lane == 0) task = dry ? warp : atomicAdd(&sc->merge_next, 1u);
             task = __shfl_sync(0xffffffffu, task, 0);
             if (task >= ntasks) break;
             const uint32_t a = task / (r * nd), rem = task % (r * nd);
             const uint32_t h = rem / nd, d = (rem % nd) * 32 + lane;
             const uint32_t u = act_unit[a];
             const uint32_t L = act_len[a];
-            if (lane == 0) {
+            if (lane == 0 && !dry) {
                 // watchdog: a unit that never completes (a bug) must not hang
                 // the GPU; after 2 s report an error and give up the task
                 const unsigned long long t_spin = globaltimer();
@@ -1452,10 +1510,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
             }
             __syncwarp();
-            warp_merge_r<D>(t, u, h, d - lane, lane, xoff, sm_o + warp * 64);
+            warp_merge_r<D>(t, u, h, d - lane, lane, xoff, sm_o + warp * 64, dry);
+            if (dry) break;
             if (h == 0 && d == 0) t.tokens[u] = L;
+            // every warp of the grid claims once, so with no more tasks than
+            // warps a second claim finds nothing: skip its L2 round trip (the
+            // dry pass claims nothing; every CTA claims in its real pass)
+            if (ntasks <= G * (kThreads / 32)) break;
         }
     }
+    if (dry) __syncthreads();  // scratch (sm_o) free before the stream
+    }  // pass
 
     // ======================= mode 3: merge every rank's partials ===============
     // Every merge task signalled every rank once (warp_merge), so this step's

@@ -43,8 +43,9 @@ for tau in (0.5, 2.0):
             a = np.array(buf, dtype=np.float64).reshape(G, 8)
             t0 = a[:, 4].min()
             rel = lambda x: (x - t0) / 1e3
+            x5 = a[:, 5][a[:, 5] > 0]
             rows.append((rel(a[:, 4]).max(), rel(a[:, 0]).max(), rel(a[:, 1]).max(), rel(a[:, 2]).max(),
-                         rel(a[:, 5][a[:, 5] > 0]).max()))
+                         rel(x5).max() if len(x5) else float("nan")))
         m = np.median(np.array(rows), axis=0)
         print(f"L={L} tau={tau} {'cold' if cold else 'warm'}: CTA start spread {m[0]:.2f}, routing end {m[1]:.2f}, "
-              f"stream end {m[2]:.2f}, merge end {m[3]:.2f}, reset {m[4]:.2f} us")
+              f"stream end {m[2]:.2f}, merge end {m[3]:.2f}, last-CTA stamp {m[4]:.2f} us")

@@ -28,7 +28,7 @@ for L in Ls:
         q = torch.from_numpy(spec.queries()[0]).cuda()
         out = torch.empty_like(q)
         st = torch.cuda.ExternalStream(cache.stream)
-        for name, tau in (("routed", 0.5), ("dense", 2.0)):
+        for name, tau in (("routed", 0.5), ("dense", 2.0))[:int(os.environ.get("AB_CASES", 2))]:
             cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(tau), excluded_layers=())
 
             def step():
@@ -42,15 +42,16 @@ for L in Ls:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            for _ in range(40):
+            nb = int(os.environ.get("AB_STEPS", 40))
+            for _ in range(nb):
                 step()
             e1.record(st)
             torch.cuda.synchronize()
-            b2b = e0.elapsed_time(e1) / 40 * 1e3
+            b2b = e0.elapsed_time(e1) / nb * 1e3
             evs = []
             with torch.cuda.stream(st):
                 torch.cuda._sleep(8_000_000)
-                for _ in range(20):
+                for _ in range(int(os.environ.get("AB_COLD", 20))):
                     flush.sum()
                     a = torch.cuda.Event(enable_timing=True)
                     b = torch.cuda.Event(enable_timing=True)
@@ -59,7 +60,11 @@ for L in Ls:
                     b.record(st)
                     evs.append((a, b))
             torch.cuda.synchronize()
-            cold = statistics.median(x.elapsed_time(y) * 1e3 for x, y in evs)
+            ts = sorted(x.elapsed_time(y) * 1e3 for x, y in evs)
+            cold = statistics.median(ts)
+            k = len(ts) // 10
+            cold_mean = statistics.fmean(ts[k:len(ts) - k])  # 10 % trimmed: event ticks are ~1 us
             P.fetch_step_info(cache)  # raises on a step-kernel error
-            res[f"{L}_{name}"] = {"b2b_us": round(b2b, 2), "flushed_us": round(cold, 2)}
+            res[f"{L}_{name}"] = {"b2b_us": round(b2b, 2), "flushed_us": round(cold, 2),
+                                  "flushed_mean_us": round(cold_mean, 2)}
 print(json.dumps(res), flush=True)
