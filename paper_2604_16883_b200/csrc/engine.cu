@@ -102,8 +102,8 @@ static uint32_t static_pct() {
     }();
     return v;
 }
-// Merge-code prewarm of the single-sequence step (StepTables.prewarm);
-// SINKR_PREWARM=0/1 overrides (A/B runs).
+// Code prewarm of the single-sequence step (StepTables.prewarm: region bit
+// mask, 8 = all regions in CTA G-1); SINKR_PREWARM overrides (A/B runs).
 static uint32_t prewarm_default() {
     static uint32_t v = [] {
         const char* s = std::getenv("SINKR_PREWARM");

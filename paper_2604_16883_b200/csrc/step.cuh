@@ -381,14 +381,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Code prewarm (single-sequence steps).  A decode step in a model runs
     // with a cold L2, so every code region a step enters for the first time
     // is fetched from DRAM -- by all 148 SMs at once, on the critical path
-    // (cold code).  The last kPrewarmCtas CTAs first run one
-    // region each DRY (no waits, no claims, no stores): CTA G-1 one consumer
-    // iteration over stale shared memory, CTA G-2 one flush, CTA G-3 one
-    // merge task per warp over slot 0.  That brings the regions' code into L2
-    // in parallel while the other CTAs route; the dry CTAs then route and
-    // stream on dynamic claims only (no static range), so their late start
-    // costs no tail.  The dry and the real pass are one loop over the same
-    // code, so they execute the same instructions.
+    // (cold code).  The last CTA(s) first run code regions DRY
+    // (no waits, no claims, no stores): one consumer iteration over stale
+    // shared memory, one flush, one merge task per warp over slot 0.  That
+    // brings the regions' code into L2 while the other CTAs route; the dry
+    // CTAs then route and stream on dynamic claims only (no static range), so
+    // their late start costs no tail.  The dry and the real pass are one loop
+    // over the same code, so they execute the same instructions.  Default
+    // (engine): all three regions in CTA G-1 -- splitting them over three
+    // CTAs fetched faster but cost 2.5 us back to back at 512K
+    // (profiles/r02_prewarm_ab.txt).
     // t.prewarm: bit mask of the regions (bit 0 consumer body, 1 flush, 2
     // merge), the k-th set bit to CTA G-1-k; bit 3: all three in CTA G-1
     const uint32_t pw_mask = (LEAN && G >= 64u) ? (t.prewarm & 15u) : 0u;
