@@ -516,6 +516,18 @@ def next_rows(P, torch, args, spec_cls, peak):
         for _ in range(50):
             cal.collect_scores(cache, q, 0)
         gpu_us = (time.perf_counter() - t0) / 50 * 1e6
+        # a calibration length's samples in one launch (sinkr_collect_scores_batch)
+        nb = 128
+        qb = np.stack([spec_cls(**SHAPE, length=32768, sink_fraction=0.625,
+                                seed=args.seed + 1 + i).queries()[0] for i in range(nb)])
+        for _ in range(3):
+            cal.collect_scores_batch(cache, qb, 0)
+        tb = []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            cal.collect_scores_batch(cache, qb, 0)
+            tb.append(time.perf_counter() - t0)
+        batch_us = statistics.median(tb) / nb * 1e6
         k = np.stack([cache.historical(0, g, 0, spec.length)[0] for g in range(8)])
         v = np.stack([cache.historical(0, g, 0, spec.length)[1] for g in range(8)])
     rc = oracle.RefCache(oracle.ref(), 1, 32, 8, 128, spec.length)
@@ -529,10 +541,12 @@ def next_rows(P, torch, args, spec_cls, peak):
         ts.append(time.perf_counter() - t0)
     out["f1_score_collection"] = {
         "context": spec.length, "gpu_us_per_sample": round(gpu_us, 1),
+        "gpu_us_per_sample_batched": round(batch_us, 2), "batch": nb,
         "reference_observe_only_step_us": round(statistics.median(ts) * 1e6, 1),
         "reference_threads": threads,
-        "note": "collect_scores (blocking C-ABI call: H2D q, probe kernel writing the scores into mapped host memory) vs the "
-                "reference's observe-only routed_decode_step, which its calibration runs per sample"}
+        "note": "collect_scores (blocking C-ABI call: H2D q, probe kernel writing the scores into mapped host memory) "
+                "and collect_scores_batch (one call and one launch for `batch` samples of a length, median of 10) "
+                "vs the reference's observe-only routed_decode_step, which its calibration runs per sample"}
     # f2: snapshot replay, reference-written snapshot of the same cache
     with tempfile.TemporaryDirectory() as d:
         rc.save_snapshot(d)
@@ -541,6 +555,15 @@ def next_rows(P, torch, args, spec_cls, peak):
         c2 = P.KvCache.load_snapshot(d)
         ours_s = time.perf_counter() - t0
         c2.close()
+        # the replay alone (engine already created): file reads + uploads +
+        # device conversion, pipelined across slots
+        reps = []
+        for _ in range(3):
+            with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as c3:
+                t0 = time.perf_counter()
+                c3.load_snapshot_into(d)
+                reps.append(time.perf_counter() - t0)
+        replay_s = min(reps)
         t0 = time.perf_counter()
         r2 = oracle.ref().load_snapshot(d, 1, 32, 8, 128)
         ref_s = time.perf_counter() - t0
@@ -548,9 +571,13 @@ def next_rows(P, torch, args, spec_cls, peak):
     rc.close()
     out["f2_snapshot_load"] = {"context": spec.length, "bytes": nbytes,
                                "engine_s": round(ours_s, 3), "engine_gbs": round(nbytes / ours_s / 1e9, 2),
+                               "replay_s": round(replay_s, 3), "replay_gbs": round(nbytes / replay_s / 1e9, 2),
                                "reference_s": round(ref_s, 3),
-                               "note": "reference-written SNKT snapshot; engine: file read + one H2D + "
-                                       "device bf16 conversion per slot; reference: row-by-row append"}
+                               "note": "reference-written SNKT snapshot; engine_s: load_snapshot (engine "
+                                       "creation + replay); replay_s: load_snapshot_into an existing engine "
+                                       "(best of 3): file reads into pinned memory, upload and device bf16 "
+                                       "conversion pipelined across slots; reference: load_snapshot, "
+                                       "row-by-row append"}
     # f4: BOS mass over the headline cache (K rows of all 8 groups, 512K)
     L = args.length
     spec = spec_cls(**SHAPE, length=L, sink_fraction=args.sink_fraction, seed=args.seed)

@@ -349,6 +349,13 @@ sinkr_status sinkr_load_profile(const char* path, sinkr_profile* out);
 sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t layer,
                                   const sinkr_routing_config* config, double* head_scores,
                                   double* group_scores, int32_t* sink);
+/* The same for n_samples query sets over the same cache layer in one launch
+ * (a calibration length's samples): queries [n][B][H_q][D]; head_scores
+ * [n][B][H_q], group_scores [n][B][H_kv], sink [n][B][H_kv] (each may be
+ * NULL).  Bit-identical to n sinkr_collect_scores calls. */
+sinkr_status sinkr_collect_scores_batch(sinkr_engine* e, const float* queries, size_t n_samples,
+                                        size_t layer, const sinkr_routing_config* config,
+                                        double* head_scores, double* group_scores, int32_t* sink);
 
 /* ---- snapshots (kv_cache.hpp:72-80, tensor.hpp:86-96) -----
  * SNKT tensor files and the snapshot directory layout of the reference

@@ -102,7 +102,7 @@ EXPORTS = (
     # calibration (f1)
     "sinkr_profile_default", "sinkr_profile_constant", "sinkr_sweep", "sinkr_skip_ratio_at",
     "sinkr_solve_threshold", "sinkr_fit_cubic", "sinkr_calibrate", "sinkr_save_profile",
-    "sinkr_load_profile", "sinkr_collect_scores",
+    "sinkr_load_profile", "sinkr_collect_scores", "sinkr_collect_scores_batch",
     # snapshots / device prefill (f2)
     "sinkr_write_tensor", "sinkr_read_tensor", "sinkr_snkt_file_size", "sinkr_save_snapshot",
     "sinkr_load_snapshot", "sinkr_load_snapshot_into", "sinkr_kv_append_device_f32",
@@ -165,6 +165,7 @@ def lib():
             "sinkr_load_profile": [C.c_char_p, vp],
             "sinkr_profile_default": [vp],
             "sinkr_collect_scores": [vp, vp, sz, vp, vp, vp, vp],
+            "sinkr_collect_scores_batch": [vp, vp, sz, sz, vp, vp, vp, vp],
             "sinkr_write_tensor": [C.c_char_p, vp, sz, vp],
             "sinkr_read_tensor": [C.c_char_p, vp, vp, vp, sz],
             "sinkr_save_snapshot": [vp, sz, C.c_char_p],

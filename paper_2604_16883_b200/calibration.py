@@ -214,17 +214,46 @@ def collect_scores(cache: KvCache, queries, layer: int, config: Optional[Routing
     return hs, gs, sk.astype(bool)
 
 
+def collect_scores_batch(cache: KvCache, queries, layer: int, config: Optional[RoutingConfig] = None):
+    """collect_scores for n query samples over the same cache layer in ONE
+    launch (sinkr_collect_scores_batch): queries [n][B][H_q][D] ->
+    (head_scores [n][B*H_q], group_scores [n][B*H_kv], sink [n][B*H_kv] bool),
+    bit-identical to n collect_scores calls."""
+    cfg = cache.config()
+    B = cfg.num_seqs
+    per = B * cfg.num_q_heads * cfg.head_dim
+    q = np.ascontiguousarray(queries, dtype=np.float32)
+    if q.size == 0 or q.size % per:
+        raise ValueError("queries must be n x B x H_q x D for one layer")
+    n = q.size // per
+    hs = np.zeros((n, B * cfg.num_q_heads), dtype=np.float64)
+    gs = np.zeros((n, B * cfg.num_kv_heads), dtype=np.float64)
+    sk = np.zeros((n, B * cfg.num_kv_heads), dtype=np.int32)
+    keep = None
+    cptr = None
+    if config is not None:
+        c, keep = config._c()
+        cptr = C.byref(c)
+    check(lib().sinkr_collect_scores_batch(cache.handle, q.ctypes.data, C.c_size_t(n),
+                                           C.c_size_t(layer), cptr, hs.ctypes.data,
+                                           gs.ctypes.data, sk.ctypes.data))
+    del keep
+    return hs, gs, sk.astype(bool)
+
+
 def gpu_score_collector(cache: KvCache, query_source: Callable[[int, int], np.ndarray],
                         layers: Sequence[int], samples: int) -> ScoreCollector:
     """A ScoreCollector over an engine whose cache is (re)filled per length by
     `query_source(length, sample)` -> queries [B][H_q][D]; every group score of
     every sample and layer joins the population (skipping disabled)."""
     def collect(length: int) -> ScorePopulation:
+        # all samples of a length in one launch per layer; the population
+        # keeps the reference's order (sample-major, then layer)
         pop = ScorePopulation()
+        qs = np.stack([np.asarray(query_source(length, s), dtype=np.float32) for s in range(samples)])
+        per_layer = [collect_scores_batch(cache, qs, layer)[1] for layer in layers]
         for s in range(samples):
-            q = query_source(length, s)
-            for layer in layers:
-                _, gs, _ = collect_scores(cache, q, layer)
-                pop.extend(gs, layer, length)
+            for li, layer in enumerate(layers):
+                pop.extend(per_layer[li][s], layer, length)
         return pop
     return collect

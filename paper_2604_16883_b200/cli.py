@@ -109,8 +109,8 @@ def cmd_calibrate(args) -> int:
         pop = cal.ScorePopulation()
         D, r = args.dim, args.hq // args.hkv
         mu = args.score_base + args.score_shift * L / max(lengths)
-        for _ in range(args.samples):
-            q = np.zeros((args.hq, D), dtype=np.float32)
+        qs = np.zeros((args.samples, args.hq, D), dtype=np.float32)
+        for q in qs:
             for g in range(args.hkv):
                 k0 = spec.first_rows(0, g)[0].astype(np.float64)
                 kh = k0 / np.linalg.norm(k0)
@@ -120,9 +120,12 @@ def cmd_calibrate(args) -> int:
                     n /= np.linalg.norm(n)
                     c = float(np.clip(rng.normal(mu, args.score_spread), -0.95, 0.95))
                     q[g * r + i] = np.sqrt(D) * (c * kh + np.sqrt(1 - c * c) * n)
+        # every sample of this length in one launch per layer (population in
+        # the reference's sample-major order)
+        per_layer = [cal.collect_scores_batch(cache, qs, layer)[1] for layer in range(args.layers)]
+        for s in range(args.samples):
             for layer in range(args.layers):
-                _, gs, _ = cal.collect_scores(cache, q, layer)
-                pop.extend(gs, layer, L)
+                pop.extend(per_layer[layer][s], layer, L)
         return pop
 
     excluded = tuple(_ints(args.excluded)) if args.excluded else ()

@@ -150,6 +150,8 @@ struct sinkr_engine {
     // the blocking call spins on it instead of synchronising the stream
     uint32_t* h_done = nullptr;
     uint32_t* h_done_dev = nullptr;
+    uint8_t* d_score_scratch = nullptr;  // sinkr_collect_scores_batch (grown on demand)
+    size_t score_scratch_bytes = 0;
 
     dev::WorkState* d_ws = nullptr;
     uint32_t* d_active = nullptr;
@@ -998,6 +1000,10 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
             CK(cudaFuncSetAttribute(dev::probe_kernel<128>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, probe_smem(e)));
+            for (const void* fn : {(const void*)dev::score_batch_kernel<32>, (const void*)dev::score_batch_kernel<64>,
+                                   (const void*)dev::score_batch_kernel<128>})
+                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        2 * dev::kScoreHeads * (int)(e->D + 1) * 8));
             // one shared-memory carveout for all step kernels: switching the
             // L1/smem split between back-to-back kernels stalls the SMs
             for (const void* fn : {(const void*)dev::probe_kernel<32>, (const void*)dev::probe_kernel<64>,
@@ -1061,6 +1067,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     if (e->h_in) cudaFreeHost(e->h_in);
     if (e->h_res) cudaFreeHost(e->h_res);
     if (e->h_done) cudaFreeHost(e->h_done);
+    if (e->d_score_scratch) cudaFree(e->d_score_scratch);
     if (e->h_len_stage) cudaFreeHost(e->h_len_stage);
     cudaFree(e->d_len);
     if (e->h_bos) cudaFreeHost(e->h_bos);
@@ -1746,6 +1753,77 @@ sinkr_status sinkr_collect_scores(sinkr_engine* e, const float* queries, size_t 
     });
 }
 
+sinkr_status sinkr_collect_scores_batch(sinkr_engine* e, const float* queries, size_t n_samples,
+                                        size_t layer, const sinkr_routing_config* config,
+                                        double* head_scores, double* group_scores, int32_t* sink) {
+    return guard([&] {
+        if (!e || !queries) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        if (layer >= e->layers) fail(SINKR_OUT_OF_RANGE, "layer index out of range");
+        if (n_samples == 0) return;
+        CK(cudaSetDevice(e->device));
+        const size_t NH = e->B * e->cfg.num_q_heads, U = e->U, D = e->D;
+        for (size_t s = 0; s < e->B; ++s)
+            for (size_t g = 0; g < e->cfg.num_kv_heads; ++g)
+                if (!e->anchored[e->slot_index(layer, s, g)])
+                    fail(SINKR_RUNTIME_ERROR, "anchor requested from empty cache slot");
+        if (n_samples * U > (size_t)0xFFFFFFFFu / 2) fail(SINKR_INVALID_ARGUMENT, "too many samples");
+        // device scratch: tau [B] | queries [n][NH][D] | head [n][NH] | group [n][U] | sink [n][U]
+        const size_t off_q = align_up(e->B * 8, 256);
+        const size_t off_h = align_up(off_q + n_samples * NH * D * 4, 256);
+        const size_t off_g = align_up(off_h + n_samples * NH * 8, 256);
+        const size_t off_s = align_up(off_g + n_samples * U * 8, 256);
+        const size_t bytes = off_s + n_samples * U * 4;
+        if (bytes > e->score_scratch_bytes) {
+            if (e->d_score_scratch) CK(cudaFree(e->d_score_scratch));
+            e->d_score_scratch = nullptr;
+            e->score_scratch_bytes = 0;
+            CK(cudaMalloc(&e->d_score_scratch, bytes));
+            e->score_scratch_bytes = bytes;
+        }
+        uint8_t* d = e->d_score_scratch;
+        std::vector<double> tau(e->B, 0.0);
+        dev::ScoreBatchArgs a{};
+        if (config) {
+            for (size_t s = 0; s < e->B; ++s) {
+                const size_t L = token_count(e, s);
+                if (L == 0) fail(SINKR_RUNTIME_ERROR, "routed decode over an empty cache");
+                tau[s] = threshold_for_length(L, config->profile);
+            }
+            a.flags = (config->sink_on_tie ? dev::kSinkOnTie : 0u) |
+                      (layer_excluded(layer, *config) ? dev::kLayerExcluded : 0u);
+            a.has_cfg = 1;
+        }
+        CK(cudaMemcpyAsync(d, tau.data(), e->B * 8, cudaMemcpyHostToDevice, e->stream));
+        CK(cudaMemcpyAsync(d + off_q, queries, n_samples * NH * D * 4, cudaMemcpyHostToDevice, e->stream));
+        a.q = reinterpret_cast<const float*>(d + off_q);
+        a.anchors = e->d_anchor + layer * U * D;
+        a.anchor_norm = e->d_anchor_norm + layer * U;
+        a.tau = reinterpret_cast<const double*>(d);
+        a.head_scores = reinterpret_cast<double*>(d + off_h);
+        a.group_scores = reinterpret_cast<double*>(d + off_g);
+        a.sink = reinterpret_cast<int32_t*>(d + off_s);
+        a.n = (uint32_t)n_samples;
+        a.U = (uint32_t)U;
+        a.Hkv = (uint32_t)e->cfg.num_kv_heads;
+        a.r = (uint32_t)e->r;
+        a.units_per_cta = (uint32_t)std::max<size_t>(1, dev::kScoreHeads / e->r);
+        const unsigned grid = (unsigned)((n_samples * U + a.units_per_cta - 1) / a.units_per_cta);
+        const size_t smem = 2 * dev::kScoreHeads * (D + 1) * 8;
+        switch (D) {
+            case 32: dev::score_batch_kernel<32><<<grid, dev::kScoreThreads, smem, e->stream>>>(a); break;
+            case 64: dev::score_batch_kernel<64><<<grid, dev::kScoreThreads, smem, e->stream>>>(a); break;
+            default: dev::score_batch_kernel<128><<<grid, dev::kScoreThreads, smem, e->stream>>>(a); break;
+        }
+        CK(cudaGetLastError());
+        if (head_scores)
+            CK(cudaMemcpyAsync(head_scores, d + off_h, n_samples * NH * 8, cudaMemcpyDeviceToHost, e->stream));
+        if (group_scores)
+            CK(cudaMemcpyAsync(group_scores, d + off_g, n_samples * U * 8, cudaMemcpyDeviceToHost, e->stream));
+        if (sink) CK(cudaMemcpyAsync(sink, d + off_s, n_samples * U * 4, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+    });
+}
+
 static void launch_bos(sinkr_engine* e, const dev::BosArgs& a) {
 #define SINKR_BOS_LAUNCH(DD)                                                                     \
     {                                                                                            \
@@ -2153,3 +2231,84 @@ sinkr_status sinkr_set_timing(sinkr_engine* e, int enabled) {
 }
 
 }  // extern "C"
+
+// ---- pipelined multi-slot f32 append (snapshot replay) ----------------------
+namespace sinkr {
+namespace host {
+
+void append_slots_f32(sinkr_engine* e, size_t seq, size_t rows, const SlotReader& read) {
+    if (!e) fail(SINKR_INVALID_ARGUMENT, "null engine");
+    CK(cudaSetDevice(e->device));
+    const size_t H = e->cfg.num_kv_heads, nslots = e->layers * H, D = e->D, n = rows * D;
+    if (rows == 0 || nslots == 0) return;
+    for (size_t l = 0; l < e->layers; ++l)
+        for (size_t h = 0; h < H; ++h) {
+            check_slot(e, seq, l, h);
+            if (e->len[e->slot_index(l, seq, h)] + rows > e->cap)
+                fail(SINKR_RUNTIME_ERROR, "kv cache overflow: slot at capacity " + std::to_string(e->cap));
+        }
+    struct Res {
+        cudaStream_t s = nullptr;
+        float* hp[2] = {};
+        float* dp = nullptr;
+        double* d_n64 = nullptr;
+        cudaEvent_t ev[2] = {};
+        ~Res() {
+            if (s) cudaStreamSynchronize(s);  // no copy may still read the pinned buffers
+            for (auto* p : hp)
+                if (p) cudaFreeHost(p);
+            if (dp) cudaFree(dp);
+            if (d_n64) cudaFree(d_n64);
+            for (auto v : ev)
+                if (v) cudaEventDestroy(v);
+        }
+    } r;
+    r.s = e->stream;
+    const size_t nv = (n + 3) / 4 * 4;  // 16-byte aligned halves
+    for (auto*& p : r.hp) CK(cudaHostAlloc(reinterpret_cast<void**>(&p), 2 * nv * 4, cudaHostAllocDefault));
+    CK(cudaMalloc(&r.dp, 4 * nv * 4));
+    CK(cudaMalloc(&r.d_n64, nslots * 8));
+    for (auto& v : r.ev) CK(cudaEventCreateWithFlags(&v, cudaEventDisableTiming));
+    std::vector<uint8_t> first(nslots, 0);
+    read(0, 0, r.hp[0], r.hp[0] + nv);
+    for (size_t i = 0; i < nslots; ++i) {
+        const int b = (int)(i & 1);
+        const size_t l = i / H, h = i % H, idx = e->slot_index(l, seq, h);
+        float* dk = r.dp + 2 * nv * b;
+        float* dv = dk + nv;
+        CK(cudaMemcpyAsync(dk, r.hp[b], 2 * nv * 4, cudaMemcpyHostToDevice, e->stream));
+        const size_t off = (e->row_base(l, seq, h) + e->len[idx]) * D;
+        const int grid = (int)std::min<size_t>((n / 4 + 255) / 256 + 1, (size_t)e->num_sms * 8);
+        dev::f32_to_bf16_kernel<<<grid, 256, 0, e->stream>>>(dk, e->d_k + off, n);
+        dev::f32_to_bf16_kernel<<<grid, 256, 0, e->stream>>>(dv, e->d_v + off, n);
+        if (e->len[idx] == 0) {
+            first[i] = 1;
+            dev::anchor_capture_kernel<<<1, 32, 0, e->stream>>>(e->d_k + idx * e->cap * D, (uint32_t)D,
+                                                                 e->d_anchor + idx * D, e->d_anchor_norm + idx,
+                                                                 r.d_n64 + i);
+        }
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(r.ev[b], e->stream));
+        if (i + 1 < nslots) {
+            CK(cudaEventSynchronize(r.ev[b ^ 1]));  // slot i-1 done: its pinned buffer is free
+            read((i + 1) / H, (i + 1) % H, r.hp[b ^ 1], r.hp[b ^ 1] + nv);
+        }
+    }
+    std::vector<double> norms(nslots, 0.0);
+    CK(cudaMemcpyAsync(norms.data(), r.d_n64, nslots * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (size_t i = 0; i < nslots; ++i) {
+        const size_t idx = e->slot_index(i / H, seq, i % H);
+        if (first[i]) {
+            CK(cudaMemcpy(e->h_anchor.data() + idx * D, e->d_anchor + idx * D, D * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(e->h_anchor_norm.data() + idx, e->d_anchor_norm + idx, 4, cudaMemcpyDeviceToHost));
+            if (norms[i] < 1e-12) fail(SINKR_RUNTIME_ERROR, "degenerate anchor: first-token key norm below 1e-12");
+            e->anchored[idx] = 1;
+        }
+        e->len[idx] += rows;
+        e->dlen_dirty = true;
+    }
+}
+
+}  // namespace host
+}  // namespace sinkr

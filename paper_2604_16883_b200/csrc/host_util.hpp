@@ -4,6 +4,8 @@
 // INVALID_ARGUMENT / OUT_OF_RANGE / RUNTIME_ERROR / LOGIC_ERROR.
 #pragma once
 
+#include <cstddef>
+#include <functional>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -47,6 +49,15 @@ sinkr_status guard(F&& f) {
         return SINKR_RUNTIME_ERROR;
     }
 }
+
+// Appends `rows` f32 rows to EVERY (layer, kv_head) slot of sequence `seq`,
+// the rows of each slot produced by read(layer, kv_head, k, v) into pinned
+// host memory.  Pipelined (engine.cu): slot i's upload and device bf16
+// conversion overlap read(i+1); the anchors of first rows are captured on
+// the device and validated in slot order as the sequential appends would
+// (a degenerate anchor fails at its slot, earlier slots stay appended).
+using SlotReader = std::function<void(size_t layer, size_t kv_head, float* k, float* v)>;
+void append_slots_f32(sinkr_engine* e, size_t seq, size_t rows, const SlotReader& read);
 
 }  // namespace host
 }  // namespace sinkr

@@ -117,6 +117,99 @@ struct DevTables {
 };
 
 // ============================================================================
+// score_batch: the score-collection mode over n query samples
+// of one cache layer in one launch -- proxy_score (router.cpp:36-48),
+// group_score (50-57) and the route compare (67-75,113-120), bit-exact with
+// the probe kernel (the same products, sequential chains and IEEE
+// sqrt/div/clamp).  CTA c takes units_per_cta whole units of the n x U
+// (sample, unit) space, so a group's mean needs no other CTA.
+// ============================================================================
+struct ScoreBatchArgs {
+    const float* q;             // [n][B*Hq][D]
+    const float* anchors;       // this layer's [U][D]
+    const float* anchor_norm;   // this layer's [U]
+    const double* tau;          // [B] (cfg only)
+    double* head_scores;        // [n][B*Hq]
+    double* group_scores;       // [n][U]
+    int32_t* sink;              // [n][U]
+    uint32_t n, U, Hkv, r, units_per_cta, flags, has_cfg;
+};
+constexpr int kScoreThreads = 128;
+constexpr int kScoreHeads = 64;  // heads per CTA (whole units)
+
+template <int D>
+__global__ void __launch_bounds__(kScoreThreads) score_batch_kernel(const ScoreBatchArgs a) {
+    constexpr int DP = D + 1;
+    extern __shared__ double s_prod[];  // [2][kScoreHeads][D+1]: q*k0, q*q
+    __shared__ double s_sc[kScoreHeads];
+    __shared__ uint32_t s_dg[kScoreHeads];
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t r = a.r, NH = a.U * r;
+    const uint32_t gu0 = blockIdx.x * a.units_per_cta;  // first (sample, unit) of this CTA
+    const uint32_t nu = min(a.units_per_cta, a.n * a.U - gu0);
+    const uint32_t nh = nu * r;
+    // exact fp64 products (f32 x f32 fits in 53 bits) into odd-stride rows
+    for (uint32_t hl = warp; hl < nh; hl += kScoreThreads / 32) {
+        const uint32_t gu = gu0 + hl / r, smp = gu / a.U, u = gu % a.U;
+        const float* qrow = a.q + (size_t(smp) * NH + u * r + hl % r) * D;
+        const float* krow = a.anchors + size_t(u) * D;
+        for (uint32_t j = lane; j < (uint32_t)D; j += 32) {
+            const double qj = (double)__ldg(qrow + j);
+            s_prod[hl * DP + j] = __dmul_rn(qj, (double)__ldg(krow + j));
+            s_prod[(kScoreHeads + hl) * DP + j] = __dmul_rn(qj, qj);
+        }
+    }
+    __syncthreads();
+    // thread h: the dot chain of head h; thread 64+h: its |q|^2 chain -- each a
+    // sequential sum in index order (router.cpp:40-43)
+    const uint32_t hl = tid % kScoreHeads;
+    double acc = 0.0;
+    if (hl < nh) {
+        const double* pr = s_prod + ((tid < (uint32_t)kScoreHeads ? 0 : kScoreHeads) + hl) * DP;
+#pragma unroll 16
+        for (uint32_t j = 0; j < (uint32_t)D; ++j) acc = __dadd_rn(acc, pr[j]);
+    }
+    __syncthreads();  // products dead: reuse row 0 of the second half for the |q|^2 sums
+    double* s_qq = s_prod + kScoreHeads * DP;
+    if (tid >= (uint32_t)kScoreHeads && hl < nh) s_qq[hl] = acc;
+    __syncthreads();
+    if (tid < nh) {
+        const uint32_t gu = gu0 + tid / r, smp = gu / a.U, u = gu % a.U;
+        const double qn = __dsqrt_rn(s_qq[tid]);
+        double sc = 0.0;
+        uint32_t dg = 0;
+        if (qn < 1e-12) {
+            dg = 1;
+        } else {
+            sc = __ddiv_rn(acc, __dmul_rn(qn, (double)__ldg(&a.anchor_norm[u])));
+            sc = sc < -1.0 ? -1.0 : (1.0 < sc ? 1.0 : sc);  // std::clamp
+        }
+        s_sc[tid] = sc;
+        s_dg[tid] = dg;
+        a.head_scores[size_t(smp) * NH + u * r + tid % r] = sc;
+    }
+    __syncthreads();
+    if (tid < nu) {
+        const uint32_t gu = gu0 + tid, smp = gu / a.U, u = gu % a.U;
+        double sum = 0.0;
+        uint32_t degen = 0;
+        for (uint32_t i = 0; i < r; ++i) {
+            sum = __dadd_rn(sum, s_sc[tid * r + i]);
+            degen |= s_dg[tid * r + i];
+        }
+        const double S = __ddiv_rn(sum, (double)r);
+        a.group_scores[size_t(smp) * a.U + u] = S;
+        bool sink = false;
+        if (a.has_cfg) {
+            const double tau = a.tau[u / a.Hkv];
+            const bool over = (a.flags & kSinkOnTie) ? (S >= tau) : (S > tau);
+            sink = over && !(a.flags & kLayerExcluded) && !degen;
+        }
+        a.sink[size_t(smp) * a.U + u] = sink ? 1 : 0;
+    }
+}
+
+// ============================================================================
 // probe: bit-exact with router.cpp:36-75.  Each CTA scores a tile of
 // kProbeHeads query heads: all threads form the exact fp64 products
 // (f32 x f32 is exact in fp64) into shared memory, then one thread per head

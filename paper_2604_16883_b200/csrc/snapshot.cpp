@@ -4,8 +4,9 @@
 // dims | row-major f32 payload, little-endian, tensor.hpp:86-91) and
 // kv_cache.cpp:123-191 (manifest.json + k_l{l}_h{h}.snkt / v_l{l}_h{h}.snkt
 // per slot, f32 [length][head_dim]).  Snapshots written here load in the
-// reference and vice versa (tests/test_snapshot.py).  Replay uploads each
-// slot once and converts it to bf16 on the device (sinkr_kv_append_device_f32).
+// reference and vice versa (tests/test_snapshot.py).  Replay reads each slot
+// into pinned memory, uploads it once and converts it to bf16 on the device,
+// pipelined across slots (host::append_slots_f32 in engine.cu).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -20,6 +21,7 @@
 #include "host_util.hpp"
 #include "json_lite.hpp"
 
+using sinkr::host::append_slots_f32;
 using sinkr::host::fail;
 using sinkr::host::guard;
 
@@ -133,25 +135,6 @@ Manifest read_manifest(const fs::path& dir) {
     return m;
 }
 
-// device staging for one slot's K and V rows (f32), reused across slots
-struct Staging {
-    float* d = nullptr;
-    size_t cap = 0;
-    ~Staging() {
-        if (d) cudaFree(d);
-    }
-    float* get(size_t floats) {
-        if (floats > cap) {
-            if (d) cudaFree(d);
-            d = nullptr;
-            if (cudaMalloc(&d, floats * 4) != cudaSuccess)
-                fail(SINKR_CUDA_ERROR, "cudaMalloc of the snapshot staging buffer failed");
-            cap = floats;
-        }
-        return d;
-    }
-};
-
 void replay_into(sinkr_engine* e, size_t seq, const fs::path& dir, const Manifest& m) {
     sinkr_cache_config have{};
     check(sinkr_engine_config(e, &have));
@@ -161,23 +144,15 @@ void replay_into(sinkr_engine* e, size_t seq, const fs::path& dir, const Manifes
     if (m.length > have.capacity)
         fail(SINKR_RUNTIME_ERROR, "kv cache overflow: slot at capacity " + std::to_string(have.capacity));
     const size_t D = m.cfg.head_dim, n = m.length * D;
-    std::vector<float> hk(n), hv(n);
-    Staging st;
-    float* dk = st.get(2 * n + 4);
-    float* dv = dk + ((n + 3) / 4) * 4;
-    for (size_t l = 0; l < m.cfg.num_layers; ++l) {
-        for (size_t h = 0; h < m.cfg.num_kv_heads; ++h) {
-            const auto kd = read_snkt((dir / slot_file("k", l, h)).string(), hk.data(), n, true);
-            const auto vd = read_snkt((dir / slot_file("v", l, h)).string(), hv.data(), n, true);
-            const std::vector<uint64_t> want = {m.length, D};
-            if (kd != want || vd != want)
-                fail(SINKR_RUNTIME_ERROR, "snapshot tensor shape does not match manifest");
-            if (cudaMemcpy(dk, hk.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-                cudaMemcpy(dv, hv.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-                fail(SINKR_CUDA_ERROR, "snapshot upload failed");
-            check(sinkr_kv_append_device_f32(e, seq, l, h, dk, dv, m.length));
-        }
-    }
+    const std::vector<uint64_t> want = {m.length, D};
+    // every slot's rows straight into the engine's pinned staging; the
+    // upload and device conversion of slot i overlap the file reads of i+1
+    append_slots_f32(e, seq, m.length, [&](size_t l, size_t h, float* k, float* v) {
+        const auto kd = read_snkt((dir / slot_file("k", l, h)).string(), k, n, true);
+        const auto vd = read_snkt((dir / slot_file("v", l, h)).string(), v, n, true);
+        if (kd != want || vd != want)
+            fail(SINKR_RUNTIME_ERROR, "snapshot tensor shape does not match manifest");
+    });
 }
 
 }  // namespace

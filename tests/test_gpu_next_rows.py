@@ -55,6 +55,40 @@ def test_collect_scores_bit_exact(ref):
     assert not sink0.any()
 
 
+@pytest.mark.parametrize("hq,hkv,D,B", [(32, 8, 128, 1), (40, 8, 64, 2), (8, 8, 32, 3), (64, 8, 128, 1),
+                                         (35, 7, 128, 1)])
+def test_collect_scores_batch_matches_single(hq, hkv, D, B):
+    """sinkr_collect_scores_batch over n samples == n sinkr_collect_scores
+    calls, byte for byte (head/group scores, sink flags), including a
+    degenerate (zero) query head, sink_on_tie and an excluded layer; B = 1-3,
+    r = 1, 4, 5, 8 and D = 32 / 64 / 128 (the single call is pinned to the
+    reference by test_collect_scores_bit_exact)."""
+    rng = np.random.default_rng(hq * 131 + D)
+    L = 700
+    n = 37
+    with P.KvCache(P.CacheConfig(2, hq, hkv, D, L, B)) as cache:
+        for layer in range(2):
+            for s in range(B):
+                for g in range(hkv):
+                    k = rng.standard_normal((L, D)).astype(np.float32)
+                    cache.append(layer, g, k, k * 0.5, seq=s)
+        qs = rng.standard_normal((n, B, hq, D)).astype(np.float32)
+        qs[3, 0, 1] = 0.0  # degenerate head: never sinks
+        cfgs = [None,
+                P.RoutingConfig(profile=P.ThresholdProfile.constant(0.02), excluded_layers=()),
+                P.RoutingConfig(profile=P.ThresholdProfile.constant(0.0), excluded_layers=(),
+                                sink_on_tie=True),
+                P.RoutingConfig(profile=P.ThresholdProfile.constant(-0.5), excluded_layers=(1,))]
+        for layer in range(2):
+            for cfg in cfgs:
+                hb, gb, sb = cal.collect_scores_batch(cache, qs, layer, cfg)
+                for i in range(n):
+                    h1, g1, s1 = cal.collect_scores(cache, qs[i], layer, cfg)
+                    assert hb[i].tobytes() == h1.tobytes()
+                    assert gb[i].tobytes() == g1.tobytes()
+                    assert np.array_equal(sb[i], s1)
+
+
 def _aligned_queries(rng, k0s, r, cosines, D):
     """queries whose cosine with their group's anchor is exactly `cosines`."""
     out = np.zeros((len(k0s) * r, D), dtype=np.float32)
@@ -99,8 +133,8 @@ def test_calibration_closed_loop():
     def collect(L):
         calls.append(L)
         pop = cal.ScorePopulation()
-        for q in qs[L]:
-            _, gs, _ = cal.collect_scores(caches[L], q, 0)
+        _, gss, _ = cal.collect_scores_batch(caches[L], np.stack(qs[L]), 0)
+        for gs in gss:
             pop.extend(gs, 0, L)
         return pop
 
