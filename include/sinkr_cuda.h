@@ -244,16 +244,18 @@ sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gat
 
 /* The same split with the collective fused into the step kernel: every rank's
  * kernel writes its LSE partials straight into every rank's exchange block
- * over NVLink (peer memory), signals each rank with a system-scope atomic, and
- * its last CTA waits for all ranks' partials of the step and merges them into
- * d_outputs -- one kernel per rank per step, no NCCL call.
+ * over NVLink (peer memory) as LL words {value, step tag} (one 8-byte store:
+ * a reader that sees this step's tag sees the value, no fence, no arrival
+ * counter); the CTAs that own output elements poll the words they need from
+ * every rank and merge them into d_outputs -- one kernel per rank per step,
+ * no NCCL call.
  *   sinkr_peer_setup       allocate this rank's exchange block (world <= 8)
  *   sinkr_peer_ipc_handle  64-byte cudaIpcMemHandle of the block (all-gather it)
  *   sinkr_peer_open        map every rank's block from the gathered handles
  *   sinkr_peer_set_blocks  same, from device pointers (ranks in one process)
- * All ranks must issue the same number of peer steps (the arrival counters
- * are step-numbered); a rank that never arrives turns into a step-kernel error
- * after 2 s, never a hang. */
+ * All ranks must issue the same number of peer steps (the step tags count
+ * them); a rank that never delivers turns into a step-kernel error after
+ * 2 s (NaN outputs), never a hang. */
 sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, size_t* block_bytes);
 sinkr_status sinkr_peer_ipc_handle(sinkr_engine* e, void* handle);
 sinkr_status sinkr_peer_open(sinkr_engine* e, const void* handles);

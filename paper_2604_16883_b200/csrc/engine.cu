@@ -185,19 +185,18 @@ struct sinkr_engine {
     float bos_ms = -1.f;
     size_t h_bos_bytes = 0;
     uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [2][U]
-    uint32_t* d_cta_epoch = nullptr;    // step-kernel launches per CTA slot [grid]
+    uint32_t* d_cta_epoch = nullptr;    // [2][grid]: step-kernel launches, mode-3 steps per CTA slot
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
     // sequence-sharded peer merge (mode 3): this rank's exchange block
-    // [2][world][U][PS] f32 + arrival counter, and every rank's block mapped here
+    // [2][world][U][PS] LL words {f32, step tag}, and every rank's block mapped here
     uint8_t* d_xchg = nullptr;
-    size_t xchg_floats = 0, xchg_bytes = 0;
+    size_t xchg_words = 0, xchg_bytes = 0;
     uint32_t world = 0, rank = 0;
-    float** d_peer_xchg = nullptr;          // device array [world]
-    unsigned int** d_peer_arrive = nullptr;  // device array [world]
+    unsigned long long** d_peer_xchg = nullptr;  // device array [world]: every rank's exchange block
     std::vector<void*> ipc_opened;           // peer blocks opened through CUDA IPC
-    // a peer-merge watchdog timeout leaves arrivals of the late rank in
-    // flight (they would count toward a later step): the exchange is unusable
-    // until it is set up again
+    // a peer-merge watchdog timeout leaves the ranks' step tags out of step
+    // (the late rank still counts the step it never finished): the exchange
+    // is unusable until every rank sets it up again
     bool peer_poisoned = false;
 
     CUtensorMap tmk{}, tmv{};
@@ -296,9 +295,7 @@ struct sinkr_engine {
         t.trace = d_trace;
         if (mode == 3) {
             t.peer_xchg = d_peer_xchg;
-            t.peer_arrive = d_peer_arrive;
-            t.xchg_local = reinterpret_cast<const float*>(d_xchg);
-            t.arrive_local = reinterpret_cast<const unsigned int*>(d_xchg + xchg_floats * 4);
+            t.xchg_local = reinterpret_cast<const unsigned long long*>(d_xchg);
             t.world = world;
             t.rank = rank;
         }
@@ -571,6 +568,20 @@ void run_io_graph(sinkr_engine* e, int mode = 0, long append_layer = -1) {
     const bool zc = io_mode() == 1;
     uint8_t* res = zc ? e->h_res_dev : e->d_res;
     float* out = reinterpret_cast<float*>(res);
+    if (!step_graph()) {  // A/B: the same launches without a graph
+        if (zc) *reinterpret_cast<volatile uint32_t*>(e->h_done) = 0u;
+        launch_upload(e, append_layer >= 0 ? e->in_bytes_append : e->in_bytes);
+        if (append_layer >= 0) {
+            const float* kn = reinterpret_cast<const float*>(e->d_in + e->off_kvn);
+            launch_append(e, (size_t)append_layer, kn, kn + e->U * e->D);
+        }
+        const bool timing = e->timing;
+        e->timing = false;
+        enqueue_step(e, d_q, out, mode, res, zc ? e->h_done_dev : nullptr);
+        e->timing = timing;
+        if (!zc) CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
+        return;
+    }
     if (it == e->graphs.end()) {
         sinkr_engine::GraphEntry ge;
         CK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
@@ -939,8 +950,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMalloc(&e->d_ovf, 2 * e->U * 4));
             CK(cudaMemsetAsync(e->d_ovf, 0, 2 * e->U * 4, e->stream));
             CK(cudaMemsetAsync(e->d_tokens_done, 0, 2 * e->U * 4, e->stream));
-            CK(cudaMalloc(&e->d_cta_epoch, e->grid * 4));
-            CK(cudaMemsetAsync(e->d_cta_epoch, 0, e->grid * 4, e->stream));
+            CK(cudaMalloc(&e->d_cta_epoch, 2 * e->grid * 4));  // launches, mode-3 steps
+            CK(cudaMemsetAsync(e->d_cta_epoch, 0, 2 * e->grid * 4, e->stream));
             if (const char* tr = std::getenv("SINKR_TRACE"); tr && tr[0] == '1') {
                 CK(cudaMalloc(&e->d_trace, e->grid * 8 * 8));
                 CK(cudaMemsetAsync(e->d_trace, 0, e->grid * 8 * 8, e->stream));
@@ -1056,7 +1067,6 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     for (void* pb : e->ipc_opened) cudaIpcCloseMemHandle(pb);
     cudaFree(e->d_xchg);
     cudaFree(e->d_peer_xchg);
-    cudaFree(e->d_peer_arrive);
     cudaFree(e->d_ovf);
     cudaFree(e->d_cta_epoch);
     cudaFree(e->d_head_degen);
@@ -2039,16 +2049,10 @@ sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gat
 
 // ---- fused sequence-sharded merge over peer memory (mode 3) ------------------
 static void peer_tables(sinkr_engine* e, const std::vector<uint8_t*>& blocks) {
-    std::vector<float*> px(e->world);
-    std::vector<unsigned int*> pa(e->world);
-    for (uint32_t q = 0; q < e->world; ++q) {
-        px[q] = reinterpret_cast<float*>(blocks[q]);
-        pa[q] = reinterpret_cast<unsigned int*>(blocks[q] + e->xchg_floats * 4);
-    }
-    if (!e->d_peer_xchg) CK(cudaMalloc(&e->d_peer_xchg, 8 * sizeof(float*)));
-    if (!e->d_peer_arrive) CK(cudaMalloc(&e->d_peer_arrive, 8 * sizeof(unsigned int*)));
-    CK(cudaMemcpy(e->d_peer_xchg, px.data(), e->world * sizeof(float*), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(e->d_peer_arrive, pa.data(), e->world * sizeof(unsigned int*), cudaMemcpyHostToDevice));
+    std::vector<unsigned long long*> px(e->world);
+    for (uint32_t q = 0; q < e->world; ++q) px[q] = reinterpret_cast<unsigned long long*>(blocks[q]);
+    if (!e->d_peer_xchg) CK(cudaMalloc(&e->d_peer_xchg, 8 * sizeof(unsigned long long*)));
+    CK(cudaMemcpy(e->d_peer_xchg, px.data(), e->world * sizeof(unsigned long long*), cudaMemcpyHostToDevice));
 }
 
 sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, size_t* block_bytes) {
@@ -2060,8 +2064,8 @@ sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, si
         CK(cudaSetDevice(e->device));
         if (e->d_xchg && !e->peer_poisoned) fail(SINKR_LOGIC_ERROR, "peer merge already set up");
         if (e->d_xchg) {
-            // after a watchdog timeout: a fresh exchange block, fresh device
-            // epoch / arrival base; every rank sets up and connects again
+            // after a watchdog timeout: a fresh exchange block and step
+            // tags from zero; every rank sets up and connects again
             CK(cudaStreamSynchronize(e->stream));
             for (auto& kv : e->graphs) {
                 cudaGraphExecDestroy(kv.second.exec);
@@ -2072,17 +2076,16 @@ sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, si
             e->ipc_opened.clear();
             cudaFree(e->d_xchg);
             cudaFree(e->d_peer_xchg);
-            cudaFree(e->d_peer_arrive);
             e->d_xchg = nullptr;
             e->d_peer_xchg = nullptr;
-            e->d_peer_arrive = nullptr;
-            CK(cudaMemset(e->d_ss, 0, sizeof(dev::StepState)));
+            CK(cudaMemset(e->d_cta_epoch + e->grid, 0, e->grid * 4));  // mode-3 step counts
             e->peer_poisoned = false;
         }
         e->world = world;
         e->rank = rank;
-        e->xchg_floats = 2ull * world * e->U * e->PS;
-        e->xchg_bytes = align_up(e->xchg_floats * 4, 256) + 256;
+        // [2 parities][world][U][r(D+2)] LL words (8 B each)
+        e->xchg_words = 2ull * world * e->U * e->PS;
+        e->xchg_bytes = align_up(e->xchg_words * 8, 256);
         CK(cudaMalloc(&e->d_xchg, e->xchg_bytes));
         CK(cudaMemset(e->d_xchg, 0, e->xchg_bytes));
         if (block_bytes) *block_bytes = e->xchg_bytes;

@@ -18,11 +18,13 @@
 //            groups the (group, head, 32-dim) slices are claimed by warps once
 //            a group's last row has been counted; with many groups the CTA that
 //            streams a group's last rows merges it.  Mode 3 writes the rank
-//            partials into every rank's exchange block instead and merges all
-//            ranks' partials after a cross-GPU arrival count.
+//            partials into every rank's exchange block instead, as LL words
+//            tagged with the step, and merges all ranks' partials as soon as
+//            their tags show up (no fence, no arrival counter).
 //
-// The last CTA to leave restores the cross-CTA counters to zero for the next
-// step, so the launch needs no memset and replays as a single graph node.
+// The cross-CTA counters come in two sets used by alternate launches (each
+// launch zeroes its successor's set), so the launch needs no memset and
+// replays as a single graph node.
 #pragma once
 
 #include "kernels.cuh"
@@ -47,16 +49,14 @@ constexpr uint32_t kMaxEstHeads = 2048;  // distributed form: per-CTA estimate s
 struct StepCounters {
     unsigned int flat_counter;
     unsigned int merge_next;
-    unsigned int exit_count;  // only counted when a last CTA has work (host completion word, mode 3)
+    unsigned int exit_count;  // only counted when a last CTA has work (the host completion word)
     unsigned int error;
     unsigned int route_done;  // CTAs that published their units' decisions (distributed routing)
     unsigned int pad[3];
 };
 struct StepState {
     StepCounters c[2];
-    unsigned int peer_epoch;  // mode 3: steps completed (advanced by the last CTA at exit)
-    unsigned int peer_base;   // mode 3: arrivals counted on this rank before this step
-    unsigned int pad[6];
+    unsigned int pad[8];
 };
 
 struct StepTables {
@@ -81,17 +81,16 @@ struct StepTables {
     uint32_t* slot_count;          // [2][U]
     uint32_t* tokens_done;         // [2][U]
     uint32_t* ovf;                 // [2][U] spill-slot lock (bit0) + valid (bit1)
-    uint32_t* cta_epoch;           // [grid] launches seen by each CTA slot (counter-set parity)
+    uint32_t* cta_epoch;           // [2][grid]: launches seen by each CTA slot (counter-set parity),
+                                   // then mode-3 steps seen by each CTA slot (the exchange's step tag)
     float* partials;               // [U][S][r*(D+2)]: m[r], l[r], acc[r][D]
     float* out;                    // mode 0: [B][Hq][D]; mode 1: [U][r][D+2]
     uint32_t B, Hq, Hkv, r, cap, S, mode;  // mode 0 outputs, 1 rank partial, 3 peer merge
     // mode 3 (sequence-sharded peer merge over NVLink): every rank's exchange
-    // block holds [2][world][U][r*(D+2)] rank partials (step parity) + an
-    // arrival counter
-    float* const* peer_xchg;              // [world] partial areas of every rank's block
-    unsigned int* const* peer_arrive;     // [world] arrival counters of every rank's block
-    const float* xchg_local;              // this rank's partial area
-    const unsigned int* arrive_local;     // this rank's arrival counter
+    // block holds [2][world][U][r*(D+2)] rank partials (step parity) as LL
+    // words {value, step tag} (ptx::st_ll)
+    unsigned long long* const* peer_xchg;  // [world] exchange blocks of every rank
+    const unsigned long long* xchg_local;  // this rank's block
     uint32_t world, rank;
     float qscale;                  // (1/sqrt(D)) * log2(e)
     uint32_t static_pct;           // static share of the unit-affine schedule (0: one Ck chunk)
@@ -159,7 +158,7 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 // (mode 1), or that partial into every rank's exchange block (mode 3).
 template <int D, int R>
 __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
-                                           uint32_t lane, size_t xoff, float* wsm, bool dry) {
+                                           uint32_t lane, size_t xoff, uint32_t tag, float* wsm, bool dry) {
     // R = t.r at compile time: the partial stride is an immediate, so each of
     // the 64 acc loads is one LDG with an immediate offset.  This loop is cold
     // code at the end of every step, and instruction fetch from DRAM costs
@@ -233,36 +232,33 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
         }
         P[2 * r + h * D + d] = acc;
     } else {  // mode 3: this rank's partial straight into every rank's exchange block
+        // as LL words tagged with the step: no fence, no arrival counter --
+        // an owner that reads the tag reads the value (one 8-byte store)
         for (uint32_t q = 0; q < t.world; ++q) {
-            float* P = t.peer_xchg[q] + xoff + size_t(u) * PS;
+            unsigned long long* P = t.peer_xchg[q] + xoff + size_t(u) * PS;
             if (d == 0) {
-                P[h] = mx;
-                P[r + h] = lsum;
+                ptx::st_ll(P + h, mx, tag);
+                ptx::st_ll(P + r + h, lsum, tag);
             }
-            P[2 * r + h * D + d] = acc;
+            ptx::st_ll(P + 2 * r + h * D + d, acc, tag);
         }
-        // one arrival per task on every rank, as soon as its slice is stored:
-        // the warp's stores, then a release add per rank (system scope)
-        __syncwarp();
-        if (lane == 0)
-            for (uint32_t q = 0; q < t.world; ++q)
-                asm volatile("red.release.sys.global.add.u32 [%0], 1;" :: "l"(t.peer_arrive[q]) : "memory");
     }
 }
 
 // warp_merge for the runtime GQA width
 template <int D>
 __device__ __forceinline__ void warp_merge_r(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
-                                             uint32_t lane, size_t xoff, float* wsm, bool dry = false) {
+                                             uint32_t lane, size_t xoff, uint32_t tag, float* wsm,
+                                             bool dry = false) {
     switch (t.r) {
-        case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff, wsm, dry); break;
-        case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff, wsm, dry); break;
-        case 3: warp_merge<D, 3>(t, u, h, d0, lane, xoff, wsm, dry); break;
-        case 4: warp_merge<D, 4>(t, u, h, d0, lane, xoff, wsm, dry); break;
-        case 5: warp_merge<D, 5>(t, u, h, d0, lane, xoff, wsm, dry); break;
-        case 6: warp_merge<D, 6>(t, u, h, d0, lane, xoff, wsm, dry); break;
-        case 7: warp_merge<D, 7>(t, u, h, d0, lane, xoff, wsm, dry); break;
-        default: warp_merge<D, 8>(t, u, h, d0, lane, xoff, wsm, dry); break;
+        case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        case 3: warp_merge<D, 3>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        case 4: warp_merge<D, 4>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        case 5: warp_merge<D, 5>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        case 6: warp_merge<D, 6>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        case 7: warp_merge<D, 7>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        default: warp_merge<D, 8>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
     }
 }
 
@@ -406,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned long long t_stream_end = 0;
     constexpr bool lean = LEAN;
     bool exact_later = false;  // distributed form: exact record after streaming starts
-    uint32_t nact = 0, Ck = 0, Cs = 0, epoch = 0, peer_base = 0;
+    uint32_t nact = 0, Ck = 0, Cs = 0, epoch = 0;
     bool flat = false, queue_mode = true, lean_fast = false;
     size_t xoff = 0;
 #pragma unroll 1
@@ -948,8 +944,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ahead never overwrites partials a slower rank is still merging).  The
     // step number lives on the device (advanced by the last CTA at exit, after
     // every CTA has read it), so the graph needs no per-step parameter patch.
-    epoch = t.mode == 3 ? ld_volatile(&t.ss->peer_epoch) : 0u;
-    peer_base = t.mode == 3 ? ld_volatile(&t.ss->peer_base) : 0u;
+    epoch = t.mode == 3 ? ld_volatile(&t.cta_epoch[G + bid]) : 0u;  // (the same in every CTA)
     xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
@@ -1290,7 +1285,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // merge every partial of unit u (consumers only; few partials)
         auto merge_unit = [&](uint32_t u, uint32_t L) {
             for (uint32_t task = cw; task < r * (D / 32); task += kCWarps)
-                warp_merge_r<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff, sm_o + warp * 64);
+                warp_merge_r<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff, epoch + 1u,
+                                sm_o + warp * 64);
             if (ctid == 0) t.tokens[u] = L;
         };
         auto flush = [&](uint32_t u, uint32_t L) {
@@ -1481,6 +1477,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         STAMP(9);
         t_stream_end = globaltimer();
         if (t.trace && tid == 0) t.trace[bid * 8 + 1] = t_stream_end;
+    } else if (t.trace && tid == 0) {
+        t.trace[bid * 8 + 3] = globaltimer();  // dry stream pass done (trace only)
     }
 
     // ======================= phase M: distributed merge ========================
@@ -1512,7 +1510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
             }
             __syncwarp();
-            warp_merge_r<D>(t, u, h, d - lane, lane, xoff, sm_o + warp * 64, dry);
+            warp_merge_r<D>(t, u, h, d - lane, lane, xoff, epoch + 1u, sm_o + warp * 64, dry);
             if (dry) break;
             if (h == 0 && d == 0) t.tokens[u] = L;
             // every warp of the grid claims once, so with no more tasks than
@@ -1521,52 +1519,60 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ntasks <= G * (kThreads / 32)) break;
         }
     }
-    if (dry) __syncthreads();  // scratch (sm_o) free before the stream
+    if (dry) {
+        __syncthreads();  // scratch (sm_o) free before the stream
+        if (t.trace && tid == 0) t.trace[bid * 8 + 5] = globaltimer();  // dry merge done (trace only)
+    }
     }  // pass
 
     // ======================= mode 3: merge every rank's partials ===============
-    // Every merge task signalled every rank once (warp_merge), so this step's
-    // partials are all here when the arrivals reach base + world * tasks (a
-    // rank a step ahead only adds arrivals that causally follow every partial
-    // of this step).  The CTAs that own output elements wait, then merge them
-    // -- BEFORE they count out below, so the status the last CTA publishes
-    // covers their waits.  A rank that never delivers is a watchdog error:
-    // the owners then write NaN rather than a merge of incomplete partials.
-    const uint32_t peer_want = peer_base + t.world * (nact * r * (D / 32));
+    // Every rank's merge warps stored its partial into this rank's exchange
+    // block as LL words tagged with the step (warp_merge): an owner thread
+    // polls the three words it needs from each rank -- (m, l) of its head and
+    // its acc element -- until all carry this step's tag, then merges.  No
+    // fence and no arrival counter on the critical path; a word of an older
+    // step (same parity two steps back) has another tag.  The owners finish
+    // BEFORE they count out below, so the status a last CTA publishes covers
+    // their waits.  A rank that never delivers is a watchdog error: the
+    // owners then write NaN rather than a merge of incomplete partials.
     __syncthreads();
     STAMP(10);
     if (t.mode == 3 && bid * kThreads < nact * r * D) {
-        if (tid == 0) {
-            const unsigned int want = peer_want;
-            const unsigned long long t_spin = globaltimer();
-            uint32_t late = 0;
-            for (;;) {
-                unsigned int v;
-                asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(t.arrive_local) : "memory");
-                if ((int)(v - want) >= 0) break;
-                if (globaltimer() - t_spin > 2000000000ull) {
-                    raise_error(t, sc, 5u);
-                    late = 1;
-                    break;
-                }
-            }
-            misc[kMiscPeerLate] = late;
-        }
-        __syncthreads();
-        const bool late = misc[kMiscPeerLate] != 0;
-        const uint32_t PSx = r * (D + 2);
-        const float* X = t.xchg_local + size_t((epoch & 1u) * t.world) * U * PSx;
+        const uint32_t PSx = r * (D + 2), tag = epoch + 1u, world = t.world;
+        const unsigned long long* X = t.xchg_local + size_t((epoch & 1u) * world) * U * PSx;
+        const unsigned long long t_spin = globaltimer();
         for (uint32_t e = bid * kThreads + tid; e < nact * r * D; e += G * kThreads) {
             const uint32_t a = e / (r * D), h = (e / D) % r, d = e % D;
             const uint32_t u = act_unit[a];
             float mq[8], aq[8], lq[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const bool ok = (uint32_t)q < t.world;
-                const float* Pq = X + (size_t(q) * U + u) * PSx;
-                mq[q] = ok ? __ldcg(Pq + h) : -INFINITY;
-                lq[q] = ok ? __ldcg(Pq + r + h) : 0.f;
-                aq[q] = ok ? __ldcg(Pq + 2 * r + h * D + d) : 0.f;
+                mq[q] = -INFINITY;
+                lq[q] = 0.f;
+                aq[q] = 0.f;
+            }
+            uint32_t pending = (1u << world) - 1u;
+            bool late = false;
+            while (pending) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if ((pending >> q) & 1u) {
+                        const unsigned long long* Pq = X + (size_t(q) * U + u) * PSx;
+                        const unsigned long long wm = ptx::ld_ll(Pq + h), wl = ptx::ld_ll(Pq + r + h),
+                                                 wa = ptx::ld_ll(Pq + 2 * r + h * D + d);
+                        if (ptx::ll_tag(wm) == tag && ptx::ll_tag(wl) == tag && ptx::ll_tag(wa) == tag) {
+                            mq[q] = ptx::ll_val(wm);
+                            lq[q] = ptx::ll_val(wl);
+                            aq[q] = ptx::ll_val(wa);
+                            pending &= ~(1u << q);
+                        }
+                    }
+                }
+                if (pending && globaltimer() - t_spin > 2000000000ull) {
+                    raise_error(t, sc, 5u);
+                    late = true;
+                    break;
+                }
             }
             float mx = mq[0];
 #pragma unroll
@@ -1585,32 +1591,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= exit =============================================
     // Nothing to restore (the next launch zeroes this launch's counter set).
     // A last CTA is found only when it has work: the host completion word
-    // (zero-copy results) and the mode-3 step count.
+    // (zero-copy results).
     __syncthreads();
     if (t.trace && tid == 0) t.trace[bid * 8 + 2] = globaltimer();
-    if (tid == 0) t_in.cta_epoch[bid] = cta_ep + 1u;  // after every thread of the CTA read it
-    if (t.done || t.mode == 3) {
+    if (tid == 0) {
+        t_in.cta_epoch[bid] = cta_ep + 1u;  // after every thread of the CTA read it
+        if (t.mode == 3) t_in.cta_epoch[G + bid] = epoch + 1u;  // this slot's mode-3 step count
+    }
+    if (t.done) {
         if (tid == 0) {
             // acq_rel count: releases this CTA's writes (ordered before tid 0
             // by the barrier) and, for the last CTA, acquires everyone's.
             // System scope when results go to mapped host memory and a host
             // thread waits on the completion word instead of the stream.
-            const uint32_t prev = t.done ? ptx::atom_add_acq_rel_sys(&sc->exit_count, 1u)
-                                         : ptx::atom_add_acq_rel(&sc->exit_count, 1u);
+            const uint32_t prev = ptx::atom_add_acq_rel_sys(&sc->exit_count, 1u);
             if (prev == G - 1) {
                 if (t.trace) t.trace[bid * 8 + 5] = globaltimer();
                 clk[2] = t_stream_end;
                 clk[3] = globaltimer();
-                if (t.mode == 3) {
-                    t.ss->peer_epoch = epoch + 1u;
-                    t.ss->peer_base = peer_want;
-                }
-                if (t.done) {
-                    // every CTA's results (outputs, routing record, status)
-                    // are visible system-wide before the host sees the word
-                    __threadfence_system();
-                    ptx::st_release_sys(t.done, 1u);
-                }
+                // every CTA's results (outputs, routing record, status) are
+                // visible system-wide before the host sees the word
+                __threadfence_system();
+                ptx::st_release_sys(t.done, 1u);
             }
         }
     } else if (tid == 0) {

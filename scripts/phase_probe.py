@@ -64,7 +64,10 @@ for L in Ls:
               f"{rel(a[:, 0]).min():.2f}/{np.median(rel(a[:, 0])):.2f}/{rel(a[:, 0]).max():.2f}")
         se = rel(a[:, 1])
         print(f"  stream end min/med/max {se.min():.2f}/{np.median(se):.2f}/{se.max():.2f}; "
-              f"merge end max {rel(a[:, 2]).max():.2f}; reset {rel(a[:, 5][a[:, 5] > 0]).max():.2f}")
+              f"merge end max {rel(a[:, 2]).max():.2f}; last-CTA stamp {(rel(a[:, 5][a[:, 5] > 0]).max() if (a[:, 5] > 0).any() else float('nan')):.2f}")
+        lc = a[G - 1]
+        print(f"  CTA G-1 (prewarm): start {rel(lc[4]):.2f}, dry stream pass end {rel(lc[3]):.2f}, "
+              f"dry merge end {rel(lc[5]):.2f}, routing end {rel(lc[0]):.2f}, stream end {rel(lc[1]):.2f} us")
         ne = (a[:, 6].astype(np.uint64) >> np.uint64(32)).astype(np.int64)
         te = (a[:, 6].astype(np.uint64) & np.uint64(0xffffffff)).astype(np.int64)
         pe = rel(a[:, 7])
