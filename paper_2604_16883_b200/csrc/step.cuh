@@ -39,6 +39,10 @@ constexpr uint32_t kFlatMinTok = 512;  // smallest claim of the global token-spa
 // an fp32 estimate of a group score decides the route when it clears tau by
 // this much (its own error is ~1e-6); closer calls wait for the exact score
 constexpr double kRouteMargin = 1e-4;
+constexpr unsigned long long kPrewarmLateNs = 12000;  // a dry pass longer than this ran cold
+// a late CTA joins the stream only above this many unclaimed rows (all
+// units): ~2 us of the whole grid's stream at 7 TB/s and 512 B per row
+constexpr unsigned long long kLateJoinTok = 32768;
 constexpr uint32_t kMaxEstHeads = 2048;  // distributed form: per-CTA estimate slots (s_score overlay)
 
 // Cross-CTA counters of one step.  Two sets, used by alternate launches
@@ -388,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // CTAs fetched faster but cost 2.5 us back to back at 512K
     // (profiles/r02_prewarm_ab.txt).
     // t.prewarm: bit mask of the regions (bit 0 consumer body, 1 flush, 2
-    // merge), the k-th set bit to CTA G-1-k; bit 3: all three in CTA G-1
+    // merge), the k-th set bit to CTA G-1-k; bit 3: all three in CTA G-1;
+    // bits 8+: the cold-pass threshold in us (A/B; 0 = kPrewarmLateNs)
     const uint32_t pw_mask = (LEAN && G >= 64u) ? (t.prewarm & 15u) : 0u;
     const uint32_t n_pw = (pw_mask & 8u) ? 1u : __popc(pw_mask);
     const bool pw_on = n_pw != 0u;
@@ -400,9 +405,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         dry_regions = (pw_mask & 8u) ? 7u : 1u << (__ffs(m) - 1);
     }
     unsigned long long t_stream_end = 0;
+    const unsigned long long t_cta_start = prewarm ? globaltimer() : 0ull;
     constexpr bool lean = LEAN;
     bool exact_later = false;  // distributed form: exact record after streaming starts
-    uint32_t nact = 0, Ck = 0, Cs = 0, epoch = 0;
+    // mode 3: this CTA slot's mode-3 step count (the same in every CTA) tags
+    // the exchange words of this step
+    const uint32_t epoch = t.mode == 3 ? ld_volatile(&t.cta_epoch[G + bid]) : 0u;
+    uint32_t nact = 0, Ck = 0, Cs = 0;
     bool flat = false, queue_mode = true, lean_fast = false;
     size_t xoff = 0;
 #pragma unroll 1
@@ -944,7 +953,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ahead never overwrites partials a slower rank is still merging).  The
     // step number lives on the device (advanced by the last CTA at exit, after
     // every CTA has read it), so the graph needs no per-step parameter patch.
-    epoch = t.mode == 3 ? ld_volatile(&t.cta_epoch[G + bid]) : 0u;  // (the same in every CTA)
     xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
@@ -1024,9 +1032,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sz = sz / kStageTok * kStageTok;
                     return sz < (uint32_t)kStageTok ? (uint32_t)kStageTok : (sz > Ck ? Ck : sz);
                 };
+                // the prewarm CTA arrives late (after its dry pass): it joins
+                // only while there is more than ~2 us of stream left for the
+                // whole grid, else its first stage would land after the others
+                // finish and make it the tail
+                bool late_join = prewarm;
                 for (;;) {
                     if (t0 >= L) {
                         uint32_t best = 0, best_rem = 0;
+                        unsigned long long all_rem = 0;
                         for (uint32_t b0 = 0; b0 < nact; b0 += 16) {
                             uint32_t cur[16];
 #pragma unroll
@@ -1038,6 +1052,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (b < nact) {
                                     const uint32_t pos = static_end(b) + cur[k];
                                     const uint32_t rem = act_len[b] > pos ? act_len[b] - pos : 0u;
+                                    all_rem += rem;
                                     if (rem > best_rem) {
                                         best_rem = rem;
                                         best = b;
@@ -1046,6 +1061,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         if (best_rem == 0) break;
+                        if (late_join && all_rem < kLateJoinTok) break;
+                        late_join = false;
                         a = best;
                         u = act_unit[a];
                         L = act_len[a];
@@ -1516,12 +1533,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             // every warp of the grid claims once, so with no more tasks than
             // warps a second claim finds nothing: skip its L2 round trip (the
             // dry pass claims nothing; every CTA claims in its real pass)
-            if (ntasks <= G * (kThreads / 32)) break;
+            if (ntasks <= (G - n_pw) * (kThreads / 32)) break;
         }
     }
     if (dry) {
-        __syncthreads();  // scratch (sm_o) free before the stream
-        if (t.trace && tid == 0) t.trace[bid * 8 + 5] = globaltimer();  // dry merge done (trace only)
+        // A dry pass this slow ran from a cold L2 (~20 us against ~6 warm):
+        // by now the other CTAs have claimed the work and this CTA would
+        // only be the last to route and exit, so it leaves (the others'
+        // merge claims suffice: ntasks <= (G - n_pw) warps).  Warm, it joins
+        // the stream on dynamic claims.
+        if (tid == 0) {
+            const unsigned long long now = globaltimer();
+            const unsigned long long late_ns = (t.prewarm >> 8) ? (t.prewarm >> 8) * 1000ull : kPrewarmLateNs;
+            misc[kMiscTask] = (now - t_cta_start > late_ns) ? 1u : 0u;
+            if (t.trace) t.trace[bid * 8 + 5] = now;  // dry pass done (trace only)
+        }
+        __syncthreads();  // (also: scratch sm_o free before the stream)
+        if (misc[kMiscTask]) break;
     }
     }  // pass
 

@@ -56,6 +56,11 @@ for cold in (0, 1, 2):
         _abi.lib().sinkr_debug_trace(cache.handle, buf)
         a = np.array(buf, dtype=np.float64).reshape(G, 8)
         t0 = a[:, 4].min()
+        if os.environ.get("SHOW_LATE"):
+            ex = a[:, 2]
+            late = np.argsort(ex)[-3:]
+            print("   latest exits:", [(int(b), round((a[b, 0] - t0) / 1e3, 2), round((a[b, 1] - t0) / 1e3, 2),
+                                        round((ex[b] - t0) / 1e3, 2)) for b in late])
         for k, c in cols.items():
             x = a[:, c]
             x = x[x > t0 - 1]
