@@ -8,6 +8,7 @@
 #include <filesystem>
 #include <functional>
 #include <set>
+#include <stdexcept>
 #include <span>
 #include <utility>
 #include <vector>
@@ -155,6 +156,24 @@ inline std::vector<double> collect_group_scores(const KvCache& cache,
     std::vector<double> gs(c.num_seqs * c.num_kv_heads);
     check(sinkr_collect_scores(cache.handle(), queries.data(), layer, nullptr, nullptr, gs.data(),
                                nullptr));
+    return gs;
+}
+
+// The same for n query blocks [n][B][H_q][D] over one layer in one launch
+// (a calibration length's samples): group scores [n][B*H_kv], bit-identical
+// to n collect_group_scores calls.
+inline std::vector<double> collect_group_scores_batch(const KvCache& cache,
+                                                      std::span<const float> queries,
+                                                      std::size_t layer) {
+    const auto& c = cache.config();
+    const std::size_t per = c.num_seqs * c.num_q_heads * c.head_dim;
+    if (per == 0 || queries.size() % per != 0)
+        throw std::invalid_argument("queries must be n x B x H_q x D for one layer");
+    const std::size_t n = queries.size() / per;
+    std::vector<double> gs(n * c.num_seqs * c.num_kv_heads);
+    if (n)
+        check(sinkr_collect_scores_batch(cache.handle(), queries.data(), n, layer, nullptr, nullptr,
+                                         gs.data(), nullptr));
     return gs;
 }
 

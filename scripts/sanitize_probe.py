@@ -1,5 +1,7 @@
-"""Dev tool: one small routed step, one batched step and one BOS-mass pass,
-sized for compute-sanitizer (memcheck / racecheck / synccheck)."""
+"""Dev tool: small routed steps (single-sequence with the code prewarm,
+batched), score collection (single and batched), BOS mass, the span
+operators, append+step and the fused peer merge, sized for compute-sanitizer
+(memcheck / racecheck / synccheck)."""
 import os
 import sys
 
@@ -26,6 +28,8 @@ for B, L in ((1, 4096), (4, 3000), (40, 600)):
         from paper_2604_16883_b200 import calibration as cal
         hs, gs, _ = cal.collect_scores(cache, q, 0)
         assert np.isfinite(hs).all() and np.isfinite(gs).all()
+        hb, gb, _ = cal.collect_scores_batch(cache, np.stack([q, q * 0.5, -q]), 0)
+        assert np.isfinite(hb).all() and np.isfinite(gb).all()
         a0 = A.attention_bos_mass(cache, q, 0)
         w = A.attention_weights(cache, q[0, :4], 0, 1)
         assert np.isfinite(a0).all() and np.isfinite(w).all()
@@ -50,4 +54,19 @@ with P.KvCache(P.CacheConfig(1, 32, 8, 128, 1003)) as cache:
         o = run(rng.standard_normal((8, 128)).astype(np.float32),
                 rng.standard_normal((8, 128)).astype(np.float32), spec.queries()[0])
         assert np.isfinite(o).all()
+# the fused peer merge (mode 3, LL exchange) at world 1, several steps
+import torch
+from paper_2604_16883_b200 import sharding
+spec = WorkloadSpec(length=5000, sink_fraction=0.5, seed=6)
+with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as cache:
+    spec.fill(cache)
+    P.set_timing(cache, False)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    dq = torch.from_numpy(spec.queries()[0]).cuda()
+    dout = torch.empty_like(dq)
+    (pm,) = sharding.peer_merge_in_process(P, [cache])
+    for _ in range(3):
+        pm.step(dq, dout, cfg, P.EngineOptions())
+    torch.cuda.synchronize()
+    assert torch.isfinite(dout).all()
 print("sanitize probe OK")

@@ -91,10 +91,18 @@ int main() {
         seen.push_back(len);
         sc::ScorePopulation pop;
         std::normal_distribution<float> shift(0.02f * (float)len / 100.0f, 1.0f);
+        std::vector<float> qs(8 * hq * D);  // the length's 8 samples
+        for (auto& x : qs) x = shift(rng);
+        // one launch for all samples, bit-identical to one call per sample
+        const auto batch = sc::collect_group_scores_batch(cache, qs, 1);
         for (int sample = 0; sample < 8; ++sample) {
-            std::vector<float> qs(hq * D);
-            for (auto& x : qs) x = shift(rng);
-            for (double g : sc::collect_group_scores(cache, qs, 1)) pop.add(g, 1, len);
+            const auto one = sc::collect_group_scores(
+                cache, std::span<const float>(qs.data() + sample * hq * D, hq * D), 1);
+            for (std::size_t g = 0; g < one.size(); ++g) {
+                if (one[g] != batch[sample * one.size() + g])
+                    throw std::runtime_error("collect_group_scores_batch != collect_group_scores");
+                pop.add(one[g], 1, len);
+            }
         }
         return pop;
     };

@@ -82,8 +82,8 @@ def _one_gpu_peer_setup(P, caches):
 
 def test_peer_merge_world1_matches_fused_step():
     """The fused peer-merge step at world 1 (the kernel writes its partial into
-    its own exchange block, counts itself in, merges) equals the plain step,
-    over several steps (step-parity buffers, monotonic arrival counters)."""
+    its own exchange block as tagged LL words, merges) equals the plain step,
+    over several steps (step-parity buffers, step tags advancing)."""
     spec = WorkloadSpec(length=40000, sink_fraction=0.5, seed=3)
     cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
     with P.KvCache(P.CacheConfig(1, 32, 8, 128, spec.length)) as cache:
