@@ -165,6 +165,7 @@ struct sinkr_engine {
     // A/B profiling (SINKR_FUSED=0) and serves the multi-rank merge.
     bool fused = true;
     bool lean = false;  // single-sequence step-kernel instantiation (step.cuh LEAN)
+    bool wide = false;  // GQA width 9-16: the step kernel's WIDE form (two 8-head tiles)
     dev::StepState* d_ss = nullptr;
     uint32_t* d_cursor = nullptr;
     uint32_t* d_tokens_done = nullptr;
@@ -374,12 +375,19 @@ static int debug_kernel_mask() {
     return m;
 }
 
-// the step-kernel instantiation of this engine (lean: single-sequence shapes)
+// the step-kernel instantiation of this engine (lean: single-sequence shapes;
+// wide: GQA width 9-16)
+using StepFn = void (*)(const dev::StepTables, const dev::ProbeParams);
+template <int D>
+StepFn step_fn_d(const sinkr_engine* e) {
+    if (e->wide) return e->lean ? dev::step_kernel<D, true, true> : dev::step_kernel<D, false, true>;
+    return e->lean ? dev::step_kernel<D, true, false> : dev::step_kernel<D, false, false>;
+}
 const void* step_fn(const sinkr_engine* e) {
     switch (e->D) {
-        case 32: return e->lean ? (const void*)dev::step_kernel<32, true> : (const void*)dev::step_kernel<32, false>;
-        case 64: return e->lean ? (const void*)dev::step_kernel<64, true> : (const void*)dev::step_kernel<64, false>;
-        default: return e->lean ? (const void*)dev::step_kernel<128, true> : (const void*)dev::step_kernel<128, false>;
+        case 32: return (const void*)step_fn_d<32>(e);
+        case 64: return (const void*)step_fn_d<64>(e);
+        default: return (const void*)step_fn_d<128>(e);
     }
 }
 
@@ -420,7 +428,7 @@ void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, e->lean ? dev::step_kernel<D, true> : dev::step_kernel<D, false>, st, e->pp));
+    CK(cudaLaunchKernelEx(&cfg, step_fn_d<D>(e), st, e->pp));
 }
 
 void enqueue_step(sinkr_engine* e, const float* d_q, float* d_out, int mode,
@@ -853,8 +861,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
         if (c.capacity == 0) fail(SINKR_INVALID_ARGUMENT, "capacity must be positive");
         if (c.head_dim != 32 && c.head_dim != 64 && c.head_dim != 128)
             fail(SINKR_INVALID_ARGUMENT, "head_dim must be 32, 64 or 128 on the GPU engine");
-        if (c.num_q_heads / c.num_kv_heads > (size_t)dev::kMaxR)
-            fail(SINKR_INVALID_ARGUMENT, "GQA group width above 8 is not supported");
+        if (c.num_q_heads / c.num_kv_heads > (size_t)dev::kMaxRWide)
+            fail(SINKR_INVALID_ARGUMENT, "GQA group width above 16 is not supported");
 
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -941,6 +949,7 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             e->probe_grid = (int)((e->B * Hq + dev::kProbeHeads - 1) / dev::kProbeHeads);
             // the step kernel's lean routing form (step.cuh): every single-sequence shape
             e->lean = e->B * Hq <= (size_t)dev::kRouteTile && e->U <= 32;
+            e->wide = e->r > (size_t)dev::kMaxR;
             CK(cudaMalloc(&e->d_ss, sizeof(dev::StepState)));
             CK(cudaMemsetAsync(e->d_ss, 0, sizeof(dev::StepState), e->stream));
             // per-unit step counters: two sets, used by alternate launches
@@ -960,8 +969,11 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             }
             {
                 const char* f = std::getenv("SINKR_FUSED");
-                e->fused = !(f && f[0] == '0') && e->U <= (size_t)dev::kMaxUnits &&
-                           e->B * Hq <= (size_t)dev::kMaxStepHeads;
+                const bool fits = e->U <= (size_t)dev::kMaxUnits && e->B * Hq <= (size_t)dev::kMaxStepHeads;
+                // (the three-kernel A/B pipeline holds one 8-head tile per group)
+                e->fused = fits && (e->wide || !(f && f[0] == '0'));
+                if (e->wide && !fits)
+                    fail(SINKR_INVALID_ARGUMENT, "GQA group width above 8 needs B*H_kv <= 1280 and B*H_q <= 4096");
             }
             CK(cudaMalloc(&e->d_ws, sizeof(dev::WorkState)));
             CK(cudaMemsetAsync(e->d_ws, 0, sizeof(dev::WorkState), e->stream));
@@ -2004,6 +2016,7 @@ sinkr_status sinkr_attention_bos_mass(sinkr_engine* e, const float* queries, siz
                                       double* alpha0) {
     return guard([&] {
         if (!e || !queries || !alpha0) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        if (e->wide) fail(SINKR_INVALID_ARGUMENT, "attention_bos_mass supports GQA group width <= 8");
         CK(cudaSetDevice(e->device));
         const size_t nq = e->B * e->cfg.num_q_heads * e->D;
         run_bos(e, queries, nq, 0, layer, 0, (uint32_t)e->U, alpha0, nullptr);
@@ -2014,6 +2027,7 @@ sinkr_status sinkr_attention_weights(sinkr_engine* e, const float* queries, size
                                      size_t layer, size_t kv_head, float* weights) {
     return guard([&] {
         if (!e || !queries || !weights) fail(SINKR_INVALID_ARGUMENT, "null argument");
+        if (e->wide) fail(SINKR_INVALID_ARGUMENT, "attention_weights supports GQA group width <= 8");
         check_slot(e, seq, layer, kv_head);
         CK(cudaSetDevice(e->device));
         const uint32_t u = (uint32_t)(seq * e->cfg.num_kv_heads + kv_head);

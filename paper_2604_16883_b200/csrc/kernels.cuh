@@ -31,6 +31,7 @@ constexpr int kWarpTok = 16;                          // tokens per consumer war
 constexpr int kCWarps = kStageTok / kWarpTok;         // consumer warps
 constexpr int kThreads = 32 * (1 + kCWarps);          // + 1 TMA producer warp
 constexpr int kMaxR = 8;                              // GQA width per MMA row tile (hi/lo split)
+constexpr int kMaxRWide = 16;                         // step kernel WIDE form: two 8-head tiles per group
 constexpr uint32_t kEnd = 0xFFFFFFFFu;
 constexpr int kProbeThreads = 256;
 constexpr int kChunksPerCta = 128;                    // dynamic-scheduling granularity target

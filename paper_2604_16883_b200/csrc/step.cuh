@@ -111,7 +111,7 @@ struct StepCfg {
     static constexpr int kOffMeta = kOffBars + 2 * C::kStages * 8;
     static constexpr int kOffO = kOffMeta + C::kStages * 16;
     static constexpr int kOffML = kOffO + kCWarps * kMaxR * C::kOStride * 4;
-    static constexpr int kOffMisc = kOffML + (kCWarps + 1) * kMaxR * 2 * 4;  // + spill staging
+    static constexpr int kOffMisc = kOffML + (kCWarps * kMaxR + kMaxRWide) * 2 * 4;  // + spill staging [16][2]
     static constexpr int kOffAct = kOffMisc + 64;
     static constexpr int kOffPrefix = kOffAct + kMaxUnits * 2;
     static constexpr int kOffLen = kOffPrefix + (kMaxUnits + 1) * 4;
@@ -249,11 +249,24 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
     }
 }
 
-// warp_merge for the runtime GQA width
-template <int D>
+// warp_merge for the runtime GQA width (WIDE kernels: 9 <= r <= 16)
+template <int D, bool WIDE>
 __device__ __forceinline__ void warp_merge_r(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
                                              uint32_t lane, size_t xoff, uint32_t tag, float* wsm,
                                              bool dry = false) {
+    if constexpr (WIDE) {
+        switch (t.r) {
+            case 9: warp_merge<D, 9>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+            case 10: warp_merge<D, 10>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+            case 11: warp_merge<D, 11>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+            case 12: warp_merge<D, 12>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+            case 13: warp_merge<D, 13>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+            case 14: warp_merge<D, 14>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+            case 15: warp_merge<D, 15>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+            default: warp_merge<D, 16>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
+        }
+        return;
+    }
     switch (t.r) {
         case 1: warp_merge<D, 1>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
         case 2: warp_merge<D, 2>(t, u, h, d0, lane, xoff, tag, wsm, dry); break;
@@ -280,7 +293,11 @@ __device__ __forceinline__ void raise_error(const StepTables& t, StepCounters* s
 // scheduler and their exact record are compiled out, so the binary a step
 // fetches (cold, from DRAM, at the start of every step in a model) is smaller.
 // The engine picks the instantiation once, from its shape (engine.cu step_fn).
-template <int D, bool LEAN>
+// WIDE: GQA width 9-16 (e.g. 128 q / 8 kv heads): consumer warp cw takes the
+// head half cw & 1 (two 8-head hi/lo MMA tiles per group) and 32 tokens of
+// each stage as two 16-token sub-tiles, so every warp keeps one 8-head tile
+// of online-softmax state and the per-stage work is unchanged.
+template <int D, bool LEAN, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1)
     step_kernel(const StepTables t_in, const ProbeParams p) {
     using C = Cfg<D>;
@@ -1018,6 +1035,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // (the prewarm CTAs, the last ones, have no static range either)
                 const uint32_t cpu = (G + nact - 1) / nact;  // CTAs per unit
                 const uint32_t Gs = G - n_pw;  // CTAs [0, Gs) hold static ranges
+                // (static CTAs interleaved over the entries: contiguous blocks of
+                // CTAs per entry ran 1-1.8 us slower back to back, r02 A/B)
                 auto static_end = [&](uint32_t e) {        // statically covered prefix of entry e
                     return (e < Gs ? ((Gs - e + nact - 1) / nact) - (e == 0 ? 1u : 0u) : 0u) * Cs;
                 };
@@ -1262,11 +1281,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::named_bar_sync(1, kCWarps * 32);
         }
-        const int tb = cw * kWarpTok;
+        // this warp's tokens of a stage (kSub 16-token sub-tiles from tb0) and
+        // query heads (hbase .. hbase+7; WIDE: the group's head half cw & 1)
+        constexpr int kSub = WIDE ? 2 : 1;
+        const int tb0 = WIDE ? (cw >> 1) * (2 * kWarpTok) : cw * kWarpTok;
+        const uint32_t hbase = WIDE ? 8u * (cw & 1) : 0u;
         const int grp = lane >> 2, qd = lane & 3;
         const int lj = lane >> 3, li = lane & 7;
-        const uint32_t k_tok = tb + ((lj >> 1) << 3) + li, k_csel = lj & 1;
-        const uint32_t v_tok = tb + ((lj & 1) << 3) + li, v_csel = lj >> 1;
+        const uint32_t k_csel = lj & 1, v_csel = lj >> 1;
         const uint32_t PS = r * (D + 2);
 
         uint32_t qa[C::kNK][4];
@@ -1282,8 +1304,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             l_acc = 0.f;
         };
         auto load_q = [&](uint32_t u) {
-            const bool live = grp < (int)r;
-            const float* qrow = t.q + (size_t(u) * r + (live ? grp : 0)) * D;
+            const bool live = hbase + grp < r;
+            const float* qrow = t.q + (size_t(u) * r + (live ? hbase + grp : 0)) * D;
 #pragma unroll
             for (int kk = 0; kk < C::kNK; ++kk) {
                 float2 x = make_float2(0.f, 0.f), y = make_float2(0.f, 0.f);
@@ -1302,14 +1324,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // merge every partial of unit u (consumers only; few partials)
         auto merge_unit = [&](uint32_t u, uint32_t L) {
             for (uint32_t task = cw; task < r * (D / 32); task += kCWarps)
-                warp_merge_r<D>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff, epoch + 1u,
-                                sm_o + warp * 64);
+                warp_merge_r<D, WIDE>(t, u, task / (D / 32), (task % (D / 32)) * 32, lane, xoff, epoch + 1u,
+                                      sm_o + warp * 64);
             if (ctid == 0) t.tokens[u] = L;
         };
         auto flush = [&](uint32_t u, uint32_t L) {
             float l_tot = l_acc + __shfl_xor_sync(0xffffffffu, l_acc, 1);
             l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
-            if (grp < (int)r) {
+            if (hbase + grp < r) {
                 float* so = sm_o + (cw * kMaxR + grp) * C::kOStride;
 #pragma unroll
                 for (int nt = 0; nt < 2 * C::kNK; ++nt) {
@@ -1355,16 +1377,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             for (uint32_t idx = ctid; idx < r * D; idx += kCWarps * 32) {
                 const uint32_t h = idx / D, d = idx % D;
+                // the warps holding head h, and its row in their tiles (WIDE:
+                // warps h/8 and h/8 + 2, row h % 8; else all warps, row h)
+                constexpr int kHW = WIDE ? 2 : kCWarps;
+                const uint32_t w0 = WIDE ? h / 8 : 0u, hr = WIDE ? h % 8 : h;
+                constexpr uint32_t kWs = WIDE ? 2u : 1u;
                 float mx = -INFINITY;
                 // (dry: everything but the stores below)
 #pragma unroll
-                for (int w = 0; w < kCWarps; ++w) mx = fmaxf(mx, sm_ml[(w * kMaxR + h) * 2]);
+                for (int i = 0; i < kHW; ++i) mx = fmaxf(mx, sm_ml[((w0 + i * kWs) * kMaxR + hr) * 2]);
                 float acc = 0.f, lsum = 0.f;
 #pragma unroll
-                for (int w = 0; w < kCWarps; ++w) {
-                    const float sc = ptx::ex2(sm_ml[(w * kMaxR + h) * 2] - mx);
-                    acc += sm_o[(w * kMaxR + h) * C::kOStride + d] * sc;
-                    lsum += sm_ml[(w * kMaxR + h) * 2 + 1] * sc;
+                for (int i = 0; i < kHW; ++i) {
+                    const uint32_t row = (w0 + i * kWs) * kMaxR + hr;
+                    const float sc = ptx::ex2(sm_ml[row * 2] - mx);
+                    acc += sm_o[row * C::kOStride + d] * sc;
+                    lsum += sm_ml[row * 2 + 1] * sc;
                 }
                 if (combine) {
                     const float mo = old_ml[2 * h], mn = fmaxf(mo, mx);
@@ -1424,6 +1452,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const uint32_t ntok = dry ? ((dry_regions & 1u) ? (uint32_t)kStageTok : 0u) : meta[stage].ntok;
             run_tokens += ntok;
+#pragma unroll
+            for (int sub = 0; sub < kSub; ++sub) {
+            const int tb = tb0 + sub * kWarpTok;
+            const uint32_t k_tok = tb + ((lj >> 1) << 3) + li;
+            const uint32_t v_tok = tb + ((lj & 1) << 3) + li;
             const int n = (int)ntok - tb;
             if (n > 0) {
                 const uint32_t kbase = ptx::smem_u32(ring + stage * C::kStageBytes);
@@ -1481,6 +1514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mma_bf16(o[2 * nn + 1], pa, b[2], b[3]);
                 }
             }
+            }  // sub
             __syncwarp();
             if (lane == 0 && !dry) ptx::mbar_arrive(&empty[stage]);
             if (++stage == C::kStages) {
@@ -1527,7 +1561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t.trace) t.trace[bid * 8 + 3] = globaltimer();
             }
             __syncwarp();
-            warp_merge_r<D>(t, u, h, d - lane, lane, xoff, epoch + 1u, sm_o + warp * 64, dry);
+            warp_merge_r<D, WIDE>(t, u, h, d - lane, lane, xoff, epoch + 1u, sm_o + warp * 64, dry);
             if (dry) break;
             if (h == 0 && d == 0) t.tokens[u] = L;
             // every warp of the grid claims once, so with no more tasks than

@@ -113,7 +113,7 @@ def test_config_validation_mirrors_reference(L):
     bad = [P.CacheConfig(0, 32, 8, 128, 16), P.CacheConfig(1, 32, 0, 128, 16),
            P.CacheConfig(1, 30, 8, 128, 16), P.CacheConfig(1, 32, 8, 0, 16),
            P.CacheConfig(1, 32, 8, 128, 0), P.CacheConfig(1, 32, 8, 96, 16),
-           P.CacheConfig(1, 32, 2, 128, 16)]
+           P.CacheConfig(1, 34, 2, 128, 16)]  # GQA width 17 > 16
     for cfg in bad:
         with pytest.raises(ValueError):
             P.KvCache(cfg)

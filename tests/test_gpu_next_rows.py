@@ -56,12 +56,12 @@ def test_collect_scores_bit_exact(ref):
 
 
 @pytest.mark.parametrize("hq,hkv,D,B", [(32, 8, 128, 1), (40, 8, 64, 2), (8, 8, 32, 3), (64, 8, 128, 1),
-                                         (35, 7, 128, 1)])
+                                         (35, 7, 128, 1), (128, 8, 128, 1), (24, 2, 64, 2)])
 def test_collect_scores_batch_matches_single(hq, hkv, D, B):
     """sinkr_collect_scores_batch over n samples == n sinkr_collect_scores
     calls, byte for byte (head/group scores, sink flags), including a
     degenerate (zero) query head, sink_on_tie and an excluded layer; B = 1-3,
-    r = 1, 4, 5, 8 and D = 32 / 64 / 128 (the single call is pinned to the
+    r = 1, 4, 5, 8, 12, 16 and D = 32 / 64 / 128 (the single call is pinned to the
     reference by test_collect_scores_bit_exact)."""
     rng = np.random.default_rng(hq * 131 + D)
     L = 700

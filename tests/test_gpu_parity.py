@@ -90,6 +90,11 @@ CASES = [
     (8, 8, 64, 1500, 0.25),      # D = 64
     (16, 4, 32, 777, 0.5),       # D = 32
     (12, 4, 128, 333, 0.5),      # r = 3 (padded MMA rows)
+    # wide GQA (the step kernel's WIDE form: two 8-head tiles per group)
+    (128, 8, 128, 4096, 0.625),  # r = 16 (Llama-3.1-405B attention shape)
+    (16, 1, 64, 3000, 0.0),      # r = 16, one KV head, D = 64
+    (96, 8, 128, 2000, 0.5),     # r = 12 (second tile half full)
+    (20, 2, 32, 500, 0.5),       # r = 10, D = 32
 ]
 
 
@@ -250,6 +255,19 @@ def test_batched_sequences(oracle_libs):
             assert_parity(res.outputs[s], ref, 4, 128, res.groups[s * 4:(s + 1) * 4])
 
 
+def test_wide_gqa_envelope():
+    """GQA width 9-16 runs on the WIDE step kernel; above 16 is rejected at
+    creation, and the f4 analysis pass (one 8-head tile) rejects r > 8."""
+    with pytest.raises(ValueError, match="above 16"):
+        P.KvCache(P.CacheConfig(1, 34, 2, 128, 16))
+    spec = WorkloadSpec(num_q_heads=32, num_kv_heads=2, head_dim=128, length=100, seed=2)
+    with make_cache(spec) as cache:
+        from paper_2604_16883_b200 import analysis as A
+
+        with pytest.raises(ValueError, match="group width"):
+            A.attention_bos_mass(cache, spec.queries()[0], 0)
+
+
 def test_errors_mirror_reference():
     spec = WorkloadSpec(num_q_heads=8, num_kv_heads=2, head_dim=64, length=10)
     cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5))
@@ -348,7 +366,7 @@ def test_partial_spill_slot(oracle_libs, monkeypatch, slots):
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("SINKR_PARITY_SEEDS", 100))))
 def test_randomized_parity(oracle_libs, seed):
-    """SPEC.md acceptance 1-2 style: random shapes (D 32/64/128, r 1-8, B 1-3,
+    """SPEC.md acceptance 1-2 style: random shapes (D 32/64/128, r 1-16, B 1-3,
     L 1-5000), random keys and queries at random cosines to the anchor (so
     groups land on both sides of tau and near it), random routing options
     (tau, sink_on_tie, observe_only, excluded layers) -- bit-exact routing,
@@ -358,7 +376,7 @@ def test_randomized_parity(oracle_libs, seed):
     _, orc = oracle_libs
     rng = np.random.default_rng(1000 + seed)
     D = int(rng.choice([32, 64, 128]))
-    r = int(rng.choice([1, 2, 3, 4, 8]))
+    r = int(rng.choice([1, 2, 3, 4, 8, 12, 16]))
     hkv = int(rng.choice([1, 2, 4, 8]))
     B = int(rng.choice([1, 1, 2, 3]))
     L = int(rng.choice([1, 2, 63, 64, 65, 777, 2048, 5000]))
@@ -426,9 +444,10 @@ def test_randomized_batched_parity(oracle_libs, seed):
     _, orc = oracle_libs
     rng = np.random.default_rng(5000 + seed)
     D = int(rng.choice([64, 128]))
-    r = int(rng.choice([1, 2, 4, 8]))
+    r = int(rng.choice([1, 2, 4, 8, 16]))
     hkv = int(rng.choice([4, 8]))
     B = int(rng.choice([5, 12, 24, 40]))
+    B = min(B, 4096 // (hkv * r))  # B * H_q <= 4096 per engine
     hq = hkv * r
     cap = 2600
     lens = rng.integers(1, cap + 1, size=B)
