@@ -1452,6 +1452,86 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const uint32_t ntok = dry ? ((dry_regions & 1u) ? (uint32_t)kStageTok : 0u) : meta[stage].ntok;
             run_tokens += ntok;
+            if constexpr (WIDE) {
+                // the warp's 32 tokens as ONE online-softmax step: both 16-token
+                // sub-tiles' QK chains interleaved, one max / rescale / exp pass,
+                // then both PV products (two independent k16 slices)
+                const int n = (int)ntok - tb0;
+                if (n > 0) {
+                    const uint32_t kbase = ptx::smem_u32(ring + stage * C::kStageBytes);
+                    const uint32_t vbase = kbase + C::kTileBytes;
+                    float sacc[2][2][2][4];  // [sub][8-token n-tile][chain][4]
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                        for (int a = 0; a < 2; ++a)
+#pragma unroll
+                            for (int b = 0; b < 2; ++b)
+                                sacc[s2][a][b][0] = sacc[s2][a][b][1] = sacc[s2][a][b][2] = sacc[s2][a][b][3] = 0.f;
+#pragma unroll
+                    for (int kk = 0; kk < C::kNK; ++kk) {
+#pragma unroll
+                        for (int s2 = 0; s2 < 2; ++s2) {
+                            const uint32_t k_tok = tb0 + s2 * kWarpTok + ((lj >> 1) << 3) + li;
+                            uint32_t b[4];
+                            ptx::ldsm_x4(b, kbase + swz<D>(k_tok, 2 * kk + k_csel));
+                            ptx::mma_bf16(sacc[s2][0][kk & 1], qa[kk], b[0], b[1]);
+                            ptx::mma_bf16(sacc[s2][1][kk & 1], qa[kk], b[2], b[3]);
+                        }
+                    }
+                    float sc[2][4];
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int nt = j >> 1, col = j & 1;
+                            const float v = (sacc[s2][nt][0][col] + sacc[s2][nt][1][col]) +
+                                            (sacc[s2][nt][0][col + 2] + sacc[s2][nt][1][col + 2]);
+                            const int tok = s2 * kWarpTok + nt * 8 + 2 * qd + col;
+                            sc[s2][j] = tok < n ? v : -INFINITY;
+                        }
+                    float bm = fmaxf(fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[0][2], sc[0][3])),
+                                     fmaxf(fmaxf(sc[1][0], sc[1][1]), fmaxf(sc[1][2], sc[1][3])));
+                    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 1));
+                    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+                    const bool need = bm > m_used + 8.0f;
+                    if (__any_sync(0xffffffffu, need)) {
+                        const float m_new = need ? bm : m_used;
+                        const float alpha = need ? ptx::ex2(m_used - m_new) : 1.0f;
+                        l_acc *= alpha;
+#pragma unroll
+                        for (int i = 0; i < 2 * C::kNK; ++i) {
+                            o[i][0] *= alpha; o[i][1] *= alpha; o[i][2] *= alpha; o[i][3] *= alpha;
+                        }
+                        m_used = m_new;
+                    }
+                    uint32_t pa[2][4];
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        float pr[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) pr[j] = ptx::ex2(sc[s2][j] - m_used);
+                        l_acc += (pr[0] + pr[1]) + (pr[2] + pr[3]);
+                        pa[s2][0] = ptx::pack_bf16(pr[0], pr[1]);
+                        pa[s2][1] = ptx::pack_bf16(pr[0] - ptx::bf16_lo_as_f32(pa[s2][0]),
+                                                   pr[1] - ptx::bf16_hi_as_f32(pa[s2][0]));
+                        pa[s2][2] = ptx::pack_bf16(pr[2], pr[3]);
+                        pa[s2][3] = ptx::pack_bf16(pr[2] - ptx::bf16_lo_as_f32(pa[s2][2]),
+                                                   pr[3] - ptx::bf16_hi_as_f32(pa[s2][2]));
+                    }
+#pragma unroll
+                    for (int nn = 0; nn < C::kNK; ++nn) {
+#pragma unroll
+                        for (int s2 = 0; s2 < 2; ++s2) {
+                            const uint32_t v_tok = tb0 + s2 * kWarpTok + ((lj & 1) << 3) + li;
+                            uint32_t b[4];
+                            ptx::ldsm_x4_t(b, vbase + swz<D>(v_tok, 2 * nn + v_csel));
+                            ptx::mma_bf16(o[2 * nn], pa[s2], b[0], b[1]);
+                            ptx::mma_bf16(o[2 * nn + 1], pa[s2], b[2], b[3]);
+                        }
+                    }
+                }
+            } else {
 #pragma unroll
             for (int sub = 0; sub < kSub; ++sub) {
             const int tb = tb0 + sub * kWarpTok;
@@ -1515,6 +1595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             }  // sub
+            }  // !WIDE
             __syncwarp();
             if (lane == 0 && !dry) ptx::mbar_arrive(&empty[stage]);
             if (++stage == C::kStages) {
