@@ -104,6 +104,15 @@ static uint32_t static_pct() {
     }();
     return v;
 }
+// Stages of its first static range a CTA prefetches into L2 under the layer's
+// previous Active set (StepTables.spec_stages); SINKR_SPEC_STAGES overrides.
+static uint32_t spec_stages() {
+    static uint32_t v = [] {
+        const char* s = std::getenv("SINKR_SPEC_STAGES");
+        return s ? (uint32_t)std::atoi(s) : 8u;
+    }();
+    return v;
+}
 // Code prewarm of the single-sequence step (StepTables.prewarm: region bit
 // mask, 8 = all regions in CTA G-1); SINKR_PREWARM overrides (A/B runs).
 static uint32_t prewarm_default() {
@@ -188,6 +197,7 @@ struct sinkr_engine {
     float bos_ms = -1.f;
     size_t h_bos_bytes = 0;
     uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [2][U]
+    uint32_t* d_spec_mask = nullptr;    // [layers] Active bitmask of each layer's last single-sequence step
     uint32_t* d_cta_epoch = nullptr;    // [2][grid]: step-kernel launches, mode-3 steps per CTA slot
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
     // sequence-sharded peer merge (mode 3): this rank's exchange block
@@ -295,6 +305,8 @@ struct sinkr_engine {
         t.qscale = (1.0f / std::sqrt((float)D)) * 1.4426950408889634f;
         t.static_pct = static_pct();
         t.prewarm = prewarm_default();
+        t.spec_mask = d_spec_mask;
+        t.spec_stages = spec_stages();
         t.trace = d_trace;
         if (mode == 3) {
             t.peer_xchg = d_peer_xchg;
@@ -961,6 +973,8 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMalloc(&e->d_ovf, 2 * e->U * 4));
             CK(cudaMemsetAsync(e->d_ovf, 0, 2 * e->U * 4, e->stream));
             CK(cudaMemsetAsync(e->d_tokens_done, 0, 2 * e->U * 4, e->stream));
+            CK(cudaMalloc(&e->d_spec_mask, e->layers * 4));
+            CK(cudaMemsetAsync(e->d_spec_mask, 0, e->layers * 4, e->stream));
             CK(cudaMalloc(&e->d_cta_epoch, 2 * e->grid * 4));  // launches, mode-3 steps
             CK(cudaMemsetAsync(e->d_cta_epoch, 0, 2 * e->grid * 4, e->stream));
             if (const char* tr = std::getenv("SINKR_TRACE"); tr && tr[0] == '1') {
@@ -1083,6 +1097,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_peer_xchg);
     cudaFree(e->d_ovf);
     cudaFree(e->d_cta_epoch);
+    cudaFree(e->d_spec_mask);
     cudaFree(e->d_head_degen);
     cudaFree(e->d_active);
     cudaFree(e->d_prefix);

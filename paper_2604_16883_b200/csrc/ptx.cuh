@@ -116,6 +116,13 @@ __device__ __forceinline__ float ldg_last(const void* p, uint64_t pol) {
     return v;
 }
 // 2D tiled load global -> shared, completion signalled on `bar` (complete_tx).
+// one TMA box from global memory into L2 only (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x,
                                             int32_t y, uint64_t* bar, uint64_t policy) {
     asm volatile(

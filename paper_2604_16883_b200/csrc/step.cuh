@@ -43,6 +43,9 @@ constexpr unsigned long long kPrewarmLateNs = 12000;  // a dry pass longer than 
 // a late CTA joins the stream only above this many unclaimed rows (all
 // units): ~2 us of the whole grid's stream at 7 TB/s and 512 B per row
 constexpr unsigned long long kLateJoinTok = 32768;
+// the speculative L2 prefetch runs when the Active rows per CTA reach this
+// (64K per unit at 3 of 8 groups Active: 1,328; 32K: 664)
+constexpr uint32_t kSpecMinFairTok = 1024;
 constexpr uint32_t kMaxEstHeads = 2048;  // distributed form: per-CTA estimate slots (s_score overlay)
 
 // Cross-CTA counters of one step.  Two sets, used by alternate launches
@@ -99,6 +102,8 @@ struct StepTables {
     float qscale;                  // (1/sqrt(D)) * log2(e)
     uint32_t static_pct;           // static share of the unit-affine schedule (0: one Ck chunk)
     uint32_t prewarm;              // single-sequence steps: the last CTAs dry-run code regions first
+    uint32_t* spec_mask;           // [layers] single-sequence steps: Active units of the layer's last step
+    uint32_t spec_stages;          // stages of its first static range a CTA prefetches into L2 (0: off)
     unsigned long long* trace;     // optional [grid][4] per-CTA globaltimer stamps
     uint32_t* done;                // optional completion word in mapped host memory (set to 1 last)
 };
@@ -463,6 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1]
         double* sk = sq + kRouteTile * SC::kDP;
         float* est = reinterpret_cast<float*>(s_score);  // [2][kRouteTile] fp32 dot, |q|^2
+        // the layer's previous Active set (speculative prefetch below), loaded
+        // by the thread that issues the prefetch while warp 0 routes
+        const bool spec = t.spec_stages && p.inline_seqs && bid != 0 && !prewarm && tid == 32;
+        const uint32_t smask = spec ? ld_volatile(&t.spec_mask[layer]) : 0u;
         constexpr int kW = kThreads / 32;
         constexpr int kHPW = (kRouteTile + kW - 1) / kW;
         constexpr int kV = D / 32;
@@ -519,6 +528,45 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncthreads();
         STAMP(15);
+        // Speculative L2 prefetch of this CTA's first static range under the
+        // layer's previous Active set (sink heads are stable across decode
+        // steps), issued by a warp-1 thread while warp 0 routes: DRAM streams
+        // during the rest of routing and the first stages come from L2.  A
+        // hint only -- the plan comes from this step's routing; a changed set
+        // costs a few idle-time DRAM reads, never a result.  (Issued together
+        // with the routing loads, the prefetches delayed them: +1.7 us at 32K.)
+        if (spec) {
+            const uint32_t ns = __popc(smask);
+            if (ns != 0u && bid < G - n_pw) {
+                uint32_t T = 0, u = 0;
+                const uint32_t a = bid % ns;
+                uint32_t m = smask;
+                for (uint32_t i = 0; m; ++i, m &= m - 1u) {
+                    const uint32_t uu = __ffs(m) - 1;
+                    T += s_len[uu / t.Hkv];
+                    if (i == a) u = uu;
+                }
+                // long steps only: at 32K per unit the prefetches cost more than
+                // they hide (+0.7 us back to back, +1.4 L2-flushed)
+                const bool go = T >= G * kSpecMinFairTok;
+                // the chunk plan route_units builds (below) for this set
+                const uint32_t gdiv = G * kChunksPerCta;
+                uint32_t cc = (T + gdiv - 1) / gdiv;
+                cc = (cc + kStageTok - 1) / kStageTok * kStageTok;
+                const uint32_t Cs = static_chunk(T, G, t.static_pct, cc < kMinChunkTok ? kMinChunkTok : cc);
+                const uint32_t L = s_len[u / t.Hkv];
+                const uint32_t t0 = (bid / ns - (a == 0 ? 1u : 0u)) * Cs;
+                const uint32_t t1 = min(min(t0 + Cs, L), t0 + t.spec_stages * (uint32_t)kStageTok);
+                const int32_t row0 = (int32_t)((size_t(layer) * U + u) * t.cap);
+                for (uint32_t tk = t0; go && tk < t1; tk += kStageTok)
+#pragma unroll
+                    for (int hf = 0; hf < C::kHalves; ++hf) {
+                        ptx::tma_prefetch_l2_2d(t.tmk, hf * C::kBoxDim, row0 + (int32_t)tk);
+                        ptx::tma_prefetch_l2_2d(t.tmv, hf * C::kBoxDim, row0 + (int32_t)tk);
+                    }
+            }
+        }
+
         // warp 0: one unit per lane -> decisions (from the estimates, or from the
         // exact scores on the second pass), then the Active list by ballot
         auto route_units = [&](bool exact) -> bool {
@@ -598,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 misc[kMiscChunk] = cc < kMinChunkTok ? kMinChunkTok : cc;
                 misc[kMiscStatic] = static_chunk(T, G, t.static_pct, misc[kMiscChunk]);
                 misc[kMiscFlat] = 0u;  // U <= 32 < #SMs: unit-affine scheduling
+                if (lead && t.spec_stages) t.spec_mask[layer] = mask;  // the next step's guess
             }
             return true;
         };
