@@ -501,3 +501,28 @@ def test_step_runner_pinned_io_matches(oracle_libs):
         res = pin.result()
         assert [g.decision.sink for g in res.groups] == [g.decision.sink for g in info.groups]
         assert res.counters.kv_floats_loaded == info.counters.kv_floats_loaded
+
+
+def test_speculative_prefetch_changing_routes(oracle_libs):
+    """The speculative L2 prefetch guesses each layer's Active set from its
+    previous step: steps that alternate between routes (a hit, a miss, a
+    different layer, the dense route) stay bit-exact in routing and within
+    tolerance, on a cache long enough for the prefetch to run (>= 1,024 Active
+    rows per CTA)."""
+    _, orc = oracle_libs
+    specs = [WorkloadSpec(num_layers=2, layer=l, length=80000, sink_fraction=0.5, seed=17)
+             for l in (0, 1)]
+    opts = P.EngineOptions()
+    cfgs = {"routed": P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=()),
+            "dense": P.RoutingConfig(profile=P.ThresholdProfile.constant(2.0), excluded_layers=()),
+            "few": P.RoutingConfig(profile=P.ThresholdProfile.constant(-0.5), excluded_layers=(1,))}
+    q = specs[0].queries()[0]
+    refs = {}
+    with make_cache(specs[0]) as cache:
+        specs[1].fill(cache)
+        for layer, name in [(0, "routed"), (0, "routed"), (0, "dense"), (0, "routed"), (1, "few"),
+                            (0, "few"), (1, "routed"), (0, "routed")]:
+            res = P.routed_decode_step(q, layer, cache, cfgs[name], opts)
+            if (layer, name) not in refs:
+                refs[layer, name] = oracle_step(orc, specs[layer], 0, q, cfgs[name], opts)
+            assert_parity(res.outputs, refs[layer, name], specs[0].r, specs[0].head_dim, res.groups)
