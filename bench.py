@@ -491,6 +491,72 @@ def other_configs(P, torch, args, spec_cls, dense_cfg, routed_cfg):
     return out
 
 
+def shard_projection(P, torch, args, spec_cls, dense_cfg, routed_cfg, peak):
+    """One rank's share of the 8-way sequence-sharded step (north star: 512K
+    over 8 B200), run at world 1 on this GPU: the 64K-token shard with the
+    fused LL peer merge (mode 3), tau from the global length.  Per-rank
+    roofline fraction = this rank's Active K+V bytes / step time.  Labelled as
+    a projection: the exchange with 7 NVLink peers is not in these numbers."""
+    from paper_2604_16883_b200 import sharding
+
+    world, out = 8, []
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for name, hq in (("headline llama3.1-8b-attn L=524288 / 8 ranks", 32),
+                     ("C4 llama3.1-70b-attn L=524288 / 8 ranks", 64)):
+        Ls = args.length // world
+        spec = spec_cls(num_q_heads=hq, num_kv_heads=8, head_dim=128, length=Ls,
+                        sink_fraction=args.sink_fraction, seed=args.seed)
+        opts = P.EngineOptions(global_context_len=args.length)
+        with P.KvCache(P.CacheConfig(1, hq, 8, 128, Ls)) as cache:
+            spec.fill(cache)
+            P.set_timing(cache, False)
+            (pm,) = sharding.peer_merge_in_process(P, [cache])
+            dq = torch.from_numpy(spec.queries()[0]).cuda()
+            dout = torch.empty_like(dq)
+            st = torch.cuda.ExternalStream(cache.stream)
+            res = {}
+            for cname, cfg in (("routed", routed_cfg), ("dense", dense_cfg)):
+                for _ in range(5):
+                    pm.step(dq, dout, cfg, opts)
+                torch.cuda.synchronize()
+                gate(torch, st, 2.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(50):
+                    pm.step(dq, dout, cfg, opts)
+                e1.record(st)
+                torch.cuda.synchronize()
+                b2b = e0.elapsed_time(e1) / 50 * 1e3
+                evs = []
+                gate(torch, st, 0.5 * FLUSHED_REPS)
+                with torch.cuda.stream(st):
+                    for _ in range(FLUSHED_REPS):
+                        flush.sum()
+                        a = torch.cuda.Event(enable_timing=True)
+                        b = torch.cuda.Event(enable_timing=True)
+                        a.record(st)
+                        pm.step(dq, dout, cfg, opts)
+                        b.record(st)
+                        evs.append((a, b))
+                torch.cuda.synchronize()
+                res[cname] = (trimmed_mean([a.elapsed_time(b) * 1e3 for a, b in evs]), b2b)
+                if cname == "routed":
+                    n_act = P.fetch_step_info(cache).counters.groups_active
+        kvb = n_act * 2 * Ls * 128 * 2
+        row = {"config": name, "tokens_per_rank": Ls, "groups_active": n_act,
+               "routed_us": round(res["routed"][0], 2), "routed_us_back_to_back": round(res["routed"][1], 2),
+               "dense_us": round(res["dense"][0], 2), "dense_us_back_to_back": round(res["dense"][1], 2),
+               "per_rank_kv_gbs_routed": round(kvb / (res["routed"][0] * 1e-6) / 1e9, 1),
+               "per_rank_roofline_frac_routed": round(kvb / (res["routed"][0] * 1e-6) / 1e9 / peak, 3)}
+        out.append(row)
+    del flush
+    return {"rows": out, "note": "world-1 run of ONE rank's share of the 8-way sequence-sharded step "
+                                 "(64K-token shard, fused LL peer merge into a local exchange block, tau "
+                                 "from the global 512K length), routed/dense single steps behind a 256 MiB "
+                                 "L2 flush (10 %-trimmed mean of 30) and back to back; a projection, not a "
+                                 "multi-GPU measurement: the stores to 7 NVLink peers are not in it"}
+
+
 def next_rows(P, torch, args, spec_cls, peak):
     """The §8 "next" rows measured beside the hot path, each against the
     compiled reference on this host: f1 GPU score collection (routing phase
@@ -712,8 +778,31 @@ def run_ours(args, world, rank, local_rank):
         t0 = time.perf_counter()
         runner()
         e2e_ts.append((time.perf_counter() - t0) * 1e6)
-    e2e_us = statistics.median(e2e_ts)
-    e2e_mean = statistics.fmean(e2e_ts)
+    py_us = statistics.median(e2e_ts)
+    py_mean = statistics.fmean(e2e_ts)
+    # the same blocking C-ABI call (sinkr_routed_decode_step over the same
+    # pinned buffers) from a C++ decode loop -- what a reference caller, which
+    # is C++, pays per step; tools/e2e_timer.cpp times each call
+    e2e_us, e2e_mean, e2e_src = py_us, py_mean, "python"
+    try:
+        import ctypes as C
+
+        from paper_2604_16883_b200 import build as _b
+        from paper_2604_16883_b200._abi import check as _check
+
+        timer = C.CDLL(_b.BENCH_LIB).sinkr_bench_time_steps
+        timer.restype = C.c_int
+        timer.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t] + [C.c_void_p] * 6 + [C.c_size_t, C.c_void_p]
+        h, _, layer_, cfg_p, opt_p, out_p, grp_p, hs_p, ctr_p = runner._args
+        n_c = max(args.steps, 200)
+        us_c = np.zeros(n_c)
+        timer(h, runner.queries.ctypes.data, 0, cfg_p, opt_p, out_p, grp_p, hs_p, ctr_p, 10,
+              us_c.ctypes.data)  # warm-up
+        _check(timer(h, runner.queries.ctypes.data, 0, cfg_p, opt_p, out_p, grp_p, hs_p, ctr_p, n_c,
+                     us_c.ctypes.data))
+        e2e_us, e2e_mean, e2e_src = float(np.median(us_c)), float(np.mean(us_c)), "cabi"
+    except (OSError, AttributeError) as ex:  # bench-support library not built
+        print(f"bench: C-ABI e2e timer unavailable ({ex}); e2e from the Python loop", file=sys.stderr)
     res_host = runner.result()
     h2d, d2h = cache.step_io_bytes()
 
@@ -768,9 +857,13 @@ def run_ours(args, world, rank, local_rank):
                      "alg_bytes_per_launch": alg_r, "peak_source": peak_src},
         "e2e": {"value": round(e2e_us, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "mean_us": round(e2e_mean, 2), "calls": len(e2e_ts),
-                "method": "host clock around each blocking StepRunner call (H2D of the "
-                          "pinned query buffer, step, routing record + outputs into pinned "
-                          "host memory), median"},
+                "method": ("steady clock around each blocking sinkr_routed_decode_step call of a "
+                           "C++ decode loop (tools/e2e_timer.cpp): H2D of the pinned query "
+                           "buffer, step, routing record + outputs into pinned host memory; median"
+                           if e2e_src == "cabi" else
+                           "host clock around each blocking StepRunner call, median"),
+                "python_step_runner_us": round(py_us, 2),
+                "python_step_runner_mean_us": round(py_mean, 2)},
         "gpu_launches": nlaunch * args.steps,
         "clocks": clk.summary(),
     }
@@ -816,6 +909,11 @@ def run_ours(args, world, rank, local_rank):
     cache.close()
     if not args.no_sweep:
         line["other_configs"] = other_configs(P, torch, args, WorkloadSpec, dense_cfg, routed_cfg)
+        try:
+            line["sharded_8way_projection"] = shard_projection(P, torch, args, WorkloadSpec, dense_cfg,
+                                                               routed_cfg, peak)
+        except Exception as e:  # report, never lose the headline line
+            line["sharded_8way_projection"] = {"failed": f"{type(e).__name__}: {e}"}
         try:
             line["next_rows"] = next_rows(P, torch, args, WorkloadSpec, peak)
         except Exception as e:  # reported, never silently dropped

@@ -16,6 +16,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libsinkr_cuda.so")
+# bench support (tools/e2e_timer.cpp): a C++ caller's timed decode loop
+BENCH_LIB = os.path.join(LIB_DIR, "libsinkr_bench.so")
+TOOLS = os.path.join(HERE, "tools")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -45,8 +48,23 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps)
 
 
+def build_bench_lib(force: bool = False) -> str:
+    src = os.path.join(TOOLS, "e2e_timer.cpp")
+    if (not force and os.path.exists(BENCH_LIB) and os.path.exists(LIB)
+            and os.path.getmtime(BENCH_LIB) >= max(os.path.getmtime(src), os.path.getmtime(LIB))):
+        return BENCH_LIB
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", os.path.join(ROOT, "include"), src,
+           "-L", LIB_DIR, "-lsinkr_cuda", "-Wl,-rpath,$ORIGIN", "-o", BENCH_LIB + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("g++ failed:\n" + res.stdout + res.stderr)
+    os.replace(BENCH_LIB + ".tmp", BENCH_LIB)
+    return BENCH_LIB
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
+        build_bench_lib()
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
     cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo",
@@ -61,6 +79,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(LIB + ".tmp", LIB)
+    build_bench_lib(force=True)
     return LIB
 
 
