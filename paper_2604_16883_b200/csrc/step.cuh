@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* est = reinterpret_cast<float*>(s_score);  // [2][kRouteTile] fp32 dot, |q|^2
         // the layer's previous Active set (speculative prefetch below), loaded
         // by the thread that issues the prefetch while warp 0 routes
-        const bool spec = t.spec_stages && p.inline_seqs && bid != 0 && !prewarm && tid == 32;
+        const bool spec = t.spec_stages && p.inline_seqs && bid != 0 && !prewarm && warp == 1;
         const uint32_t smask = spec ? ld_volatile(&t.spec_mask[layer]) : 0u;
         constexpr int kW = kThreads / 32;
         constexpr int kHPW = (kRouteTile + kW - 1) / kW;
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         STAMP(15);
         // Speculative L2 prefetch of this CTA's first static range under the
         // layer's previous Active set (sink heads are stable across decode
-        // steps), issued by a warp-1 thread while warp 0 routes: DRAM streams
+        // steps), issued by warp 1 (a box per lane) while warp 0 routes: DRAM streams
         // during the rest of routing and the first stages come from L2.  A
         // hint only -- the plan comes from this step's routing; a changed set
         // costs a few idle-time DRAM reads, never a result.  (Issued together
@@ -558,12 +558,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t t0 = (bid / ns - (a == 0 ? 1u : 0u)) * Cs;
                 const uint32_t t1 = min(min(t0 + Cs, L), t0 + t.spec_stages * (uint32_t)kStageTok);
                 const int32_t row0 = (int32_t)((size_t(layer) * U + u) * t.cap);
-                for (uint32_t tk = t0; go && tk < t1; tk += kStageTok)
-#pragma unroll
-                    for (int hf = 0; hf < C::kHalves; ++hf) {
-                        ptx::tma_prefetch_l2_2d(t.tmk, hf * C::kBoxDim, row0 + (int32_t)tk);
-                        ptx::tma_prefetch_l2_2d(t.tmv, hf * C::kBoxDim, row0 + (int32_t)tk);
-                    }
+                // one box per lane (every lane of warp 1 computed the plan)
+                const uint32_t nbox = go && t1 > t0 ? (t1 - t0 + kStageTok - 1) / kStageTok * 2 * C::kHalves : 0u;
+                for (uint32_t i = lane; i < nbox; i += 32) {
+                    const uint32_t st = i / (2 * C::kHalves), hf = (i / 2) % C::kHalves;
+                    ptx::tma_prefetch_l2_2d((i & 1) ? t.tmv : t.tmk, (int32_t)hf * C::kBoxDim,
+                                            row0 + (int32_t)(t0 + st * kStageTok));
+                }
             }
         }
 
