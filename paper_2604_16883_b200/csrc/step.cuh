@@ -47,6 +47,9 @@ constexpr unsigned long long kLateJoinTok = 32768;
 // (64K per unit at 3 of 8 groups Active: 1,328; 32K: 664)
 constexpr uint32_t kSpecMinFairTok = 1024;
 constexpr uint32_t kMaxEstHeads = 2048;  // distributed form: per-CTA estimate slots (s_score overlay)
+// LEAN routing scratch in sm_o (bytes): est [2][64] f32, s_score [64] f64,
+// s_degen [64] u8, s_tau [64] f64, s_len [64] u32 (B*H_q <= 64)
+constexpr int kLsScore = 512, kLsDegen = 1024, kLsTau = 1088, kLsLen = 1600, kLsBytes = 1856;
 
 // Cross-CTA counters of one step.  Two sets, used by alternate launches
 // (parity of the per-CTA launch count, StepTables.cta_epoch): a launch zeroes
@@ -130,6 +133,7 @@ struct StepCfg {
     static constexpr int kOvSeq = kOvDegen + kMaxStepHeads;             // tau f64 [B], len u32 [B]
     static_assert(kOvSeq + 12 * kMaxUnits <= kRing, "routing overlay exceeds the ring");
     static_assert(kSmemBytes <= 232448, "step kernel shared memory");
+    static_assert(kLsBytes <= kCWarps * kMaxR * C::kOStride * 4, "LEAN routing scratch exceeds sm_o");
 };
 
 // misc smem words
@@ -329,10 +333,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint16_t* act_unit = reinterpret_cast<uint16_t*>(smem + SC::kOffAct);
     uint32_t* act_prefix = reinterpret_cast<uint32_t*>(smem + SC::kOffPrefix);
     uint32_t* act_len = reinterpret_cast<uint32_t*>(smem + SC::kOffLen);  // rows per Active entry
-    double* s_score = reinterpret_cast<double*>(ring + SC::kOvScore);
-    uint8_t* s_degen = ring + SC::kOvDegen;
-    double* s_tau = reinterpret_cast<double*>(ring + SC::kOvSeq);                 // [B]
-    uint32_t* s_len = reinterpret_cast<uint32_t*>(ring + SC::kOvSeq + 8 * kMaxUnits);  // [B]
+    // routing scratch: the single-sequence (LEAN) form keeps its ~2 KB in the
+    // flush staging sm_o (idle until the first flush), so the ring stays free
+    // during routing; the distributed form overlays the ring
+    uint8_t* const ls = reinterpret_cast<uint8_t*>(sm_o);
+    double* s_score = LEAN ? reinterpret_cast<double*>(ls + kLsScore) : reinterpret_cast<double*>(ring + SC::kOvScore);
+    uint8_t* s_degen = LEAN ? ls + kLsDegen : ring + SC::kOvDegen;
+    double* s_tau = LEAN ? reinterpret_cast<double*>(ls + kLsTau) : reinterpret_cast<double*>(ring + SC::kOvSeq);  // [B]
+    uint32_t* s_len = LEAN ? reinterpret_cast<uint32_t*>(ls + kLsLen)
+                           : reinterpret_cast<uint32_t*>(ring + SC::kOvSeq + 8 * kMaxUnits);  // [B]
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t G = gridDim.x, bid = blockIdx.x;
@@ -384,22 +393,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define STAMP(i) do { if (lead && tid == 0) dbg[i] = clock64(); } while (0)
     STAMP(0);
     STAMP(1);
-    // per-sequence tau / length into smem once (no dynamic indexing of the
-    // parameter block in the loops below)
-    if (p.inline_seqs) {
-        if (tid == 0) {
-#pragma unroll
-            for (int k = 0; k < kParamSeqs; ++k) {  // compile-time indices: plain LDC
-                s_tau[k] = p.tau[k];
-                s_len[k] = p.len[k];
-            }
-        }
-    } else {
-        for (uint32_t sq = tid; sq < t.B; sq += kThreads) {
-            s_tau[sq] = __ldg(&t.tau_g[sq]);
-            s_len[sq] = __ldg(&t.len_g[sq]);
-        }
-    }
     // Code prewarm (single-sequence steps).  A decode step in a model runs
     // with a cold L2, so every code region a step enters for the first time
     // is fetched from DRAM -- by all 148 SMs at once, on the critical path
@@ -440,6 +433,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t pass = prewarm ? 0u : 1u; pass < 2u; ++pass) {
     const bool dry = pass == 0u;
     if (!dry) {
+    // per-sequence tau / length into smem once (no dynamic indexing of the
+    // parameter block in the loops below; after the dry pass, which uses sm_o)
+    if (p.inline_seqs) {
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < kParamSeqs; ++k) {  // compile-time indices: plain LDC
+                s_tau[k] = p.tau[k];
+                s_len[k] = p.len[k];
+            }
+        }
+    } else {
+        for (uint32_t sq = tid; sq < t.B; sq += kThreads) {
+            s_tau[sq] = __ldg(&t.tau_g[sq]);
+            s_len[sq] = __ldg(&t.len_g[sq]);
+        }
+    }
     // ======================= phase R: routing ================================
     // proxy_score (router.cpp:36-48), group_score (50-57), route (67-75) and the
     // task build (131-145).  Two forms with identical results:
@@ -465,9 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // exact in fp64, so s + p is bit-identical to the reference's
         // `s += (double)q[i] * k0[i]`), thread h runs its head's dot and |q|^2
         // chains (sequential DADDs in index order), and warp 0 routes.
-        double* sq = reinterpret_cast<double*>(ring + SC::kOvProd);  // [kRouteTile][D+1]
-        double* sk = sq + kRouteTile * SC::kDP;
-        float* est = reinterpret_cast<float*>(s_score);  // [2][kRouteTile] fp32 dot, |q|^2
+        float* est = reinterpret_cast<float*>(ls);  // [2][kRouteTile] fp32 dot, |q|^2
         // the layer's previous Active set (speculative prefetch below), loaded
         // by the thread that issues the prefetch while warp 0 routes
         const bool spec = t.spec_stages && p.inline_seqs && bid != 0 && !prewarm && warp == 1;
@@ -659,40 +666,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
         STAMP(16);
         if (!misc[kMiscFast]) {
-            // exact scores before any decision: products, chains, then route
-#pragma unroll
-            for (int a = 0; a < kHPW; ++a) {
-                const uint32_t h = warp + a * kW;
-                if (h < NH) {
-#pragma unroll
-                    for (int e = 0; e < kV; ++e) {
-                        const uint32_t idx = (e + lane) % kV;
-                        float qf = qv[a][0], kf = kv[a][0];
-#pragma unroll
-                        for (int c = 1; c < kV; ++c)
-                            if (idx == (uint32_t)c) {
-                                qf = qv[a][c];
-                                kf = kv[a][c];
-                            }
-                        const double qd = (double)qf;
-                        sq[h * SC::kDP + kV * lane + idx] = __dmul_rn(qd, (double)kf);
-                        sk[h * SC::kDP + kV * lane + idx] = __dmul_rn(qd, qd);
-                    }
-                }
-            }
-            __syncthreads();
+            // exact scores before any decision: thread h runs its head's dot
+            // and |q|^2 chains over its q row and its group's k0 row (in L2:
+            // the estimate just loaded them), the products exact in fp64 off
+            // the chain, each a sequential fp64 sum in index order
+            // (router.cpp:40-43) -- no shared-memory staging, so the ring
+            // stays free for the speculative stages
             if (tid < NH) {
-                // the dot and |q|^2 chains of head tid, interleaved: each a
-                // sequential fp64 sum in index order (router.cpp:40-43)
                 const uint32_t u = tid / r;
+                const float4* qrow = reinterpret_cast<const float4*>(t.q + size_t(tid) * D);
+                const float4* krow = reinterpret_cast<const float4*>(t.anchors + (size_t(layer) * U + u) * D);
                 const float kn = ptx::ldg_last(&t.anchor_norm[size_t(layer) * U + u], ptx::policy_evict_last());
-                const double* pa = sq + tid * SC::kDP;
-                const double* pb = sk + tid * SC::kDP;
                 double dot = 0.0, qq = 0.0;
-#pragma unroll 16
-                for (uint32_t j = 0; j < (uint32_t)D; ++j) {
-                    dot = __dadd_rn(dot, pa[j]);
-                    qq = __dadd_rn(qq, pb[j]);
+#pragma unroll 8
+                for (int c = 0; c < D / 4; ++c) {
+                    const float4 x = __ldg(qrow + c), y = __ldg(krow + c);
+                    const float qf[4] = {x.x, x.y, x.z, x.w}, kf[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const double qd = (double)qf[e];
+                        dot = __dadd_rn(dot, __dmul_rn(qd, (double)kf[e]));
+                        qq = __dadd_rn(qq, __dmul_rn(qd, qd));
+                    }
                 }
                 const double qn = __dsqrt_rn(qq);
                 double sc = 0.0;
