@@ -617,10 +617,13 @@ def next_rows(P, torch, args, spec_cls, peak):
     with tempfile.TemporaryDirectory() as d:
         rc.save_snapshot(d)
         nbytes = 2 * 8 * spec.length * 128 * 4
-        t0 = time.perf_counter()
-        c2 = P.KvCache.load_snapshot(d)
-        ours_s = time.perf_counter() - t0
-        c2.close()
+        loads = []
+        for _ in range(3):  # best of 3 (the first can pay one-time driver work)
+            t0 = time.perf_counter()
+            c2 = P.KvCache.load_snapshot(d)
+            loads.append(time.perf_counter() - t0)
+            c2.close()
+        ours_s = min(loads)
         # the replay alone (engine already created): file reads + uploads +
         # device conversion, pipelined across slots
         reps = []
@@ -640,7 +643,7 @@ def next_rows(P, torch, args, spec_cls, peak):
                                "replay_s": round(replay_s, 3), "replay_gbs": round(nbytes / replay_s / 1e9, 2),
                                "reference_s": round(ref_s, 3),
                                "note": "reference-written SNKT snapshot; engine_s: load_snapshot (engine "
-                                       "creation + replay); replay_s: load_snapshot_into an existing engine "
+                                       "creation + replay, best of 3); replay_s: load_snapshot_into an existing engine "
                                        "(best of 3): file reads into pinned memory, upload and device bf16 "
                                        "conversion pipelined across slots; reference: load_snapshot, "
                                        "row-by-row append"}
