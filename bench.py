@@ -807,6 +807,30 @@ def run_ours(args, world, rank, local_rank):
     except (OSError, AttributeError) as ex:  # bench-support library not built
         print(f"bench: C-ABI e2e timer unavailable ({ex}); e2e from the Python loop", file=sys.stderr)
     res_host = runner.result()
+    # ---- append + step: the reference decode loop appends the new token's K/V
+    # to every slot and then steps over the grown cache; one
+    # call = one graph (upload of params + q + the new rows, append kernel,
+    # step kernel), on a cache with room to grow
+    append_us = None
+    try:
+        with P.KvCache(P.CacheConfig(1, 32, 8, 128, L + 1024)) as ca:
+            spec.fill(ca)
+            P.set_timing(ca, False)
+            arun = P.AppendStepRunner(ca, routed_cfg, pinned_io=True)
+            arun.queries[...] = np.asarray(q_host).reshape(arun.queries.shape)
+            rng_a = np.random.default_rng(args.seed)
+            kn = rng_a.standard_normal((8, 128)).astype(np.float32)
+            vn = rng_a.standard_normal((8, 128)).astype(np.float32)
+            for _ in range(5):
+                arun(kn, vn)
+            ts_a = []
+            for _ in range(200):
+                t0 = time.perf_counter()
+                arun(kn, vn)
+                ts_a.append((time.perf_counter() - t0) * 1e6)
+            append_us = statistics.median(ts_a)
+    except Exception as ex:  # report, never lose the headline line
+        print(f"bench: append+step e2e failed: {ex}", file=sys.stderr)
     h2d, d2h = cache.step_io_bytes()
 
     # DRAM bytes per launch of this kernel from the committed ncu capture of
@@ -866,7 +890,12 @@ def run_ours(args, world, rank, local_rank):
                            if e2e_src == "cabi" else
                            "host clock around each blocking StepRunner call, median"),
                 "python_step_runner_us": round(py_us, 2),
-                "python_step_runner_mean_us": round(py_mean, 2)},
+                "python_step_runner_mean_us": round(py_mean, 2),
+                "append_step_us": None if append_us is None else round(append_us, 2),
+                "append_step_method": "AppendStepRunner (sinkr_decode_append_step): append the new "
+                                      "token's K/V (host f32, 8 KB) to all 8 slots, then the routed "
+                                      "step over L+1 tokens, one graph per call; Python loop, median "
+                                      "of 200"},
         "gpu_launches": nlaunch * args.steps,
         "clocks": clk.summary(),
     }

@@ -117,3 +117,16 @@ def test_config_validation_mirrors_reference(L):
     for cfg in bad:
         with pytest.raises(ValueError):
             P.KvCache(cfg)
+
+
+def test_bench_support_library(L):
+    """The bench's C++ decode-loop timer (tools/e2e_timer.cpp) is built beside
+    the product library, links against it and exports its one entry point;
+    the product library does not carry it."""
+    build.build_bench_lib()
+    nm = subprocess.run(["nm", "-D", "--defined-only", build.BENCH_LIB], capture_output=True, text=True)
+    assert re.search(r"\bT sinkr_bench_time_steps\b", nm.stdout)
+    ldd = subprocess.run(["ldd", build.BENCH_LIB], capture_output=True, text=True).stdout
+    assert "libsinkr_cuda.so" in ldd
+    prod = subprocess.run(["nm", "-D", "--defined-only", build.LIB], capture_output=True, text=True).stdout
+    assert "sinkr_bench_time_steps" not in prod
