@@ -137,7 +137,7 @@ struct StepCfg {
 };
 
 // misc smem words
-enum : int { kMiscNact = 0, kMiscChunk, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast, kMiscPeerLate,
+enum : int { kMiscNact = 0, kMiscChunk, kMiscSlot, kMiscLast, kMiscTask, kMiscFlat, kMiscFast,
              kMiscStatic };
 
 // Unit-affine scheduling: the static first range of a CTA is static_pct % of
@@ -1013,8 +1013,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     lean_fast = lean && misc[kMiscFast] != 0;
     // mode 3: partial slots double-buffered by step parity (a rank one step
     // ahead never overwrites partials a slower rank is still merging).  The
-    // step number lives on the device (advanced by the last CTA at exit, after
-    // every CTA has read it), so the graph needs no per-step parameter patch.
+    // step number is each CTA slot's own count of mode-3 launches
+    // (cta_epoch[G + bid], advanced by that CTA at exit), so the graph needs
+    // no per-step parameter patch.
     xoff = (size_t((epoch & 1u) * t.world + t.rank)) * U * (r * (D + 2));
     __syncthreads();  // routing overlay dead from here on; the ring is free
     STAMP(8);
