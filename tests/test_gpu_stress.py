@@ -1,7 +1,8 @@
 """GPU stress: many back-to-back steps across the kernel's code paths on one
 engine set (lean / distributed routing, estimate-first / exact-first
 decisions, unit-affine / global-token scheduling, queue / per-unit merge,
-modes 0 / 1 / 3), interleaved, each compared with a fresh single step and with
+modes 0 / 1 / 3, the speculative prefetch hitting and missing, GQA width 16),
+interleaved, each compared with a fresh single step and with
 the previous replay of the same configuration.  Counters and locks must be
 restored by every step; no step may report a kernel error."""
 import os
@@ -28,6 +29,11 @@ def test_interleaved_paths_stay_consistent():
         "lean-r8": WorkloadSpec(num_q_heads=64, num_kv_heads=8, length=9000, sink_fraction=0.375, seed=2),
         "dist": WorkloadSpec(num_q_heads=32, num_kv_heads=4, num_seqs=6, length=7000, sink_fraction=0.5, seed=3),
         "flat": WorkloadSpec(num_q_heads=40, num_kv_heads=40, num_seqs=6, length=3000, sink_fraction=0.25, seed=4),
+        # long enough for the speculative L2 prefetch (>= 1,024 Active rows per CTA)
+        "long": WorkloadSpec(length=80000, sink_fraction=0.5, seed=5),
+        # GQA width 16: the WIDE instantiation, single-sequence and distributed
+        "wide": WorkloadSpec(num_q_heads=16, num_kv_heads=1, length=30000, sink_fraction=0.0, seed=6),
+        "wide-dist": WorkloadSpec(num_q_heads=128, num_kv_heads=8, length=5000, sink_fraction=0.5, seed=7),
     }
     caches, qs, refs, outs = {}, {}, {}, {}
     cfgs = {"routed": _cfg(0.5), "dense": _cfg(2.0), "tie_exact": None}
