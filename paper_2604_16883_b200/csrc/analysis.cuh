@@ -41,8 +41,8 @@ constexpr int kBosCWarps = 8;                  // consumer warps, 16 tokens each
 constexpr int kBosThreads = 32 * (1 + kBosCWarps);
 constexpr int kBosTok = kWarpTok * kBosCWarps;  // tokens per stage (2 per SMSP in flight)
 constexpr int kBosBoxes = kBosTok / kStageTok;  // 64-row TMA boxes per stage and half
-constexpr int kBosHeads = 8;                   // heads per unit (mma rows 0-7)
-static_assert(kBosHeads >= kMaxR, "one stream pass covers a GQA group (mma rows 0-7)");
+constexpr int kBosHeads = 16;                  // heads per unit: up to two 8-head mma tiles
+static_assert(kBosHeads >= kMaxRWide, "one stream pass covers a GQA group");
 
 struct BosArgs {
     const uint32_t* pre;      // [n_units + 1] token prefix over the launch's units
@@ -115,7 +115,9 @@ __device__ __forceinline__ void bos_finish_head(const BosArgs& a, uint32_t i, ui
     }
 }
 
-template <int D>
+// NT: 8-head query tiles per group (1: r <= 8; 2: r <= 16, each K fragment
+// feeds both tiles' MMAs)
+template <int D, int NT>
 __global__ void __launch_bounds__(kBosThreads, 1)
     bos_stream_kernel(const __grid_constant__ CUtensorMap tmk, BosArgs a) {
     using C = BosCfg<D>;
@@ -214,45 +216,52 @@ __global__ void __launch_bounds__(kBosThreads, 1)
         const int grp = lane >> 2, qd = lane & 3;
         const int lj = lane >> 3, li = lane & 7;
         const uint32_t k_tok = tb + ((lj >> 1) << 3) + li, k_csel = lj & 1;
-        const uint32_t nh = a.r;  // <= kMaxR <= kBosHeads: one pass covers the group
-        const bool live = grp < (int)nh;
+        const uint32_t nh = a.r;  // <= 8 * NT: one pass covers the group
 
-        uint32_t q1[C::kNK][4], q2[C::kNK][2];  // A1 = [hi; lo], A2 = [lo2; 0]
-        float m = -INFINITY, l = 0.f;
+        // per tile: A1 = [hi; lo], A2 = [lo2; 0] of heads 8 ht + grp
+        uint32_t q1[NT][C::kNK][4], q2[NT][C::kNK][2];
+        float m[NT], l[NT];
         uint32_t cur = kEnd;
 
         auto load_q = [&](uint32_t i) {
-            const float* qrow = a.q + (size_t(a.u_first + i) * a.r + (live ? grp : 0)) * D;
 #pragma unroll
-            for (int kk = 0; kk < C::kNK; ++kk) {
+            for (int ht = 0; ht < NT; ++ht) {
+                const bool live = 8 * ht + grp < (int)nh;
+                const float* qrow = a.q + (size_t(a.u_first + i) * a.r + (live ? 8 * ht + grp : 0)) * D;
 #pragma unroll
-                for (int hv = 0; hv < 2; ++hv) {
-                    float2 x = make_float2(0.f, 0.f);
-                    if (live) x = *reinterpret_cast<const float2*>(qrow + 16 * kk + 8 * hv + 2 * qd);
-                    x.x *= a.qscale;
-                    x.y *= a.qscale;
-                    const uint32_t hi = ptx::pack_bf16(x.x, x.y);
-                    const float r0 = x.x - ptx::bf16_lo_as_f32(hi), r1 = x.y - ptx::bf16_hi_as_f32(hi);
-                    const uint32_t lo = ptx::pack_bf16(r0, r1);
-                    q1[kk][2 * hv] = hi;
-                    q1[kk][2 * hv + 1] = lo;
-                    q2[kk][hv] = ptx::pack_bf16(r0 - ptx::bf16_lo_as_f32(lo), r1 - ptx::bf16_hi_as_f32(lo));
+                for (int kk = 0; kk < C::kNK; ++kk) {
+#pragma unroll
+                    for (int hv = 0; hv < 2; ++hv) {
+                        float2 x = make_float2(0.f, 0.f);
+                        if (live) x = *reinterpret_cast<const float2*>(qrow + 16 * kk + 8 * hv + 2 * qd);
+                        x.x *= a.qscale;
+                        x.y *= a.qscale;
+                        const uint32_t hi = ptx::pack_bf16(x.x, x.y);
+                        const float r0 = x.x - ptx::bf16_lo_as_f32(hi), r1 = x.y - ptx::bf16_hi_as_f32(hi);
+                        const uint32_t lo = ptx::pack_bf16(r0, r1);
+                        q1[ht][kk][2 * hv] = hi;
+                        q1[ht][kk][2 * hv + 1] = lo;
+                        q2[ht][kk][hv] = ptx::pack_bf16(r0 - ptx::bf16_lo_as_f32(lo), r1 - ptx::bf16_hi_as_f32(lo));
+                    }
                 }
             }
         };
         auto flush = [&](uint32_t i) {
-            float mo = __shfl_xor_sync(0xffffffffu, m, 1), lo = __shfl_xor_sync(0xffffffffu, l, 1);
-            float mx = fmaxf(m, mo);
-            l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
-            m = mx;
-            mo = __shfl_xor_sync(0xffffffffu, m, 2);
-            lo = __shfl_xor_sync(0xffffffffu, l, 2);
-            mx = fmaxf(m, mo);
-            l = mx == -INFINITY ? 0.f : l * exp2f(m - mx) + lo * exp2f(mo - mx);
-            m = mx;
-            if (qd == 0) {
-                sm_ml[(cw * kBosHeads + grp) * 2] = m;
-                sm_ml[(cw * kBosHeads + grp) * 2 + 1] = l;
+#pragma unroll
+            for (int ht = 0; ht < NT; ++ht) {
+                float mo = __shfl_xor_sync(0xffffffffu, m[ht], 1), lo = __shfl_xor_sync(0xffffffffu, l[ht], 1);
+                float mx = fmaxf(m[ht], mo);
+                l[ht] = mx == -INFINITY ? 0.f : l[ht] * exp2f(m[ht] - mx) + lo * exp2f(mo - mx);
+                m[ht] = mx;
+                mo = __shfl_xor_sync(0xffffffffu, m[ht], 2);
+                lo = __shfl_xor_sync(0xffffffffu, l[ht], 2);
+                mx = fmaxf(m[ht], mo);
+                l[ht] = mx == -INFINITY ? 0.f : l[ht] * exp2f(m[ht] - mx) + lo * exp2f(mo - mx);
+                m[ht] = mx;
+                if (qd == 0) {
+                    sm_ml[(cw * kBosHeads + 8 * ht + grp) * 2] = m[ht];
+                    sm_ml[(cw * kBosHeads + 8 * ht + grp) * 2 + 1] = l[ht];
+                }
             }
             if (ctid == 0) sm_slot[0] = atomicAdd(&a.ctr[1 + i], 1u);
             ptx::named_bar_sync(1, kBosCWarps * 32);
@@ -282,55 +291,69 @@ __global__ void __launch_bounds__(kBosThreads, 1)
                 if (cur != kEnd) flush(cur);
                 cur = unit;
                 load_q(unit);
-                m = -INFINITY;
-                l = 0.f;
+#pragma unroll
+                for (int ht = 0; ht < NT; ++ht) {
+                    m[ht] = -INFINITY;
+                    l[ht] = 0.f;
+                }
             }
             const uint32_t tok0 = meta[stage].tok0;
             const int n = (int)meta[stage].ntok - tb;
             if (n > 0) {
                 const uint32_t kbase = ptx::smem_u32(ring + stage * C::kStageBytes);
-                float s1[2][2][4], s2[2][4];
+                float s1[NT][2][2][4], s2[NT][2][4];
 #pragma unroll
-                for (int x = 0; x < 2; ++x) {
-                    s2[x][0] = s2[x][1] = s2[x][2] = s2[x][3] = 0.f;
+                for (int ht = 0; ht < NT; ++ht)
 #pragma unroll
-                    for (int y = 0; y < 2; ++y) s1[x][y][0] = s1[x][y][1] = s1[x][y][2] = s1[x][y][3] = 0.f;
-                }
+                    for (int x = 0; x < 2; ++x) {
+                        s2[ht][x][0] = s2[ht][x][1] = s2[ht][x][2] = s2[ht][x][3] = 0.f;
+#pragma unroll
+                        for (int y = 0; y < 2; ++y)
+                            s1[ht][x][y][0] = s1[ht][x][y][1] = s1[ht][x][y][2] = s1[ht][x][y][3] = 0.f;
+                    }
 #pragma unroll
                 for (int kk = 0; kk < C::kNK; ++kk) {
                     uint32_t b[4];
                     ptx::ldsm_x4(b, kbase + bos_swz<D>(k_tok, 2 * kk + k_csel));
-                    const uint32_t a2[4] = {q2[kk][0], 0u, q2[kk][1], 0u};
-                    ptx::mma_bf16(s1[0][kk & 1], q1[kk], b[0], b[1]);
-                    ptx::mma_bf16(s1[1][kk & 1], q1[kk], b[2], b[3]);
-                    ptx::mma_bf16(s2[0], a2, b[0], b[1]);
-                    ptx::mma_bf16(s2[1], a2, b[2], b[3]);
-                }
-                float z[4];
-                float bm = -INFINITY;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int nt = j >> 1, col = j & 1;
-                    const float hi = s1[nt][0][col] + s1[nt][1][col];
-                    const float lo = s1[nt][0][col + 2] + s1[nt][1][col + 2];
-                    const int tok = nt * 8 + 2 * qd + col;
-                    z[j] = tok < n ? (hi + lo) + s2[nt][col] : -INFINITY;
-                    bm = fmaxf(bm, z[j]);
-                }
-                if (tok0 + tb == 0 && live && qd == 0)  // token 0 of the unit: j = 0 of lane quad 0
-                    a.z0[size_t(a.u_first + unit) * a.r + grp] = z[0];
-                if (a.zout != nullptr && live) {  // attention_weights: keep every logit
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int tok = (j >> 1) * 8 + 2 * qd + (j & 1);
-                        if (tok < n) a.zout[size_t(grp) * a.pre[1] + tok0 + tb + tok] = z[j];
+                    for (int ht = 0; ht < NT; ++ht) {
+                        const uint32_t a2[4] = {q2[ht][kk][0], 0u, q2[ht][kk][1], 0u};
+                        ptx::mma_bf16(s1[ht][0][kk & 1], q1[ht][kk], b[0], b[1]);
+                        ptx::mma_bf16(s1[ht][1][kk & 1], q1[ht][kk], b[2], b[3]);
+                        ptx::mma_bf16(s2[ht][0], a2, b[0], b[1]);
+                        ptx::mma_bf16(s2[ht][1], a2, b[2], b[3]);
                     }
                 }
-                if (bm != -INFINITY) {
-                    const float mn = fmaxf(m, bm);
-                    l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) +
-                        ((exp2f(z[0] - mn) + exp2f(z[1] - mn)) + (exp2f(z[2] - mn) + exp2f(z[3] - mn)));
-                    m = mn;
+#pragma unroll
+                for (int ht = 0; ht < NT; ++ht) {
+                    const int head = 8 * ht + grp;
+                    const bool live = head < (int)nh;
+                    float z[4];
+                    float bm = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int nt = j >> 1, col = j & 1;
+                        const float hi = s1[ht][nt][0][col] + s1[ht][nt][1][col];
+                        const float lo = s1[ht][nt][0][col + 2] + s1[ht][nt][1][col + 2];
+                        const int tok = nt * 8 + 2 * qd + col;
+                        z[j] = tok < n ? (hi + lo) + s2[ht][nt][col] : -INFINITY;
+                        bm = fmaxf(bm, z[j]);
+                    }
+                    if (tok0 + tb == 0 && live && qd == 0)  // token 0 of the unit: j = 0 of lane quad 0
+                        a.z0[size_t(a.u_first + unit) * a.r + head] = z[0];
+                    if (a.zout != nullptr && live) {  // attention_weights: keep every logit
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int tok = (j >> 1) * 8 + 2 * qd + (j & 1);
+                            if (tok < n) a.zout[size_t(head) * a.pre[1] + tok0 + tb + tok] = z[j];
+                        }
+                    }
+                    if (bm != -INFINITY) {
+                        const float mn = fmaxf(m[ht], bm);
+                        l[ht] = (m[ht] == -INFINITY ? 0.f : l[ht] * exp2f(m[ht] - mn)) +
+                                ((exp2f(z[0] - mn) + exp2f(z[1] - mn)) + (exp2f(z[2] - mn) + exp2f(z[3] - mn)));
+                        m[ht] = mn;
+                    }
                 }
             }
             __syncwarp();

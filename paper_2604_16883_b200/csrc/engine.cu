@@ -1023,12 +1023,17 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaFuncSetAttribute(dev::decode_kernel<128>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem_bytes<128>()));
-            CK(cudaFuncSetAttribute(dev::bos_stream_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dev::BosCfg<32>::kSmemBytes));
-            CK(cudaFuncSetAttribute(dev::bos_stream_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dev::BosCfg<64>::kSmemBytes));
-            CK(cudaFuncSetAttribute(dev::bos_stream_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dev::BosCfg<128>::kSmemBytes));
+            for (int nt = 1; nt <= 2; ++nt) {
+                CK(cudaFuncSetAttribute(nt == 1 ? (const void*)dev::bos_stream_kernel<32, 1>
+                                                : (const void*)dev::bos_stream_kernel<32, 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, dev::BosCfg<32>::kSmemBytes));
+                CK(cudaFuncSetAttribute(nt == 1 ? (const void*)dev::bos_stream_kernel<64, 1>
+                                                : (const void*)dev::bos_stream_kernel<64, 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, dev::BosCfg<64>::kSmemBytes));
+                CK(cudaFuncSetAttribute(nt == 1 ? (const void*)dev::bos_stream_kernel<128, 1>
+                                                : (const void*)dev::bos_stream_kernel<128, 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, dev::BosCfg<128>::kSmemBytes));
+            }
             CK(cudaFuncSetAttribute(step_fn(e), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     e->D == 32 ? dev::StepCfg<32>::kSmemBytes
                                     : e->D == 64 ? dev::StepCfg<64>::kSmemBytes
@@ -1864,10 +1869,13 @@ sinkr_status sinkr_collect_scores_batch(sinkr_engine* e, const float* queries, s
 }
 
 static void launch_bos(sinkr_engine* e, const dev::BosArgs& a) {
-#define SINKR_BOS_LAUNCH(DD)                                                                     \
-    {                                                                                            \
-        constexpr int smem = dev::BosCfg<DD>::kSmemBytes; /* attribute set at creation */     \
-        dev::bos_stream_kernel<DD><<<a.G, dev::kBosThreads, smem, e->stream>>>(e->tmk, a);       \
+#define SINKR_BOS_LAUNCH(DD)                                                                      \
+    {                                                                                             \
+        constexpr int smem = dev::BosCfg<DD>::kSmemBytes; /* attribute set at creation */      \
+        if (e->wide)                                                                              \
+            dev::bos_stream_kernel<DD, 2><<<a.G, dev::kBosThreads, smem, e->stream>>>(e->tmk, a); \
+        else                                                                                      \
+            dev::bos_stream_kernel<DD, 1><<<a.G, dev::kBosThreads, smem, e->stream>>>(e->tmk, a); \
     }
     switch (e->D) {
         case 32: SINKR_BOS_LAUNCH(32) break;
@@ -1969,7 +1977,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
             e->bos_bytes = 0;
         }
     } guard_scratch{e};
-    static_assert(dev::kBosHeads >= dev::kMaxR, "one stream pass covers a GQA group");
+    static_assert(dev::kBosHeads >= dev::kMaxRWide, "one stream pass covers a GQA group");
     // uploads (query rows, token prefix) + stream + finish [+ weights]: one graph
     auto enqueue = [&] {
         CK(cudaMemcpyAsync(e->d_in + e->off_q + q_offset * 4, e->h_in + e->off_q + q_offset * 4,
@@ -2031,7 +2039,6 @@ sinkr_status sinkr_attention_bos_mass(sinkr_engine* e, const float* queries, siz
                                       double* alpha0) {
     return guard([&] {
         if (!e || !queries || !alpha0) fail(SINKR_INVALID_ARGUMENT, "null argument");
-        if (e->wide) fail(SINKR_INVALID_ARGUMENT, "attention_bos_mass supports GQA group width <= 8");
         CK(cudaSetDevice(e->device));
         const size_t nq = e->B * e->cfg.num_q_heads * e->D;
         run_bos(e, queries, nq, 0, layer, 0, (uint32_t)e->U, alpha0, nullptr);
@@ -2042,7 +2049,6 @@ sinkr_status sinkr_attention_weights(sinkr_engine* e, const float* queries, size
                                      size_t layer, size_t kv_head, float* weights) {
     return guard([&] {
         if (!e || !queries || !weights) fail(SINKR_INVALID_ARGUMENT, "null argument");
-        if (e->wide) fail(SINKR_INVALID_ARGUMENT, "attention_weights supports GQA group width <= 8");
         check_slot(e, seq, layer, kv_head);
         CK(cudaSetDevice(e->device));
         const uint32_t u = (uint32_t)(seq * e->cfg.num_kv_heads + kv_head);

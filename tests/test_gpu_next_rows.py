@@ -244,12 +244,13 @@ def test_bos_mass_and_weights_vs_reference(ref, L, p, seed):
         assert np.abs(a0[g * r:(g + 1) * r] - rw[:, 0]).max() <= 1e-6
 
 
-@pytest.mark.parametrize("B,hq,hkv,D", [(2, 32, 4, 128), (3, 8, 8, 64), (1, 16, 4, 32), (2, 64, 8, 128)])
+@pytest.mark.parametrize("B,hq,hkv,D", [(2, 32, 4, 128), (3, 8, 8, 64), (1, 16, 4, 32), (2, 64, 8, 128),
+                                         (1, 128, 8, 128), (2, 24, 2, 64)])
 def test_bos_mass_ragged_shapes(ref, B, hq, hkv, D):
     """BOS pass over ragged slots (units of different lengths share the flat
-    token space and CTA ranges straddle units), r = 8, r = 1
-    and D = 64/32; alpha0 and weights against attention_weights
-    (attention.cpp:75-99) per group, layer 1 of 2."""
+    token space and CTA ranges straddle units), r = 8, r = 1, the two-tile
+    widths r = 16 / 12 and D = 64/32; alpha0 and weights against
+    attention_weights (attention.cpp:75-99) per group, layer 1 of 2."""
     rng = np.random.default_rng(B * 1000 + hq + D)
     r = hq // hkv
     cap = 9000
