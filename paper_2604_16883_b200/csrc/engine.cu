@@ -216,6 +216,7 @@ struct sinkr_engine {
     CUtensorMap* d_tmap = nullptr;  // device copies of tmk, tmv (fused kernel)
     cudaEvent_t ev[4] = {};
     cudaEvent_t ev_in = nullptr;
+    bool ev_in_pending = false;  // ev_in recorded since the last wait (else a wait is a no-op API call)
     bool timing = true;
     bool step_events = false;  // events around graph replays (last_step_stats step_ms)
     bool params_valid = false;
@@ -723,6 +724,14 @@ bool check_token_append(sinkr_engine* e, size_t layer) {
 
 // Validates a step (router.cpp:85-90) and stages hdr / tau / len into the
 // pinned input block; uploads them only when they changed.
+// the pinned input block is free once the last copy out of it ran (the
+// one-graph host-buffer path needs no event: the call returns after its step)
+void wait_input_block(sinkr_engine* e) {
+    if (!e->ev_in_pending) return;
+    CK(cudaEventSynchronize(e->ev_in));
+    e->ev_in_pending = false;
+}
+
 void stage_params(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg,
                   const sinkr_engine_options* opt, bool defer_upload) {
     if (!cfg) fail(SINKR_INVALID_ARGUMENT, "routing config is null");
@@ -731,7 +740,7 @@ void stage_params(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg
     o.block_size = dev::kStageTok;
     if (opt) o = *opt;
     // wait until the previous upload consumed the pinned staging block
-    CK(cudaEventSynchronize(e->ev_in));
+    wait_input_block(e);
     auto* hdr = reinterpret_cast<dev::StepHdr*>(e->h_in);
     auto* tau = reinterpret_cast<double*>(e->h_in + e->off_tau);
     auto* len = reinterpret_cast<uint32_t*>(e->h_in + e->off_len);
@@ -765,6 +774,7 @@ void stage_params(sinkr_engine* e, size_t layer, const sinkr_routing_config* cfg
     if (!defer_upload && !same) {
         CK(cudaMemcpyAsync(e->d_in, e->h_in, pbytes, cudaMemcpyHostToDevice, e->stream));
         CK(cudaEventRecord(e->ev_in, e->stream));
+        e->ev_in_pending = true;
     }
     e->last_params.assign(e->h_in, e->h_in + pbytes);
     e->params_valid = true;
@@ -1061,6 +1071,7 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaEventCreate(&e->ev_bos[0]));
             CK(cudaEventCreate(&e->ev_bos[1]));
             CK(cudaEventRecord(e->ev_in, e->stream));
+            e->ev_in_pending = true;
             CK(cudaStreamSynchronize(e->stream));
         } catch (...) {
             sinkr_engine_destroy(e);
@@ -1432,6 +1443,7 @@ static void decode_host(sinkr_engine* e, const float* queries, size_t layer,
         } else {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
             CK(cudaEventRecord(e->ev_in, e->stream));
+            e->ev_in_pending = true;
             float* d_out = reinterpret_cast<float*>(e->d_res);
             run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), d_out, mode);
             CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
@@ -1521,6 +1533,7 @@ sinkr_status sinkr_decode_append_step(sinkr_engine* e, const float* queries, con
         } else {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes_append, cudaMemcpyHostToDevice, e->stream));
             CK(cudaEventRecord(e->ev_in, e->stream));
+            e->ev_in_pending = true;
             const float* kn = reinterpret_cast<const float*>(e->d_in + e->off_kvn);
             launch_append(e, layer, kn, kn + e->U * D);
             run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q), reinterpret_cast<float*>(e->d_res), 0);
@@ -1553,7 +1566,7 @@ sinkr_status sinkr_group_attention(sinkr_engine* e, const float* group_queries, 
                                              std::to_string(L));
         const size_t H = e->cfg.num_kv_heads, Hq = e->cfg.num_q_heads, r = e->r, D = e->D;
         const size_t u = seq * H + kv_head, row0 = (seq * Hq + kv_head * r) * D;
-        CK(cudaEventSynchronize(e->ev_in));
+        wait_input_block(e);
         auto* hdr = reinterpret_cast<dev::StepHdr*>(e->h_in);
         auto* tau = reinterpret_cast<double*>(e->h_in + e->off_tau);
         auto* len = reinterpret_cast<uint32_t*>(e->h_in + e->off_len);
@@ -1583,6 +1596,7 @@ sinkr_status sinkr_group_attention(sinkr_engine* e, const float* group_queries, 
         } else {
             CK(cudaMemcpyAsync(e->d_in, e->h_in, e->in_bytes, cudaMemcpyHostToDevice, e->stream));
             CK(cudaEventRecord(e->ev_in, e->stream));
+            e->ev_in_pending = true;
             run_graph(e, reinterpret_cast<const float*>(e->d_in + e->off_q),
                       reinterpret_cast<float*>(e->d_res), 0);
             CK(cudaMemcpyAsync(e->h_res, e->d_res, e->res_bytes, cudaMemcpyDeviceToHost, e->stream));
@@ -1938,7 +1952,7 @@ static void run_bos(sinkr_engine* e, const float* queries, size_t q_floats, size
         CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->h_bos_dev), e->h_bos, 0));
         e->h_bos_bytes = h_need;
     }
-    CK(cudaEventSynchronize(e->ev_in));  // the input block is free
+    wait_input_block(e);  // the input block is free
     std::memcpy(e->h_in + e->off_q + q_offset * 4, queries, q_floats * 4);
     std::memcpy(e->h_bos, pre.data(), (n_units + 1) * 4);
     const uint32_t parity = e->bos_parity;
