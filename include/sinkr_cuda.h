@@ -255,7 +255,9 @@ sinkr_status sinkr_merge_rank_partials_async(sinkr_engine* e, const float* d_gat
  *   sinkr_peer_set_blocks  same, from device pointers (ranks in one process)
  * All ranks must issue the same number of peer steps (the step tags count
  * them); a rank that never delivers turns into a step-kernel error after
- * 2 s (NaN outputs), never a hang. */
+ * 2 s (NaN outputs), never a hang, and the exchange refuses further steps
+ * until every rank calls sinkr_peer_setup again (which resets it: a fresh
+ * block, step tags from zero) and connects again. */
 sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, size_t* block_bytes);
 sinkr_status sinkr_peer_ipc_handle(sinkr_engine* e, void* handle);
 sinkr_status sinkr_peer_open(sinkr_engine* e, const void* handles);

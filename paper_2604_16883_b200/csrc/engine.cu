@@ -2113,10 +2113,11 @@ sinkr_status sinkr_peer_setup(sinkr_engine* e, uint32_t world, uint32_t rank, si
             fail(SINKR_INVALID_ARGUMENT, "peer merge needs 1 <= world <= 8 and rank < world");
         if (!e->fused) fail(SINKR_INVALID_ARGUMENT, "peer merge needs the fused step kernel");
         CK(cudaSetDevice(e->device));
-        if (e->d_xchg && !e->peer_poisoned) fail(SINKR_LOGIC_ERROR, "peer merge already set up");
         if (e->d_xchg) {
-            // after a watchdog timeout: a fresh exchange block and step
-            // tags from zero; every rank sets up and connects again
+            // set up again (after a watchdog timeout every rank must): a
+            // fresh, zeroed exchange block and step tags from zero, so no
+            // word of an earlier step can carry a valid tag; every rank then
+            // connects again
             CK(cudaStreamSynchronize(e->stream));
             for (auto& kv : e->graphs) {
                 cudaGraphExecDestroy(kv.second.exec);

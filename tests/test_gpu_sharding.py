@@ -276,3 +276,50 @@ def test_peer_host_buffer_step_world1(timing):
                 pm.step(dq, dout, cfg, P.EngineOptions())
                 torch.cuda.synchronize()
                 assert (dout.cpu().numpy() - ref.outputs).__abs__().max() <= 1e-6
+
+
+def test_peer_merge_watchdog_and_reconnect(monkeypatch):
+    """A rank that never delivers: the other rank's fused-merge step ends with
+    the peer-merge watchdog error after ~2 s (NaN in the outputs it owns,
+    never a hang), the exchange then refuses steps, and after every rank sets
+    it up again and reconnects a two-rank step matches the unsharded step."""
+    import time
+
+    from paper_2604_16883_b200 import sharding
+    from paper_2604_16883_b200._abi import LogicError
+
+    monkeypatch.setenv("SINKR_DEBUG_GRID", "74")
+    L = 16384
+    spec = WorkloadSpec(length=L, sink_fraction=0.5, seed=9)
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    q = torch.from_numpy(spec.queries()[0]).cuda()
+    with P.KvCache(P.CacheConfig(1, 32, 8, 128, L)) as full:
+        spec.fill(full)
+        ref = torch.empty_like(q)
+        P.routed_decode_async(q.data_ptr(), 0, full, cfg, d_outputs=ref.data_ptr())
+        torch.cuda.synchronize()
+    shards = [sharding.build_sequence_shard(P, spec, k, 2, 0)[0] for k in range(2)]
+    try:
+        pms = sharding.peer_merge_in_process(P, shards)
+        opts = P.EngineOptions(global_context_len=L)
+        out = torch.zeros_like(q)
+        t0 = time.time()
+        pms[0].step(q, out, cfg, opts)  # rank 1 never steps
+        torch.cuda.synchronize()
+        assert 1.5 < time.time() - t0 < 60
+        with pytest.raises(RuntimeError, match="peer merge watchdog"):
+            P.fetch_step_info(shards[0])
+        assert torch.isnan(out).any()
+        with pytest.raises(LogicError):
+            pms[0].step(q, out, cfg, opts)
+        pms = sharding.peer_merge_in_process(P, shards)  # every rank: set up again, reconnect
+        outs = [torch.empty_like(q) for _ in range(2)]
+        for _ in range(2):
+            for pm, o in zip(pms, outs):
+                pm.step(q, o, cfg, opts)
+            torch.cuda.synchronize()
+            for o in outs:
+                assert (o - ref).abs().max().item() <= 2e-3
+    finally:
+        for s_ in shards:
+            s_.close()
