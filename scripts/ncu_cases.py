@@ -26,6 +26,7 @@ CASES = {
     "c1routed": dict(length=32768, tau=0.5),
     "c1dense": dict(length=32768, tau=2.0),
     "c4routed": dict(length=524288, tau=0.5, hq=64),
+    "wide512kdense": dict(length=524288, tau=2.0, hq=128),  # GQA width 16 (WIDE)
 }
 
 case = CASES[sys.argv[1]]
