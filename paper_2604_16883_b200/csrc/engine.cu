@@ -197,6 +197,7 @@ struct sinkr_engine {
     float bos_ms = -1.f;
     size_t h_bos_bytes = 0;
     uint32_t* d_ovf = nullptr;          // spill-slot lock + valid per unit [2][U]
+    uint32_t* d_route_sum = nullptr;    // [grid] per-CTA Active bitmasks (distributed routing)
     uint32_t* d_spec_mask = nullptr;    // [layers] Active bitmask of each layer's last single-sequence step
     uint32_t* d_cta_epoch = nullptr;    // [2][grid]: step-kernel launches, mode-3 steps per CTA slot
     unsigned long long* d_trace = nullptr;  // SINKR_TRACE=1: per-CTA phase stamps
@@ -292,6 +293,7 @@ struct sinkr_engine {
         t.slot_count = d_slot_count;
         t.tokens_done = d_tokens_done;
         t.route_flags = d_route_flags;
+        t.route_sum = d_route_sum;
         t.ovf = d_ovf;
         t.cta_epoch = d_cta_epoch;
         t.partials = d_partials;
@@ -983,6 +985,7 @@ sinkr_status sinkr_engine_create(const sinkr_cache_config* config, int device,
             CK(cudaMalloc(&e->d_ovf, 2 * e->U * 4));
             CK(cudaMemsetAsync(e->d_ovf, 0, 2 * e->U * 4, e->stream));
             CK(cudaMemsetAsync(e->d_tokens_done, 0, 2 * e->U * 4, e->stream));
+            CK(cudaMalloc(&e->d_route_sum, e->grid * 4));
             CK(cudaMalloc(&e->d_spec_mask, e->layers * 4));
             CK(cudaMemsetAsync(e->d_spec_mask, 0, e->layers * 4, e->stream));
             CK(cudaMalloc(&e->d_cta_epoch, 2 * e->grid * 4));  // launches, mode-3 steps
@@ -1114,6 +1117,7 @@ sinkr_status sinkr_engine_destroy(sinkr_engine* e) {
     cudaFree(e->d_ovf);
     cudaFree(e->d_cta_epoch);
     cudaFree(e->d_spec_mask);
+    cudaFree(e->d_route_sum);
     cudaFree(e->d_head_degen);
     cudaFree(e->d_active);
     cudaFree(e->d_prefix);

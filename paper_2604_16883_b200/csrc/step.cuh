@@ -84,6 +84,7 @@ struct StepTables {
     double* group_scores;          // result [U]
     uint32_t* unit_flags;          // result [U]
     uint32_t* route_flags;         // [U] device scratch: decisions for the distributed routing
+    uint32_t* route_sum;           // [grid] distributed routing: each CTA's Active bitmask of its units
     unsigned long long* tokens;    // result [U] rows streamed (the skipped-block record)
     uint32_t* status;              // result: nonzero = partial-slot overflow
     StepState* ss;
@@ -865,6 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }  // !exact_later
 
         // group_score + route (router.cpp:50-57,67-75,113-120) of this CTA's units
+        bool my_act = false;  // (up <= 32: thread i decides unit u_lo + i)
         for (uint32_t u = u_lo + tid; u < u_hi; u += kThreads) {
             const uint32_t seq = u / t.Hkv;
             const uint32_t hb = (u - u_lo) * r;
@@ -889,6 +891,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool active = (flags & kObserveOnly) || !sink;
             force_route(p.only_unit, u, sink, active);
             const uint32_t fl = (sink ? kSink : 0u) | (degen ? kDegenerate : 0u) | (active ? kActive : 0u);
+            my_act = active;
             t.route_flags[u] = fl;
             if (!exact_later) t.group_scores[u] = S;
             t.unit_flags[u] = fl;
@@ -906,6 +909,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!exact_later)
             for (uint32_t h = h_lo + tid; h < h_hi; h += kThreads) t.head_scores[h] = s_score[h - h_lo];
+        // this CTA's decisions as one word (bit i: unit u_lo + i Active), so
+        // every CTA reads one word per CTA after the barrier, not one per unit
+        const bool use_sum = up <= 32u;
+        if (use_sum && warp == 0) {
+            const uint32_t m = __ballot_sync(0xffffffffu, my_act && tid < u_hi - u_lo);
+            if (lane == 0) t.route_sum[bid] = m;
+        }
         STAMP(14);
         // grid barrier: every unit's decision is published (cooperative launch,
         // all CTAs resident; a 2 s watchdog turns a bug into an error, not a hang)
@@ -927,14 +937,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         // the Active list from the published decisions: contiguous unit runs
         // per thread, then an order-preserving scan.
-        const uint32_t per = (U + kThreads - 1) / kThreads;
+        // With the per-CTA words, thread t takes CTA t's units (one load);
+        // else contiguous runs of per-unit flags.
+        const uint32_t per = use_sum ? up : (U + kThreads - 1) / kThreads;
         const uint32_t u0 = min(U, tid * per), u1 = min(U, u0 + per);
         uint32_t my_active = 0;
         unsigned long long my_tok = 0;
         uint64_t my_bits = 0;  // active bits of this thread's run (per <= 64 guaranteed)
-        // all of this thread's flags in flight at once (runs are <= 8 units for
-        // U <= 1280), then the bookkeeping
-        for (uint32_t ub = u0; ub < u1; ub += 8) {
+        if (use_sum && u0 < u1) {
+            const uint32_t m = __ldcg(&t.route_sum[tid]);
+            my_bits = m;
+            my_active = __popc(m);
+            for (uint32_t b = m; b; b &= b - 1u) my_tok += s_len[(u0 + __ffs(b) - 1) / t.Hkv];
+        }
+        // (per-unit flags: all of this thread's flags in flight at once, runs
+        // are <= 8 units for U <= 1280, then the bookkeeping)
+        for (uint32_t ub = u0; !use_sum && ub < u1; ub += 8) {
             uint32_t fl[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) fl[k] = (ub + k < u1) ? __ldcg(&t.route_flags[ub + k]) : 0u;
