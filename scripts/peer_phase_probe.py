@@ -1,6 +1,6 @@
 """Dev tool: what the fused peer merge (step mode 3) adds over a plain routed
 step, at world 1 in one process: back-to-back step time and the per-CTA trace
-(stream end, merge end, last-CTA reset).  LEN = tokens on this rank."""
+(stream end, merge end).  LEN = tokens on this rank."""
 import ctypes as C
 import os
 import sys
@@ -59,5 +59,4 @@ for name, fn in (("plain", plain), ("peer", peer)):
     t0 = a[:, 4].min()
     rel = lambda x: (x - t0) / 1e3
     print(f"{name:5s} L={L}: back-to-back {b2b:.2f} us; stream end max {rel(a[:, 1]).max():.2f}; "
-          f"merge end max {rel(a[:, 2]).max():.2f}; reset {rel(a[:, 5][a[:, 5] > 0]).max():.2f}; "
-          f"lead CTA cycles stream-end->merge-end {sv[10] - sv[9]}, merge-end->exit {sv[11] - sv[10]}")
+          f"merge end max {rel(a[:, 2]).max():.2f} us")
