@@ -557,6 +557,52 @@ def shard_projection(P, torch, args, spec_cls, dense_cfg, routed_cfg, peak):
                                  "multi-GPU measurement: the stores to 7 NVLink peers are not in it"}
 
 
+def model_decode(P, torch, args, spec_cls, peak, layers=32, L=131072):
+    """Decode attention of one token through a whole Llama-3.1-8B-shaped
+    model: `layers` layers of KV at context L in ONE engine (32 x 512 MiB of
+    bf16 KV at 128K), one routed step per layer back to back (each layer's KV
+    is cold for its step: 16 GiB against a 126 MB L2), the reference's default
+    excluded layers {0, 1} (never skipped) vs the dense path; ms per token."""
+    out = {"layers": layers, "context": L}
+    with P.KvCache(P.CacheConfig(layers, 32, 8, 128, L)) as cache:
+        specs = [spec_cls(**SHAPE, num_layers=layers, layer=l, length=L, sink_fraction=args.sink_fraction,
+                          seed=args.seed + l) for l in range(layers)]
+        for sp in specs:
+            sp.fill(cache)
+        P.set_timing(cache, False)
+        dq = [torch.from_numpy(sp.queries()[0]).cuda() for sp in specs]
+        dout = [torch.empty_like(x) for x in dq]
+        st = torch.cuda.ExternalStream(cache.stream)
+        routed = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5))  # excluded layers (0, 1)
+        dense = P.RoutingConfig(profile=P.ThresholdProfile.constant(2.0))
+        for name, cfg in (("routed", routed), ("dense", dense)):
+            def token():
+                for l in range(layers):
+                    P.routed_decode_async(dq[l].data_ptr(), l, cache, cfg, d_outputs=dout[l].data_ptr())
+
+            for _ in range(2):
+                token()
+            torch.cuda.synchronize()
+            gate(torch, st, 20.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(5):
+                token()
+            e1.record(st)
+            torch.cuda.synchronize()
+            out[f"{name}_ms_per_token"] = round(e0.elapsed_time(e1) / 5, 4)
+            P.fetch_step_info(cache)  # raises on any step-kernel error
+    act_routed = 2 * 8 + (layers - 2) * (8 - int(args.sink_fraction * 8))
+    kv_tok = act_routed * 2 * L * 128 * 2
+    out["active_groups_per_token_routed"] = act_routed
+    out["speedup_vs_dense"] = round(out["dense_ms_per_token"] / out["routed_ms_per_token"], 3)
+    out["kv_gbs_routed"] = round(kv_tok / (out["routed_ms_per_token"] * 1e-3) / 1e9, 1)
+    out["note"] = ("one token's decode attention over all layers, steps launched back to back on the "
+                   "engine stream (graph replays); routed = tau 0.5 with the reference's default excluded "
+                   "layers {0, 1}; KV GB/s = Active K+V bytes of the token / its time")
+    return out
+
+
 def next_rows(P, torch, args, spec_cls, peak):
     """The §8 "next" rows measured beside the hot path, each against the
     compiled reference on this host: f1 GPU score collection (routing phase
@@ -946,6 +992,10 @@ def run_ours(args, world, rank, local_rank):
                                                                routed_cfg, peak)
         except Exception as e:  # report, never lose the headline line
             line["sharded_8way_projection"] = {"failed": f"{type(e).__name__}: {e}"}
+        try:
+            line["model_decode_32_layers"] = model_decode(P, torch, args, WorkloadSpec, peak)
+        except Exception as e:
+            line["model_decode_32_layers"] = {"failed": f"{type(e).__name__}: {e}"}
         try:
             line["next_rows"] = next_rows(P, torch, args, WorkloadSpec, peak)
         except Exception as e:  # reported, never silently dropped
