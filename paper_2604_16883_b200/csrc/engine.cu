@@ -431,18 +431,21 @@ void launch_step(sinkr_engine* e, const dev::StepTables& st) {
     cfg.dynamicSmemBytes = dev::StepCfg<D>::kSmemBytes;
     cfg.stream = e->stream;
     // cooperative: the merge phase waits on other CTAs, so all must be resident
-    // (SINKR_STEP_LAUNCH=1 plain, =2 programmatic serialization: A/B knobs)
-    cudaLaunchAttribute attr[1];
+    // (SINKR_STEP_LAUNCH=1 plain, =2 programmatic serialization, =3 both
+    // cooperative and programmatic: A/B knobs)
+    cudaLaunchAttribute attr[2];
     const int lm = step_launch_mode();
-    if (lm == 2) {
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-    } else {
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = lm == 0 ? 1 : 0;
+    int na = 0;
+    if (lm == 0 || lm == 1 || lm == 3) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na++].val.cooperative = lm == 1 ? 0 : 1;
+    }
+    if (lm >= 2) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
     }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     CK(cudaLaunchKernelEx(&cfg, step_fn_d<D>(e), st, e->pp));
 }
 
