@@ -25,6 +25,15 @@
 // The cross-CTA counters come in two sets used by alternate launches (each
 // launch zeroes its successor's set), so the launch needs no memset and
 // replays as a single graph node.
+//
+// Instantiations: <D, LEAN, WIDE>.  LEAN = single-sequence shapes (routing
+// in every CTA, its scratch in the idle flush staging so the ring is free);
+// WIDE = GQA width 9-16 (each consumer warp takes one 8-head tile and 32
+// tokens per stage).  Single-sequence steps also (a) let CTA G-1 dry-run the
+// stream/flush/merge code before routing so a cold step finds it in L2
+// ("code prewarm"), and (b) prefetch each CTA's first static stages into L2
+// under the layer's previous Active set while warp 0 routes ("speculative
+// prefetch"); both are hints that never change a result.
 #pragma once
 
 #include "kernels.cuh"
