@@ -55,6 +55,30 @@ def test_collect_scores_bit_exact(ref):
     assert not sink0.any()
 
 
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (128, 8)])
+def test_collect_scores_batch_vs_reference(ref, hq, hkv):
+    """Batched score collection against the compiled reference's
+    routed_decode_step scores directly, per sample (r = 4 and the WIDE r = 16)."""
+    spec = WorkloadSpec(num_q_heads=hq, num_kv_heads=hkv, length=2000, sink_fraction=0.5, seed=15)
+    k, v = spec.host_cache(0)
+    rng = np.random.default_rng(hq)
+    qs = np.stack([spec.queries()[0]] + [rng.standard_normal((hq, 128)).astype(np.float32) * 3
+                                          for _ in range(4)])
+    cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(0.5), excluded_layers=())
+    with P.KvCache(P.CacheConfig(1, hq, hkv, 128, spec.length)) as cache:
+        spec.fill(cache)
+        hb, gb, sb = cal.collect_scores_batch(cache, qs, 0, cfg)
+    rc = oracle.RefCache(oracle.ref(), 1, hq, hkv, 128, spec.length)
+    for g in range(hkv):
+        rc.append_rows(0, g, k[g], v[g])
+    for i, q in enumerate(qs):
+        r = rc.routed_decode_step(q, 0, oracle.Profile.constant(0.5), excluded=())
+        assert hb[i].tobytes() == r.head_scores.tobytes()
+        assert gb[i].tobytes() == r.group_scores.tobytes()
+        assert np.array_equal(sb[i], r.sink.astype(bool))
+    rc.close()
+
+
 @pytest.mark.parametrize("hq,hkv,D,B", [(32, 8, 128, 1), (40, 8, 64, 2), (8, 8, 32, 3), (64, 8, 128, 1),
                                          (35, 7, 128, 1), (128, 8, 128, 1), (24, 2, 64, 2)])
 def test_collect_scores_batch_matches_single(hq, hkv, D, B):
