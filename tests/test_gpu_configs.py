@@ -147,3 +147,30 @@ def read_back_shard(cache, spec, rows):
         ks.append(k)
         vs.append(v)
     return np.stack(ks), np.stack(vs)
+
+
+def test_wide_gqa_405b_shape_vs_compiled_reference(oracle_libs):
+    """GQA width 16 (Llama-3.1-405B attention: 128 q / 8 KV heads, D = 128) at
+    64K on the WIDE step kernel, against the reference's own routed_decode_step
+    (oracle/_ref): bitmap and group scores bit-exact, loaded floats equal,
+    outputs within the bar."""
+    ref_lib, _ = oracle_libs
+    if ref_lib is None:
+        pytest.skip("oracle/_ref not built")
+    spec = WorkloadSpec(num_q_heads=128, num_kv_heads=8, length=65536, sink_fraction=0.5, seed=405)
+    q = spec.queries()[0]
+    with P.KvCache(P.CacheConfig(1, 128, 8, 128, spec.length)) as cache:
+        spec.fill(cache)
+        res = P.routed_decode_step(q, 0, cache, CFG)
+        rc = oracle.RefCache(ref_lib, 1, 128, 8, 128, spec.length)
+        for g in range(8):
+            k, v = cache.historical(0, g, 0, spec.length)
+            rc.append_rows(0, g, k, v)
+            del k, v
+    ref = rc.routed_decode_step(q, 0, oracle.Profile.constant(0.5), excluded=(), workers=16)
+    rc.close()
+    assert np.array_equal(res.route_bitmap.astype(np.int32), ref.sink) and ref.sink.sum() == 4
+    assert np.array([g.decision.group_score for g in res.groups]).tobytes() == ref.group_scores.tobytes()
+    assert res.counters.kv_floats_loaded == ref.counters["kv_floats_loaded"]
+    assert np.abs(res.outputs - ref.outputs).max() <= 2e-3
+    assert np.linalg.norm(res.outputs - ref.outputs) <= 1e-3 * np.linalg.norm(ref.outputs)
