@@ -2,6 +2,8 @@
 
     python scripts/ncu_cases.py CASE        # CASE: routed512k dense512k peer64k c1routed c1dense
                                             #       c4routed (70B shape, 512K)
+                                            #       c3routed / c5routed (batched: Yi-9B 200K B=16,
+                                            #       LLaVA-13B 8K B=32), wide512krouted (r = 16)
 
 Runs WARM (default 4) untimed steps, then 2 more; capture the last with
     ncu --set full --clock-control none --import-source on -k regex:step_kernel \
@@ -27,18 +29,22 @@ CASES = {
     "c1dense": dict(length=32768, tau=2.0),
     "c4routed": dict(length=524288, tau=0.5, hq=64),
     "wide512kdense": dict(length=524288, tau=2.0, hq=128),  # GQA width 16 (WIDE)
+    "wide512krouted": dict(length=524288, tau=0.5, hq=128),
+    # batched steps: distributed routing, flat / unit-affine schedules
+    "c3routed": dict(length=204800, tau=0.5, hq=32, hkv=4, seqs=16),
+    "c5routed": dict(length=8192, tau=0.5, hq=40, hkv=40, seqs=32, image=576),
 }
 
 case = CASES[sys.argv[1]]
 warm = int(os.environ.get("WARM", 4))
-hq = case.get("hq", 32)
-spec = WorkloadSpec(num_q_heads=hq, num_kv_heads=8, head_dim=128, length=case["length"],
-                    sink_fraction=0.625)
+hq, hkv, seqs = case.get("hq", 32), case.get("hkv", 8), case.get("seqs", 1)
+spec = WorkloadSpec(num_q_heads=hq, num_kv_heads=hkv, head_dim=128, length=case["length"],
+                    num_seqs=seqs, image_tokens=case.get("image", 0), sink_fraction=0.625)
 cfg = P.RoutingConfig(profile=P.ThresholdProfile.constant(case["tau"]), excluded_layers=())
-cache = P.KvCache(P.CacheConfig(1, hq, 8, 128, case["length"]))
+cache = P.KvCache(P.CacheConfig(1, hq, hkv, 128, case["length"], seqs))
 spec.fill(cache)
 P.set_timing(cache, False)
-q = torch.from_numpy(spec.queries()[0]).cuda()
+q = torch.from_numpy(spec.queries() if seqs > 1 else spec.queries()[0]).cuda()
 out = torch.empty_like(q)
 if case.get("peer"):
     (pm,) = sharding.peer_merge_in_process(P, [cache])
