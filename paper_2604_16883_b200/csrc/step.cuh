@@ -179,6 +179,23 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 // weights 2^(m_j - max) reach the lanes by shuffle.  One L2 round trip per 64
 // partials.  Writes the normalised row (mode 0), an un-normalised rank partial
 // (mode 1), or that partial into every rank's exchange block (mode 3).
+// Slots past the count enter warp_merge's FMA chains with weight 0.  A
+// non-finite value left there by an earlier step (a NaN query, an inf K/V
+// row) would make 0 * x NaN, so a non-finite merge result is recomputed over
+// the count's slots only: this step's own non-finite partials stay NaN, an
+// earlier step's do not leak into it.  Rare, so out of line.
+template <int D, int R>
+__device__ __noinline__ float merge_valid_slots(const float* base, uint32_t n, uint32_t h, uint32_t d, float mx) {
+    constexpr uint32_t PS = R * (D + 2);
+    float acc = 0.f;
+    for (uint32_t j = 0; j < n; ++j) {
+        const float m = __ldcg(base + size_t(j) * PS + h);
+        const float w = m == -INFINITY ? 0.f : ptx::ex2(m - mx);
+        acc = fmaf(__ldcg(base + size_t(j) * PS + 2 * R + h * D + d), w, acc);
+    }
+    return acc;
+}
+
 template <int D, int R>
 __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint32_t h, uint32_t d0,
                                            uint32_t lane, size_t xoff, uint32_t tag, float* wsm, bool dry) {
@@ -243,9 +260,9 @@ __device__ __forceinline__ void warp_merge(const StepTables& t, uint32_t u, uint
         acc += (a4[0] + a4[1]) + (a4[2] + a4[3]);
         __syncwarp();  // scratch reused by the next group / task
     }
-    if (dry) {
-        return;
-    } else if (t.mode == 0) {
+    if (dry) return;
+    if (!isfinite(acc)) acc = merge_valid_slots<D, R>(base, n, h, d, mx);
+    if (t.mode == 0) {
         t.out[(size_t(u) * r + h) * D + d] = acc / lsum;
     } else if (t.mode == 1) {
         float* P = t.out + size_t(u) * PS;
