@@ -57,3 +57,32 @@ def test_nan_query_does_not_poison_later_steps(hq):
             err = float((got - ref).abs().max())
             assert err <= 1e-5, (tau, err)
 
+
+
+def test_nan_query_does_not_poison_later_batched_steps():
+    # batched (distributed routing, flat token-space schedule: more Active
+    # groups than SMs, the last flusher merges): NaN heads in one step, then
+    # clean steps with another routing
+    spec = WorkloadSpec(num_q_heads=40, num_kv_heads=40, num_seqs=6, length=3000,
+                        sink_fraction=0.5, seed=13)
+    n = spec.num_seqs * spec.num_q_heads
+    with P.KvCache(P.CacheConfig(1, 40, 40, 128, spec.length, spec.num_seqs)) as cache:
+        spec.fill(cache)
+        P.set_timing(cache, False)
+        q = torch.from_numpy(spec.queries().reshape(n, 128)).cuda()
+        out = torch.empty_like(q)
+
+        def step(qq, tau):
+            P.routed_decode_async(qq.data_ptr(), 0, cache, _cfg(tau), d_outputs=out.data_ptr())
+            torch.cuda.synchronize()
+            return out.clone()
+
+        refs = {tau: step(q, tau) for tau in (2.0, 0.5)}
+        assert all(torch.isfinite(x).all() for x in refs.values())
+        bad = q.clone()
+        bad[::7] = float("nan")
+        step(bad, 2.0)
+        for tau in (0.5, 2.0, 0.5):
+            got = step(q, tau)
+            assert torch.isfinite(got).all(), f"tau={tau}: non-finite outputs after a NaN step"
+            assert float((got - refs[tau]).abs().max()) <= 1e-5
