@@ -751,7 +751,20 @@ def run_ours(args, world, rank, local_rank):
                 port = sk.getsockname()[1]
             os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
                               MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        # stdout carries only the JSON line: NCCL prints "NCCL version ..." to
+        # stdout when the communicator is created (NCCL_DEBUG=VERSION on the GPU
+        # boxes), so fd 1 points at stderr while the process group comes up
+        # (device_id: the communicator is created here, not at the first collective)
+        sys.stdout.flush()
+        saved_fd = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved_fd, 1)
+            os.close(saved_fd)
     L = args.length
     D = SHAPE["head_dim"]
     spec = WorkloadSpec(**SHAPE, length=L, sink_fraction=args.sink_fraction, seed=args.seed)
